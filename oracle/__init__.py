@@ -1,0 +1,187 @@
+"""CPU oracle for the tca hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
+--impl reference) may import this package.  The product package
+(paper_1001_5460_b200) never imports it and shares no code with it.
+
+The arithmetic is in tca_oracle.c (plain C loops, fp64); this module only
+builds it with gcc, loads it with ctypes and marshals numpy arrays.  Every
+function cites the passage of PAPER.md it follows (see the C file header).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "tca_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+OK, BREAKDOWN, NONFINITE, NOT_CONVERGED = 0, 7, 8, 9
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+def build(force: bool = False) -> str:
+    """Compile tca_oracle.c -> liboracle.so (gcc -O2 -fopenmp)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-Wall",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB)
+            L.orc_gram.argtypes = [ctypes.c_int64, ctypes.c_int64, _dp, _dp]
+            L.orc_transpose.argtypes = [ctypes.c_int64, ctypes.c_int64, _dp, _dp]
+            L.orc_mode_product.argtypes = [ctypes.c_int, _i64p, _dp, ctypes.c_int,
+                                           ctypes.c_int64, _dp, _dp]
+            L.orc_apply.argtypes = [ctypes.c_int, _i64p, ctypes.POINTER(_dp),
+                                    ctypes.POINTER(_dp), ctypes.c_double, _dp, _dp]
+            L.orc_rhs.argtypes = [ctypes.c_int, _i64p, _i64p, ctypes.POINTER(_dp), _dp, _dp]
+            L.orc_apply_point.argtypes = [ctypes.c_int, _i64p, ctypes.POINTER(_dp),
+                                          ctypes.POINTER(_dp), ctypes.c_double, _dp, _i64p]
+            L.orc_apply_point.restype = ctypes.c_double
+            L.orc_rhs_point.argtypes = [ctypes.c_int, _i64p, _i64p, ctypes.POINTER(_dp),
+                                        _dp, _i64p]
+            L.orc_rhs_point.restype = ctypes.c_double
+            L.orc_dot.argtypes = [ctypes.c_int64, _dp, _dp]
+            L.orc_dot.restype = ctypes.c_double
+            L.orc_cg.argtypes = [ctypes.c_int, _i64p, ctypes.POINTER(_dp), ctypes.POINTER(_dp),
+                                 ctypes.c_double, _dp, _dp, ctypes.c_double, ctypes.c_int, _dp,
+                                 ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+            L.orc_cg.restype = ctypes.c_int
+            L.orc_num_threads.restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a):
+    return a.ctypes.data_as(_dp)
+
+
+def _i64(v):
+    a = np.ascontiguousarray(v, dtype=np.int64)
+    return a, a.ctypes.data_as(_i64p)
+
+
+def _ptr_array(mats):
+    arr = (_dp * len(mats))()
+    for i, M in enumerate(mats):
+        arr[i] = ctypes.cast(None, _dp) if M is None else _p(M)
+    return arr
+
+
+def num_threads() -> int:
+    return lib().orc_num_threads()
+
+
+def gram(A) -> np.ndarray:
+    """G = A^T A by explicit loops."""
+    A = _f64(A)
+    m, n = A.shape
+    G = np.empty((n, n))
+    lib().orc_gram(m, n, _p(A), _p(G))
+    return G
+
+
+def mode_product(X, d: int, M) -> np.ndarray:
+    """Y = X x_d M (Eq. 4 one-dimensional transformation along mode d)."""
+    X, M = _f64(X), _f64(M)
+    s = list(X.shape)
+    rows = M.shape[0]
+    assert M.shape[1] == s[d]
+    out_shape = s.copy()
+    out_shape[d] = rows
+    Y = np.empty(out_shape)
+    sa, sp = _i64(s)
+    lib().orc_mode_product(len(s), sp, _p(X), d, rows, _p(M), _p(Y))
+    return Y
+
+
+class Operator:
+    """M = (kron_d G_d) + lam * sum_d (mode-d R_d), G_d = A_d^T A_d, R_d = L_d^T L_d.
+
+    A: list of m_d x n_d arrays; L: list of (n_d-2) x n_d arrays or None.
+    """
+
+    def __init__(self, A, L=None, lam=0.0):
+        self.A = [_f64(a) for a in A]
+        self.D = len(self.A)
+        self.n = tuple(a.shape[1] for a in self.A)
+        self.m = tuple(a.shape[0] for a in self.A)
+        self.lam = float(lam)
+        self.G = [gram(a) for a in self.A]
+        if L is None:
+            self.R = [None] * self.D
+        else:
+            self.R = [None if (l is None or l.shape[0] == 0) else gram(l) for l in L]
+        self._na, self._np = _i64(self.n)
+        self._ma, self._mp = _i64(self.m)
+        self._G = _ptr_array(self.G)
+        self._R = _ptr_array(self.R)
+        self._A = _ptr_array(self.A)
+
+    @property
+    def N(self):
+        return int(np.prod(self.n))
+
+    def apply(self, x) -> np.ndarray:
+        x = _f64(x).reshape(self.n)
+        y = np.empty(self.n)
+        lib().orc_apply(self.D, self._np, self._G, self._R, self.lam, _p(x), _p(y))
+        return y
+
+    def rhs(self, ydata) -> np.ndarray:
+        ydata = _f64(ydata).reshape(self.m)
+        b = np.empty(self.n)
+        lib().orc_rhs(self.D, self._np, self._mp, self._A, _p(ydata), _p(b))
+        return b
+
+    def apply_point(self, x, idx) -> float:
+        x = _f64(x)
+        ia, ip = _i64(idx)
+        return lib().orc_apply_point(self.D, self._np, self._G, self._R, self.lam, _p(x), ip)
+
+    def apply_points(self, x, idxs) -> np.ndarray:
+        x = _f64(x)
+        return np.array([self.apply_point(x, i) for i in np.atleast_2d(idxs)])
+
+    def rhs_point(self, ydata, idx) -> float:
+        ydata = _f64(ydata)
+        ia, ip = _i64(idx)
+        return lib().orc_rhs_point(self.D, self._np, self._mp, self._A, _p(ydata), ip)
+
+    def cg(self, b, rtol: float, max_iters: int):
+        """Fig. 2 CG from x0 = 0.  Returns (x, iters, status, rho_history)."""
+        b = _f64(b).reshape(self.n)
+        x = np.empty(self.n)
+        hist = np.zeros(max_iters + 1)
+        it = ctypes.c_int(0)
+        rf = ctypes.c_double(0.0)
+        st = lib().orc_cg(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(x),
+                          float(rtol), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
+        return x, it.value, st, hist[: it.value + 1]
+
+
+def dot(a, b) -> float:
+    a, b = _f64(a).ravel(), _f64(b).ravel()
+    assert a.size == b.size
+    return lib().orc_dot(a.size, _p(a), _p(b))

@@ -1,0 +1,363 @@
+/*
+ * tca_oracle.c -- plain, slow, obviously-correct CPU oracle (fp64).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product (paper_1001_5460_b200/,
+ * include/, the CUDA library) may include, link or call this file.  Only
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg use it.  It shares no code, header, table or constant with the
+ * CUDA path.
+ *
+ * What it computes (arxiv 1001.5460, PAPER.md line numbers):
+ *   G_d = A_d^T A_d, R_d = L_d^T L_d      A.7 "patterns like A^T A from matrix
+ *                                          normal equations"
+ *   apply  y = (G_1 x ... x G_D) x + lam * sum_d (I x .. R_d .. x I) x
+ *          Eq. 4 separable transformation as successive one-dimensional
+ *          products, Eq. 9's Kronecker sum for the
+ *          regulariser; operator per BASELINE.json configs.
+ *   rhs    b = (A_1^T x ... x A_D^T) y   (Eq. 4 with rectangular factors,
+ *          Table 1 up/down-sampling row)
+ *   dot    <a,b> = sum a o b              Eq. A13/A14
+ *   CG     Fig. 2 step by step with readings Z1 (loop
+ *          guard erratum), Z2 (relative threshold on rho), Z3 (x0 = 0),
+ *          Z12 (rho == 0 guard) from DESIGN.md.
+ *
+ * Conventions: tensors are dense row-major, mode 1 slowest;
+ * every sum runs in ascending index order; inner loops visit
+ * each matrix row's actual nonzero range [first nonzero, last nonzero],
+ * found by scanning the row (no bandwidth is assumed).  Skipped terms are
+ * exact zeros.  OpenMP only splits independent output elements; dots use a
+ * fixed chunking so results do not depend on the thread count.
+ *
+ * Parity pins: see tests/test_oracle_pins.py (P1-P9 of DESIGN.md).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_DOT_CHUNK 4096
+
+static void row_range(const double *row, int64_t len, int64_t *lo, int64_t *hi)
+{
+    int64_t a = 0, b = len - 1;
+    while (a < len && row[a] == 0.0) a++;
+    while (b >= 0 && row[b] == 0.0) b--;
+    *lo = a;
+    *hi = b; /* empty row: lo = len, hi = -1 */
+}
+
+int orc_num_threads(void)
+{
+#ifdef _OPENMP
+    int t = 1;
+#pragma omp parallel
+    {
+#pragma omp single
+        t = omp_get_num_threads();
+    }
+    return t;
+#else
+    return 1;
+#endif
+}
+
+/* G[a,c] = sum_k A[k,a] * A[k,c]; A is m x n row-major, G is n x n. */
+void orc_gram(int64_t m, int64_t n, const double *A, double *G)
+{
+    for (int64_t a = 0; a < n; a++)
+        for (int64_t c = 0; c < n; c++) {
+            double s = 0.0;
+            for (int64_t k = 0; k < m; k++)
+                s += A[k * n + a] * A[k * n + c];
+            G[a * n + c] = s;
+        }
+}
+
+/* T = M^T for an r x c row-major M. */
+void orc_transpose(int64_t r, int64_t c, const double *M, double *T)
+{
+    for (int64_t i = 0; i < r; i++)
+        for (int64_t j = 0; j < c; j++)
+            T[j * r + i] = M[i * c + j];
+}
+
+/*
+ * Mode-d product Y = X x_d M  (Eq. 4 one-dimensional transformation):
+ *   Y[o, a, in] = sum_c M[a, c] X[o, c, in]
+ * X has shape s[0..D-1]; M is rows x s[d]; Y has shape s with s[d] -> rows.
+ */
+void orc_mode_product(int D, const int64_t *s, const double *X, int d,
+                      int64_t rows, const double *M, double *Y)
+{
+    int64_t outer = 1, inner = 1, cols = s[d];
+    for (int e = 0; e < d; e++) outer *= s[e];
+    for (int e = d + 1; e < D; e++) inner *= s[e];
+    int64_t *lo = (int64_t *)malloc(sizeof(int64_t) * (rows > 0 ? rows : 1));
+    int64_t *hi = (int64_t *)malloc(sizeof(int64_t) * (rows > 0 ? rows : 1));
+    for (int64_t a = 0; a < rows; a++) row_range(M + a * cols, cols, &lo[a], &hi[a]);
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t o = 0; o < outer; o++)
+        for (int64_t a = 0; a < rows; a++) {
+            double *y = Y + (o * rows + a) * inner;
+            for (int64_t t = 0; t < inner; t++) {
+                double acc = 0.0;
+                for (int64_t c = lo[a]; c <= hi[a]; c++)
+                    acc += M[a * cols + c] * X[(o * cols + c) * inner + t];
+                y[t] = acc;
+            }
+        }
+    free(lo);
+    free(hi);
+}
+
+static int64_t prod(const int64_t *n, int D)
+{
+    int64_t p = 1;
+    for (int d = 0; d < D; d++) p *= n[d];
+    return p;
+}
+
+/*
+ * y = (G_1 x ... x G_D) x + lam * sum_d x x_d R_d.
+ * Kronecker term: successive mode products in mode order 1..D (Eq. 4);
+ * regulariser: one mode product per mode, summed in mode order (Eq. 9).
+ * R may be NULL (lam ignored) or hold NULL entries (that mode has no term).
+ */
+void orc_apply(int D, const int64_t *n, const double *const *G,
+               const double *const *R, double lam, const double *x, double *y)
+{
+    int64_t N = prod(n, D);
+    double *t0 = (double *)malloc(sizeof(double) * N);
+    double *t1 = (double *)malloc(sizeof(double) * N);
+    memcpy(t0, x, sizeof(double) * N);
+    for (int d = 0; d < D; d++) {
+        orc_mode_product(D, n, t0, d, n[d], G[d], t1);
+        double *sw = t0; t0 = t1; t1 = sw;
+    }
+    /* t0 = Kronecker term */
+    double *reg = (double *)calloc(N, sizeof(double));
+    if (R) {
+        for (int d = 0; d < D; d++) {
+            if (!R[d]) continue;
+            orc_mode_product(D, n, x, d, n[d], R[d], t1);
+            for (int64_t i = 0; i < N; i++) reg[i] += t1[i];
+        }
+    }
+    for (int64_t i = 0; i < N; i++) y[i] = t0[i] + lam * reg[i];
+    free(t0);
+    free(t1);
+    free(reg);
+}
+
+/*
+ * b = (A_1^T x ... x A_D^T) y: successive mode products with the transposed
+ * factors in mode order 1..D.  A[d] is m_d x n_d row-major; y has shape m.
+ */
+void orc_rhs(int D, const int64_t *n, const int64_t *m, const double *const *A,
+             const double *y, double *b)
+{
+    int64_t s[8];
+    for (int d = 0; d < D; d++) s[d] = m[d];
+    int64_t cur = prod(m, D);
+    double *t0 = (double *)malloc(sizeof(double) * cur);
+    memcpy(t0, y, sizeof(double) * cur);
+    for (int d = 0; d < D; d++) {
+        double *At = (double *)malloc(sizeof(double) * m[d] * n[d]);
+        orc_transpose(m[d], n[d], A[d], At);
+        int64_t next = cur / m[d] * n[d];
+        double *t1 = (double *)malloc(sizeof(double) * next);
+        orc_mode_product(D, s, t0, d, n[d], At, t1);
+        s[d] = n[d];
+        free(At);
+        free(t0);
+        t0 = t1;
+        cur = next;
+    }
+    memcpy(b, t0, sizeof(double) * cur);
+    free(t0);
+}
+
+/*
+ * One output of the apply from the plain definition (no successive
+ * products):  y[i] = sum_j prod_d G_d[i_d, j_d] x[j]
+ *                    + lam * sum_d sum_k R_d[i_d, k] x[i with i_d -> k].
+ */
+double orc_apply_point(int D, const int64_t *n, const double *const *G,
+                       const double *const *R, double lam, const double *x,
+                       const int64_t *i)
+{
+    int64_t lo[8], hi[8], j[8], stride[8];
+    int empty = 0;
+    stride[D - 1] = 1;
+    for (int d = D - 2; d >= 0; d--) stride[d] = stride[d + 1] * n[d + 1];
+    for (int d = 0; d < D; d++) {
+        row_range(G[d] + i[d] * n[d], n[d], &lo[d], &hi[d]);
+        if (lo[d] > hi[d]) empty = 1;
+        j[d] = lo[d];
+    }
+    double kron = 0.0;
+    while (!empty) {
+        double w = 1.0;
+        int64_t lin = 0;
+        for (int d = 0; d < D; d++) {
+            w *= G[d][i[d] * n[d] + j[d]];
+            lin += j[d] * stride[d];
+        }
+        kron += w * x[lin];
+        int d = D - 1;
+        while (d >= 0) {
+            if (++j[d] <= hi[d]) break;
+            j[d] = lo[d];
+            d--;
+        }
+        if (d < 0) break;
+    }
+    double reg = 0.0;
+    if (R) {
+        int64_t base = 0;
+        for (int d = 0; d < D; d++) base += i[d] * stride[d];
+        for (int d = 0; d < D; d++) {
+            if (!R[d]) continue;
+            double s = 0.0;
+            for (int64_t k = 0; k < n[d]; k++) {
+                double r = R[d][i[d] * n[d] + k];
+                if (r != 0.0) s += r * x[base + (k - i[d]) * stride[d]];
+            }
+            reg += s;
+        }
+    }
+    return kron + lam * reg;
+}
+
+/* One output of the rhs: b[i] = sum_k prod_d A_d[k_d, i_d] y[k]. */
+double orc_rhs_point(int D, const int64_t *n, const int64_t *m,
+                     const double *const *A, const double *y, const int64_t *i)
+{
+    int64_t lo[8], hi[8], k[8], stride[8];
+    stride[D - 1] = 1;
+    for (int d = D - 2; d >= 0; d--) stride[d] = stride[d + 1] * m[d + 1];
+    for (int d = 0; d < D; d++) {
+        lo[d] = m[d];
+        hi[d] = -1;
+        for (int64_t r = 0; r < m[d]; r++)
+            if (A[d][r * n[d] + i[d]] != 0.0) {
+                if (r < lo[d]) lo[d] = r;
+                hi[d] = r;
+            }
+        if (lo[d] > hi[d]) return 0.0;
+        k[d] = lo[d];
+    }
+    double acc = 0.0;
+    for (;;) {
+        double w = 1.0;
+        int64_t lin = 0;
+        for (int d = 0; d < D; d++) {
+            w *= A[d][k[d] * n[d] + i[d]];
+            lin += k[d] * stride[d];
+        }
+        acc += w * y[lin];
+        int d = D - 1;
+        while (d >= 0) {
+            if (++k[d] <= hi[d]) break;
+            k[d] = lo[d];
+            d--;
+        }
+        if (d < 0) break;
+    }
+    return acc;
+}
+
+/* <a,b> = sum_i a_i b_i (Eq. A13): ascending sums inside fixed chunks of
+ * ORC_DOT_CHUNK, then an ascending sum of the chunk sums. */
+double orc_dot(int64_t N, const double *a, const double *b)
+{
+    int64_t nchunk = (N + ORC_DOT_CHUNK - 1) / ORC_DOT_CHUNK;
+    if (nchunk == 0) return 0.0;
+    double *part = (double *)malloc(sizeof(double) * nchunk);
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < nchunk; c++) {
+        int64_t e = (c + 1) * ORC_DOT_CHUNK;
+        if (e > N) e = N;
+        double s = 0.0;
+        for (int64_t i = c * ORC_DOT_CHUNK; i < e; i++) s += a[i] * b[i];
+        part[c] = s;
+    }
+    double s = 0.0;
+    for (int64_t c = 0; c < nchunk; c++) s += part[c];
+    free(part);
+    return s;
+}
+
+/* status codes (oracle-local; the product has its own) */
+#define ORC_OK 0
+#define ORC_BREAKDOWN 7
+#define ORC_NONFINITE 8
+#define ORC_NOT_CONVERGED 9
+
+/*
+ * Tensor CG, Fig. 2, step by step:
+ *   R := B - A*C  (C = 0, Z3: R = B);  P := R;  rho := R+*R
+ *   REPEAT  Q := A*(P*D)              (D: frame relabel only, Z4)
+ *           alpha := rho / (P+*Q)
+ *           C := C + alpha*P*D
+ *           R := R - alpha*Q
+ *           rho1 := R+*R
+ *           [stop test, Z1/Z2/Z12/Z20]
+ *           P := R + (rho1/rho)*P;  rho := rho1
+ * Stop: rho1 == 0, or rtol > 0 and rho1 <= rtol^2 * rho0, or k+1 == max_iters.
+ * hist (optional, >= max_iters+1 entries) receives rho_0 .. rho_k.
+ * Returns the status; *iters = completed iterations.
+ */
+int orc_cg(int D, const int64_t *n, const double *const *G,
+           const double *const *R, double lam, const double *b, double *x,
+           double rtol, int max_iters, double *hist, int *iters,
+           double *rho_final)
+{
+    int64_t N = prod(n, D);
+    double *r = (double *)malloc(sizeof(double) * N);
+    double *p = (double *)malloc(sizeof(double) * N);
+    double *q = (double *)malloc(sizeof(double) * N);
+    int status = ORC_OK;
+    memcpy(r, b, sizeof(double) * N);           /* R := B - A*0 */
+    memset(x, 0, sizeof(double) * N);           /* C := 0 */
+    memcpy(p, r, sizeof(double) * N);           /* P := R */
+    double rho = orc_dot(N, r, r);              /* rho := R+*R */
+    double rho0 = rho;
+    if (hist) hist[0] = rho;
+    *iters = 0;
+    if (!isfinite(rho)) {
+        status = ORC_NONFINITE;
+    } else if (rho > 0.0) {
+        for (int k = 0; k < max_iters; k++) {
+            orc_apply(D, n, G, R, lam, p, q);                        /* Q := A*(P*D) */
+            double pq = orc_dot(N, p, q);
+            if (!isfinite(pq)) { status = ORC_NONFINITE; break; }
+            if (!(pq > 0.0)) { status = ORC_BREAKDOWN; break; }
+            double alpha = rho / pq;                                 /* alpha := rho/(P+*Q) */
+            for (int64_t i = 0; i < N; i++) x[i] = x[i] + alpha * p[i]; /* C := C + alpha*P*D */
+            for (int64_t i = 0; i < N; i++) r[i] = r[i] - alpha * q[i]; /* R := R - alpha*Q */
+            double rho1 = orc_dot(N, r, r);                          /* rho1 := R+*R */
+            *iters = k + 1;
+            if (hist) hist[k + 1] = rho1;
+            if (!isfinite(rho1)) { rho = rho1; status = ORC_NONFINITE; break; }
+            if (rho1 == 0.0) { rho = rho1; break; }                  /* Z12 */
+            if (rtol > 0.0 && rho1 <= rtol * rtol * rho0) { rho = rho1; break; } /* Z1, Z2 */
+            if (k + 1 == max_iters) {
+                rho = rho1;
+                if (rtol > 0.0) status = ORC_NOT_CONVERGED;
+                break;
+            }
+            double beta = rho1 / rho;
+            for (int64_t i = 0; i < N; i++) p[i] = r[i] + beta * p[i]; /* P := R + (rho1/rho)*P */
+            rho = rho1;                                              /* rho := rho1 */
+        }
+    }
+    if (rho_final) *rho_final = rho;
+    free(r);
+    free(p);
+    free(q);
+    return status;
+}

@@ -1,0 +1,358 @@
+"""Pins of the CPU oracle to things other than itself (P1-P9).
+
+Every check here compares oracle/ against the paper's printed values, closed
+forms, textbook spectra, brute-force assembly or numpy's independent dense
+linear algebra -- never against the oracle re-typed.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from conftest import read_golden
+
+TINY_SHAPES = [((5, 4, 3), (8, 7, 6)), ((4, 3, 3, 2), (6, 5, 5, 4)), ((7,), (11,)),
+               ((6, 5), (9, 9))]
+
+
+def brute_force_K(A, L, lam):
+    """Assemble K = kron_d G_d + lam sum_d (I..R_d..I) entry by entry with
+    index loops (G_d, R_d from numpy matmul, independent of the oracle)."""
+    D = len(A)
+    n = [a.shape[1] for a in A]
+    G = [a.T @ a for a in A]
+    R = [(l.T @ l) if l is not None and l.shape[0] else np.zeros((nd, nd)) for l, nd in zip(L, n)]
+    N = int(np.prod(n))
+    K = np.zeros((N, N))
+    idx = list(itertools.product(*[range(nd) for nd in n]))
+    for I, i in enumerate(idx):
+        for J, j in enumerate(idx):
+            v = 1.0
+            for d in range(D):
+                v *= G[d][i[d], j[d]]
+            reg = 0.0
+            for d in range(D):
+                if all(i[e] == j[e] for e in range(D) if e != d):
+                    reg += R[d][i[d], j[d]]
+            K[I, J] = v + lam * reg
+    return K
+
+
+def tiny_problem(n, m, seed=3, lam=0.05, basis="bspline"):
+    A, L = synth.mode_matrices(n, m, basis=basis, seed=seed)
+    return A, L, oracle.Operator(A, L, lam)
+
+
+# ---------------------------------------------------------------- P1
+@pytest.mark.parametrize("n,m", TINY_SHAPES)
+@pytest.mark.parametrize("basis", ["bspline", "gauss"])
+def test_P1_apply_equals_bruteforce_kronecker(n, m, basis):
+    A, L, op = tiny_problem(n, m, basis=basis)
+    K = brute_force_K(A, L, op.lam)
+    x = synth.random_tensor(n, seed=11)
+    y = op.apply(x)
+    ref = K @ x.ravel()
+    assert np.linalg.norm(y.ravel() - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("n,m", TINY_SHAPES[:2])
+def test_P1_cg_equals_dense_direct_solve(n, m):
+    A, L, op = tiny_problem(n, m)
+    K = brute_force_K(A, L, op.lam)
+    b = synth.random_tensor(n, seed=12)
+    x, it, st, hist = op.cg(b, rtol=1e-14, max_iters=2000)
+    assert st == oracle.OK
+    xd = np.linalg.solve(K, b.ravel())
+    assert np.linalg.norm(x.ravel() - xd) <= 1e-10 * np.linalg.norm(xd)
+    assert len(hist) == it + 1
+
+
+def test_P1_mode_product_against_einsum_nonsymmetric():
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((3, 4, 5, 2))
+    for d in range(4):
+        M = rng.standard_normal((7, X.shape[d]))  # rectangular, not symmetric
+        Y = oracle.mode_product(X, d, M)
+        sub = "abcd"
+        out = sub.replace(sub[d], "z")
+        ref = np.einsum(f"z{sub[d]},{sub}->{out}", M, X)
+        assert np.allclose(Y, ref, rtol=1e-14, atol=1e-14)
+
+
+def test_P1_apply_point_matches_apply():
+    n, m = (6, 5, 7, 4), (12, 10, 13, 8)
+    A, L, op = tiny_problem(n, m, lam=0.3)
+    x = synth.random_tensor(n, seed=13)
+    y = op.apply(x)
+    for i in [(0, 0, 0, 0), (5, 4, 6, 3), (2, 1, 3, 2), (0, 4, 1, 3), (5, 0, 6, 0)]:
+        assert abs(op.apply_point(x, i) - y[i]) <= 1e-13 * np.abs(y).max()
+
+
+def test_P1_gram_by_loops_equals_matmul():
+    A = synth.gaussian_matrix(9, 13, seed=2, mode=0)
+    assert np.allclose(oracle.gram(A), A.T @ A, rtol=1e-14, atol=1e-15)
+
+
+def test_dot_against_exactly_rounded_sum():
+    a = synth.random_tensor((10001,), seed=1)
+    b = synth.random_tensor((10001,), seed=2, stream=8)
+    exact = math.fsum(a * b)  # products rounded, then exact sum
+    assert abs(oracle.dot(a, b) - exact) <= 1e-13 * math.fsum(np.abs(a * b))
+    assert oracle.dot(a[:0], b[:0]) == 0.0
+
+
+# ---------------------------------------------------------------- P2
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_P2_symmetry_normwise_and_positive(cfg):
+    c = synth.CONFIGS[cfg]
+    A, L = synth.mode_matrices(c)
+    op = oracle.Operator(A, L, c.lam)
+    x = synth.random_tensor(c.n, seed=21)
+    y = synth.random_tensor(c.n, seed=22, stream=8)
+    Mx, My = op.apply(x), op.apply(y)
+    a = oracle.dot(x, My)
+    b = oracle.dot(Mx, y)
+    assert abs(a - b) <= 1e-13 * np.linalg.norm(x) * np.linalg.norm(My)
+    assert oracle.dot(x, Mx) > 0
+
+
+def test_P2_tiny_K_from_oracle_columns_symmetric_pd():
+    n, m = (4, 3, 3), (6, 5, 5)
+    A, L, op = tiny_problem(n, m, lam=0.1)
+    N = op.N
+    K = np.empty((N, N))
+    for j in range(N):
+        e = np.zeros(N)
+        e[j] = 1.0
+        K[:, j] = op.apply(e.reshape(n)).ravel()
+    assert np.abs(K - K.T).max() <= 1e-15 * np.abs(K).max()
+    assert np.linalg.eigvalsh(K).min() > 0
+
+
+# ---------------------------------------------------------------- P3
+def test_P3_recovery_noiseless_unregularised():
+    c = synth.CONFIGS[0]
+    A, L = synth.mode_matrices(c)
+    op = oracle.Operator(A, None, 0.0)
+    xt = synth.x_true(c.n, seed=1)
+    y = synth.forward_model(A, xt)
+    b = op.rhs(y)
+    x, it, st, _ = op.cg(b, rtol=1e-14, max_iters=5000)
+    assert st == oracle.OK
+    assert np.linalg.norm(x - xt) <= 1e-9 * np.linalg.norm(xt)
+
+
+# ---------------------------------------------------------------- P4
+def test_P4_separability_eigenvectors_of_G():
+    n, m = (5, 4, 6, 3), (9, 8, 11, 7)
+    A, _ = synth.mode_matrices(n, m)
+    op = oracle.Operator(A, None, 0.0)
+    G = [a.T @ a for a in A]
+    rng = np.random.default_rng(0)
+    for _ in range(3):
+        vs, mus = [], []
+        for Gd in G:
+            w, V = np.linalg.eigh(Gd)
+            k = rng.integers(len(w))
+            vs.append(V[:, k])
+            mus.append(w[k])
+        x = vs[0]
+        for v in vs[1:]:
+            x = np.multiply.outer(x, v)
+        y = op.apply(x)
+        assert np.allclose(y, np.prod(mus) * x, atol=1e-13 * np.abs(np.prod(mus)))
+
+
+def test_P4_kronecker_sum_spectrum_of_regulariser():
+    n = (6, 5, 7)
+    A = [np.eye(nd) for nd in n]  # G_d = I
+    L = [synth.second_difference(nd) for nd in n]
+    lam = 0.7
+    op = oracle.Operator(A, L, lam)
+    vs, nus = [], []
+    for l in L:
+        w, V = np.linalg.eigh(l.T @ l)
+        vs.append(V[:, -1])
+        nus.append(w[-1])
+    x = np.multiply.outer(np.multiply.outer(vs[0], vs[1]), vs[2])
+    y = op.apply(x)
+    assert np.allclose(y, (1.0 + lam * sum(nus)) * x, atol=1e-13 * (1 + lam * sum(nus)))
+
+
+def test_P4_rank1_separable_transformation():
+    """Eq. 4: a separable operator maps a rank-1 tensor to the rank-1 tensor of
+    the per-mode images."""
+    n, m = (5, 4, 3), (8, 7, 6)
+    A, _ = synth.mode_matrices(n, m, basis="gauss", seed=4)
+    op = oracle.Operator(A, None, 0.0)
+    G = [a.T @ a for a in A]
+    rng = np.random.default_rng(1)
+    v = [rng.standard_normal(nd) for nd in n]
+    x = np.multiply.outer(np.multiply.outer(v[0], v[1]), v[2])
+    gv = [G[d] @ v[d] for d in range(3)]
+    ref = np.multiply.outer(np.multiply.outer(gv[0], gv[1]), gv[2])
+    assert np.allclose(op.apply(x), ref, rtol=1e-13, atol=1e-14)
+
+
+# ---------------------------------------------------------------- P5
+def test_P5_commutativity_all_mode_orders():
+    n = (5, 4, 6, 3)
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal(n)
+    mats = [rng.standard_normal((nd, nd)) for nd in n]  # not symmetric
+    results = []
+    for perm in itertools.permutations(range(4)):
+        Y = X
+        for d in perm:
+            Y = oracle.mode_product(Y, d, mats[d])
+        results.append(Y)
+    ref = results[0]
+    for Y in results[1:]:
+        assert np.linalg.norm(Y - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+# ---------------------------------------------------------------- P6
+def test_P6_second_difference_gram_closed_form():
+    g = read_golden("second_difference_gram.txt")
+    n = int(g["n"])
+    R = oracle.gram(synth.second_difference(n))
+    for key in ("row0", "row1", "row3", "row6"):
+        want = np.array([float(v) for v in g[key].split()])
+        assert np.array_equal(R[int(key[3:])], want)
+    assert np.abs(R @ np.ones(n)).max() == 0.0
+    assert np.abs(R @ np.arange(n, dtype=float)).max() == 0.0
+
+
+def test_P6_bspline_closed_form_values():
+    g = read_golden("bspline_values.txt")
+    u = np.array([float(v) for v in g["u"].split()])
+    want = np.array([float(v) for v in g["beta3"].split()])
+    assert np.allclose(synth.cubic_bspline(u), want, rtol=0, atol=1e-16)
+
+
+def _cox_de_boor(t, knots, i, k):
+    if k == 0:
+        return 1.0 if knots[i] <= t < knots[i + 1] else 0.0
+    a = (t - knots[i]) / (knots[i + k] - knots[i])
+    b = (knots[i + k + 1] - t) / (knots[i + k + 1] - knots[i + 1])
+    return a * _cox_de_boor(t, knots, i, k - 1) + b * _cox_de_boor(t, knots, i + 1, k - 1)
+
+
+@pytest.mark.parametrize("n,m", [(12, 20), (16, 32), (15, 30)])
+def test_P6_bspline_matrix_vs_cox_de_boor_and_partition(n, m):
+    A = synth.bspline_matrix(n, m)
+    t = synth.sample_positions(n, m)
+    for i in range(m):
+        for k in range(n):
+            knots = [k - 2, k - 1, k, k + 1, k + 2]
+            assert abs(A[i, k] - _cox_de_boor(t[i], knots, 0, 3)) <= 1e-15
+    inner = (t >= 1) & (t <= n - 2)
+    assert np.allclose(A[inner].sum(axis=1), 1.0, atol=1e-15)
+    assert np.count_nonzero(A, axis=1).max() <= 4
+
+
+# ---------------------------------------------------------------- P7
+def test_P7_paper_printed_band_count():
+    g = read_golden("paper_band_count.txt")
+    grid = [int(v) for v in g["grid"].split()]
+    total = 1
+    for nd in grid:
+        G = oracle.gram(synth.bspline_matrix(nd, 2 * nd))
+        upper = int(np.count_nonzero(np.triu(G)))
+        assert upper == 4 * nd - 6
+        total *= upper
+    assert total == int(g["nonzeros"])
+    assert round(total * 4 / 1e9) == int(g["gbytes_single"])
+
+
+# ---------------------------------------------------------------- P8
+def test_P8_rhs_of_forward_model_equals_unregularised_apply():
+    n, m = (6, 5, 4, 3), (12, 10, 8, 6)
+    A, _ = synth.mode_matrices(n, m)
+    op = oracle.Operator(A, None, 0.0)
+    x = synth.random_tensor(n, seed=31)
+    lhs = op.rhs(synth.forward_model(A, x))
+    rhs = op.apply(x)
+    assert np.linalg.norm(lhs - rhs) <= 1e-13 * np.linalg.norm(rhs)
+
+
+def test_P8_rank1_rhs_and_pointwise():
+    n, m = (5, 4, 3), (8, 7, 6)
+    A, _ = synth.mode_matrices(n, m, basis="gauss", seed=9)
+    op = oracle.Operator(A, None, 0.0)
+    rng = np.random.default_rng(3)
+    u = [rng.standard_normal(md) for md in m]
+    y = np.multiply.outer(np.multiply.outer(u[0], u[1]), u[2])
+    b = op.rhs(y)
+    au = [A[d].T @ u[d] for d in range(3)]
+    ref = np.multiply.outer(np.multiply.outer(au[0], au[1]), au[2])
+    assert np.allclose(b, ref, rtol=1e-13, atol=1e-14)
+    for i in [(0, 0, 0), (4, 3, 2), (2, 1, 1)]:
+        assert abs(op.rhs_point(y, i) - b[i]) <= 1e-13 * np.abs(b).max()
+
+
+# ---------------------------------------------------------------- P9
+def test_P9_spec_worked_example_cg():
+    g = read_golden("spec_cg_example.txt")
+    T = np.array([[float(v) for v in row.split()] for row in g["matrix"].split(";")])
+    A1 = np.linalg.cholesky(T).T  # upper factor: A1^T A1 = T
+    ones = np.array([float(v) for v in g["b"].split()])
+    y = np.linalg.solve(A1.T, ones)  # A1^T y = 1
+    op = oracle.Operator([A1], None, 0.0)
+    b = op.rhs(y)
+    assert np.allclose(b, ones, atol=1e-14)
+    x, it, st, hist = op.cg(b, rtol=1e-15, max_iters=int(g["max_iters"]))
+    want = np.array([float(v) for v in g["x"].split()])
+    assert st == oracle.OK
+    assert np.abs(x - want).max() <= 1e-12
+    assert it <= int(g["max_iters"])
+
+
+def test_cg_zero_rhs_zero_iterations():
+    A, L, op = tiny_problem((4, 3, 3), (6, 5, 5))
+    x, it, st, hist = op.cg(np.zeros(op.n), rtol=1e-10, max_iters=10)
+    assert it == 0 and st == oracle.OK and np.all(x == 0)
+
+
+def test_cg_rho_zero_guard_and_history_decrease():
+    # order-1 diagonal system: CG converges exactly in 1 step, rho == 0 (Z12 guard)
+    op = oracle.Operator([np.diag([2.0, 2.0, 2.0])], None, 0.0)
+    x, it, st, hist = op.cg(np.ones(3), rtol=0.0, max_iters=5)
+    assert st == oracle.OK and it == 1 and hist[-1] == 0.0
+    assert np.allclose(x, 0.25)
+    c = synth.CONFIGS[0]
+    A, L = synth.mode_matrices(c)
+    op = oracle.Operator(A, L, c.lam)
+    b = op.rhs(synth.data(A, c.n, c.m))
+    x, it, st, hist = op.cg(b, rtol=c.rtol, max_iters=c.max_iters)
+    assert st == oracle.OK and hist[-1] <= c.rtol ** 2 * hist[0]
+    assert np.all(hist[1:] <= 10 * np.maximum.accumulate(hist)[:-1])
+    r = b - op.apply(x)
+    assert np.linalg.norm(r) <= 1e-10 * np.linalg.norm(b)
+
+
+def test_cg_not_converged_status():
+    c = synth.CONFIGS[0]
+    A, L = synth.mode_matrices(c)
+    op = oracle.Operator(A, L, c.lam)
+    b = op.rhs(synth.data(A, c.n, c.m))
+    x, it, st, hist = op.cg(b, rtol=1e-30, max_iters=5)
+    assert st == oracle.NOT_CONVERGED and it == 5
+
+
+def test_thread_count_independent():
+    import os
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import numpy as np, oracle, synth;"
+            "c=synth.CONFIGS[2]; A,L=synth.mode_matrices(c); op=oracle.Operator(A,L,c.lam);"
+            "x=synth.random_tensor(c.n,5); y=op.apply(x); print(repr(oracle.dot(y,y)))"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    outs = []
+    for t in ("1", "3"):
+        env = dict(os.environ, OMP_NUM_THREADS=t)
+        outs.append(subprocess.check_output([sys.executable, "-c", code], env=env).strip())
+    assert outs[0] == outs[1]
