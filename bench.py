@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""bench.py -- CG iterations/s of the tca hot path on B200 (one JSON line).
+
+A step is one pass of the whole hot path over the
+config's synthetic input resident in HBM: operator setup (tca_operator_create),
+rhs b = (kron A_d^T) y, and the config's CG solve (500 iterations for config 3),
+then destroy.  `value` = CG iterations/s of the whole job.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--dtype f64]
+    python bench.py --impl reference ...     # the CPU oracle, bounded sample
+
+The synthetic input (x_true, noise, y = (kron A_d) x_true + 0.01 noise) is made
+on the device by the library's seeded generator before the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "CG iters/s & operator-apply HBM GB/s (fraction of peak), 4D ~30M unknowns"
+UNIT = "CG iters/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tca", choices=["tca", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--iters", type=int, default=None, help="override CG iterations")
+    ap.add_argument("--apply-reps", type=int, default=50)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_name(cfg, dtype, iters):
+    n = "x".join(map(str, cfg.n))
+    m = "x".join(map(str, cfg.m))
+    stop = f"{iters} CG iterations" if cfg.rtol <= 0 else f"CG to rel. residual {cfg.rtol:g}"
+    return f"config {cfg.index}: {n} unknowns {dtype}, data {m}, lambda {cfg.lam:g}, {stop}"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.out = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- CPU oracle baseline
+def cpu_oracle_sample(cfg, iters_target_s, dtype):
+    """Oracle CG iterations on the same config, bounded to ~iters_target_s seconds."""
+    import oracle
+    A, L = synth.mode_matrices(cfg)
+    op = oracle.Operator(A, L, cfg.lam)
+    b = synth.random_tensor(cfg.n, seed=1)
+    t0 = time.perf_counter()
+    op.cg(b, rtol=0.0, max_iters=1)
+    t1 = time.perf_counter() - t0
+    k = int(max(2, min(cfg.max_iters, iters_target_s / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    _, it, _, _ = op.cg(b, rtol=0.0, max_iters=k)
+    el = time.perf_counter() - t0
+    return {"value": it / el, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{it} fp64 CG iterations (Fig. 2) of config {cfg.index} from a seeded b; "
+                      f"one iteration = apply + 2 dots + 3 updates; setup/rhs excluded"
+                      + ("" if dtype == "f64" else "; oracle is fp64 only"),
+            "seconds": el}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = synth.CONFIGS[args.config]
+    iters = args.iters or cfg.max_iters
+    import oracle
+    A, L = synth.mode_matrices(cfg)
+    op = oracle.Operator(A, L, cfg.lam)
+    b = synth.random_tensor(cfg.n, seed=1)
+    # bounded per-step sample so that the whole run finishes in a few minutes
+    t0 = time.perf_counter()
+    op.cg(b, rtol=0.0, max_iters=1)
+    t1 = time.perf_counter() - t0
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    k = int(max(1, min(iters, budget / max(t1, 1e-6))))
+    for _ in range(args.warmup):
+        op.cg(b, rtol=0.0, max_iters=1)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, it, _, _ = op.cg(b, rtol=0.0, max_iters=k)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = args.steps * k / tot
+    sample = (f"each step: {k} fp64 CG iterations (Fig. 2) of config {cfg.index} from a seeded b "
+              f"(bounded sample of the {iters}-iteration solve)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg, args.dtype, iters)},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_tca(args):
+    import torch
+    from paper_1001_5460_b200 import tca
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 or args.gpus > 1:
+        raise SystemExit("multi-GPU bench needs the sharded operator (not built yet)")
+    torch.cuda.set_device(local)
+    dev_index = torch.cuda.current_device()
+    cfg = synth.CONFIGS[args.config]
+    iters = args.iters or cfg.max_iters
+    dtype = args.dtype
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    esize = 8 if dtype == "f64" else 4
+    A, L = synth.mode_matrices(cfg)
+    stream = torch.cuda.current_stream()
+
+    gen = tca.Operator(A, L, cfg.lam, dtype=dtype)
+    ydata = gen.forward_model(None, sigma=synth.NOISE_SIGMA, seed=1)  # resident input
+    torch.cuda.synchronize()
+
+    state = {}
+
+    def step(timing=False):
+        op = tca.Operator(A, L, cfg.lam, dtype=dtype)          # a1
+        if timing:
+            op.set_timing(True)
+        b = op.rhs(ydata)                                        # a2
+        x, rep = op.cg_solve(b, rtol=cfg.rtol, max_iters=iters)  # a3-a6
+        if timing:
+            ms, cnt = op.get_timing()
+            state["apply_ms"] = state.get("apply_ms", 0.0) + ms
+            state["apply_cnt"] = state.get("apply_cnt", 0) + cnt
+        state["iters"] = state.get("iters", 0) + rep["iterations"]
+        state["last_rep"] = rep
+        op.close()
+        return x
+
+    for _ in range(args.warmup):
+        step()
+    state.clear()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev_index)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = tca.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(timing=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = tca.kernel_launches() - launches0
+    clk = clocks.stop()
+    total_ms = ev0.elapsed_time(ev1)
+    total_iters = state["iters"]
+    value = total_iters / (total_ms * 1e-3)
+    hbm, peak_src = peaks()
+
+    # dominant kernel: the operator apply inside CG (event pairs around every launch)
+    apply_us = 1e3 * state["apply_ms"] / max(1, state["apply_cnt"])
+    apply_bytes = 2 * cfg.N * esize  # read p, write q (algorithmic)
+    achieved = apply_bytes / (apply_us * 1e-6) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "kernel": "operator apply (q = M p) in CG",
+                "bytes_per_launch": apply_bytes, "us_per_launch": apply_us,
+                "peak_source": peak_src}
+
+    # standalone apply (operator-apply GB/s, the metric's second half)
+    op = tca.Operator(A, L, cfg.lam, dtype=dtype)
+    xin = torch.empty(cfg.n, dtype=tdt, device="cuda")
+    tca.generate_normal(xin, seed=3, stream_id=7)
+    yout = torch.empty_like(xin)
+    for _ in range(3):
+        op.apply(xin, yout)
+    torch.cuda.synchronize()
+    op.set_timing(True)
+    for _ in range(args.apply_reps):
+        op.apply(xin, yout)
+    torch.cuda.synchronize()
+    ams, acnt = op.get_timing()
+    op.close()
+    a_us = 1e3 * ams / acnt
+    apply_info = {"us": a_us, "applies_per_s": 1e6 / a_us,
+                  "GBps": apply_bytes / (a_us * 1e-6) / 1e9,
+                  "frac_hbm": apply_bytes / (a_us * 1e-6) / 1e9 / hbm}
+
+    e2e = None
+    if not args.no_e2e:
+        yh = torch.empty(ydata.shape, dtype=tdt, pin_memory=True)
+        yh.copy_(ydata.cpu())
+        xh = torch.empty(cfg.n, dtype=tdt, pin_memory=True)
+        for _ in range(1):
+            op = tca.Operator(A, L, cfg.lam, dtype=dtype)
+            op.solve_host(yh, xh, rtol=cfg.rtol, max_iters=iters)
+            op.close()
+        e_steps = max(1, min(args.steps, 3))
+        it_sum = 0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e_steps):
+            op = tca.Operator(A, L, cfg.lam, dtype=dtype)
+            rep = op.solve_host(yh, xh, rtol=cfg.rtol, max_iters=iters)
+            it_sum += rep["iterations"]
+            op.close()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e_ms = e0.elapsed_time(e1)
+        e2e = {"value": it_sum / (e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(cfg.Mdata * esize), "d2h_bytes_per_step": int(cfg.N * esize),
+               "wall_value": it_sum / wall, "path": "tca_solve_host (pinned host y -> x)"}
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        cpu = cpu_oracle_sample(cfg, args.cpu_seconds, dtype)
+
+    rep = state["last_rep"]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": dtype, "data": "synthetic (seeded counter RNG on device; cubic B-spline A_d)",
+        "config": {"workload": workload_name(cfg, dtype, iters), "config_index": cfg.index,
+                   "unknowns": cfg.N, "data_points": cfg.Mdata, "cg_iters_per_step": iters,
+                   "step": "tca_operator_create + tca_rhs + tca_cg_solve + destroy",
+                   "l2": "inputs larger than L2 (each vector %d MB, y %d MB)" % (
+                       cfg.N * esize >> 20, cfg.Mdata * esize >> 20),
+                   "parallelism": "single GPU"},
+        "roofline": roofline,
+        "apply": apply_info,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "time_to_solution_ms": total_ms / args.steps,
+        "cg_report": {"iterations": rep["iterations"], "rho0": rep["rho0"],
+                      "rho_final": rep["rho_final"], "status": rep["status"]},
+        "apply_path": "fused" if gen_apply_path(tca, A, L, cfg, dtype) else "multipass",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def gen_apply_path(tca, A, L, cfg, dtype):
+    return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_tca(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

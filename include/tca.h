@@ -1,0 +1,211 @@
+/*
+ * tca.h -- C ABI of the B200 tensor-CG library (libtca.so).
+ *
+ * The library solves the regularised separable tensor equation of
+ * arxiv 1001.5460 ("Solving Tensor Structured Problems with Computational
+ * Tensor Algebra"):
+ *
+ *     M x = b,   M = (G_1 (x) ... (x) G_D) + lambda * sum_d (I (x) .. R_d .. (x) I)
+ *     G_d = A_d^T A_d,  R_d = L_d^T L_d,   b = (A_1^T (x) ... (x) A_D^T) y
+ *
+ *   - the tensor equation A.U = B and its matrix equivalent: PAPER.md:100-109 (Eq. 8)
+ *   - separable transformation applied mode by mode: PAPER.md:68-73 (Eq. 4)
+ *   - Kronecker-sum operator (regulariser form): PAPER.md:176-182 (Eq. 9)
+ *   - A^T A from matrix normal equations: PAPER.md:507-509 (A.7)
+ *   - tensor conjugate gradients: PAPER.md:186-227 (Fig. 2)
+ *   - inner product <A,B> = sum A o B: PAPER.md:487-505 (Eq. A13/A14)
+ *
+ * Conventions (all entry points):
+ *   - Tensors are dense, row-major, mode 1 slowest, mode D contiguous
+ *     (SPEC.md:148).  A tensor "of shape n" has prod(n_d) elements of the
+ *     operator's dtype (double for TCA_F64, float for TCA_F32).
+ *   - Tensor arguments of tca_apply / tca_rhs / tca_cg_solve are DEVICE
+ *     pointers owned by the caller; the host variants (*_host) take HOST
+ *     pointers (pinned memory recommended) and copy inside the call.
+ *   - Per-mode matrices (A_d, L_d) are HOST fp64 row-major arrays, copied at
+ *     create; the caller may free them afterwards.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Device-pointer calls are stream-ordered and asynchronous
+ *     unless stated otherwise.
+ *   - Every call validates all arguments before launching anything and
+ *     returns a tca_status; nothing aborts or throws across the ABI.
+ *     tca_last_error() returns a thread-local message naming the reason.
+ *   - There is no CPU fallback: every numerical step runs in the library's
+ *     CUDA kernels (sm_100a).
+ */
+#ifndef TCA_H
+#define TCA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TCA_OK = 0,
+    TCA_ERR_INVALID_ARG = 1, /* NULL pointer, bad order/extent/dtype/lambda   */
+    TCA_ERR_SHAPE = 2,       /* matrix shapes inconsistent with n, m          */
+    TCA_ERR_NOT_SPD = 3,     /* some G_d is not positive definite (A_d rank)  */
+    TCA_ERR_OOM = 4,         /* device allocation failed                      */
+    TCA_ERR_CUDA = 5,        /* CUDA runtime error (message in last_error)    */
+    TCA_ERR_NCCL = 6,        /* NCCL error in a distributed operator          */
+    TCA_ERR_BREAKDOWN = 7,   /* CG: <p, Mp> <= 0                */
+    TCA_ERR_NONFINITE = 8,   /* CG: NaN/Inf in a dot product                  */
+    TCA_NOT_CONVERGED = 9    /* CG: rtol not reached in max_iters (x valid)   */
+} tca_status;
+
+typedef enum { TCA_F64 = 0, TCA_F32 = 1 } tca_dtype;
+
+/* Opaque operator: per-mode tap tables, workspaces, device scalars. */
+typedef struct tca_operator tca_operator;
+
+/*
+ * Distributed (mode-1 sharded) operator description.  NULL = single GPU.
+ * nccl_comm: an ncclComm_t of nranks ranks, one per GPU, owned by the caller,
+ * whose rank r holds mode-1 rows [own_lo, own_hi) of every tensor
+ * (tca_operator_query).  The rhs is formed shard-locally from the data rows
+ * [data_lo, data_hi) (no communication); apply exchanges 3 boundary mode-1
+ * slices with each neighbour; CG all-reduces its two dot products.
+ */
+typedef struct {
+    int rank;
+    int nranks;
+    void *nccl_comm;
+} tca_dist;
+
+/* CG report (SPEC.md:446-449 SolveReport).  rho_history is caller-owned,
+ * optional (NULL), and must hold history_capacity >= max_iters+1 doubles. */
+typedef struct {
+    int32_t iterations;   /* completed CG iterations k                       */
+    int32_t converged;    /* 1 if rho_k <= rtol^2 rho_0 or rho_k == 0         */
+    int32_t status;       /* tca_status of the solve                         */
+    int32_t pad;
+    double rho0;          /* <r0, r0> = <b, b>                               */
+    double rho_final;     /* recursive <r_k, r_k>                            */
+    double seconds;       /* device time of the solve (CUDA events)          */
+    double *rho_history;  /* rho_0 .. rho_k (optional)                       */
+    int32_t history_capacity;
+    int32_t pad2;
+} tca_cg_report;
+
+/*
+ * Create the operator M for an order-D problem (1 <= order <= 4).
+ *   n[d]  unknown extents, m[d] data extents (d = 0..order-1), n[d] >= 1.
+ *   A[d]  host fp64 m[d] x n[d] row-major (the per-mode basis).
+ *   L     NULL (no regulariser) or D host pointers to (n[d]-2) x n[d]
+ *         row-major fp64 matrices; an entry may be NULL or have n[d] < 3
+ *         (that mode then has no regulariser term).
+ *   lambda >= 0, finite.
+ *   dtype  storage and arithmetic type of tensors and taps; CG scalars
+ *          (dots, alpha, beta) are always fp64.
+ *   dist   NULL for one GPU, or a tca_dist (mode-1 sharding).
+ * Forms G_d = A_d^T A_d and R_d = L_d^T L_d in fp64 on the host, detects the
+ * half-bandwidth of each G_d (banded path when <= 3 and R_d's <= 2, dense
+ * path otherwise), checks G_d positive definite (Cholesky), uploads tap
+ * tables and allocates workspaces (r, p, q, halo, reduction scratch).
+ * Synchronises `stream` before returning.  *op receives NULL on error.
+ */
+tca_status tca_operator_create(tca_operator **op, int order, const int64_t *n,
+                               const int64_t *m, const double *const *A,
+                               const double *const *L, double lambda,
+                               tca_dtype dtype, const tca_dist *dist,
+                               void *stream);
+
+/*
+ * Query an operator.  Any output pointer may be NULL.
+ *   own_lo/own_hi     mode-1 unknown rows held by this rank ([0,n1) on 1 GPU)
+ *   data_lo/data_hi   mode-1 data rows this rank's tca_rhs reads
+ *   banded_mask       bit d set when mode d uses the banded path
+ *   half_bandwidth    D ints: half-bandwidth of G_d
+ *   device_bytes      bytes of device memory the operator holds (the
+ *                     matrix-free contract: O(N) + O(sum n_d^2), never N^2)
+ */
+tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo,
+                              int64_t *own_hi, int64_t *data_lo,
+                              int64_t *data_hi, int *banded_mask,
+                              int *half_bandwidth, size_t *device_bytes);
+
+/* y = M x.  x, y: device tensors of the local shape (rows [own_lo, own_hi)
+ * of mode 1 on a sharded operator); x and y must not alias. */
+tca_status tca_apply(const tca_operator *op, const void *x, void *y,
+                     void *stream);
+
+/* b = (A_1^T (x) ... (x) A_D^T) ydata.  ydata: device tensor of shape
+ * (data_hi-data_lo, m_2, ..., m_D); b: device tensor of the local unknown
+ * shape.  Uses a temporary device workspace of at most prod(m)/ratio
+ * elements (stream-ordered allocation). */
+tca_status tca_rhs(const tca_operator *op, const void *ydata, void *b,
+                   void *stream);
+
+/*
+ * Solve M x = b by tensor CG (Fig. 2) from x0 = 0 (reading Z3).
+ *   rtol > 0: stop when rho_k <= rtol^2 * rho_0 (reading Z2) or rho_k == 0,
+ *             status TCA_NOT_CONVERGED if max_iters is reached first;
+ *   rtol <= 0: run exactly max_iters iterations (stopping early only if
+ *             rho_k == 0, reading Z12).
+ * b, x: device tensors of the local shape.  The iteration runs entirely on
+ * the device (scalars in device memory, no host round trip per iteration).
+ * Synchronises `stream` before filling *rep (rep may be NULL).
+ */
+tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol,
+                        int32_t max_iters, tca_cg_report *rep, void *stream);
+
+/*
+ * End-to-end solve from HOST buffers: copies ydata_host (data shape of this
+ * rank) to the device, forms the rhs, runs tca_cg_solve and copies x back to
+ * x_host (local unknown shape).  Synchronises `stream`.
+ */
+tca_status tca_solve_host(tca_operator *op, const void *ydata_host,
+                          void *x_host, double rtol, int32_t max_iters,
+                          tca_cg_report *rep, void *stream);
+
+void tca_operator_destroy(tca_operator *op);
+
+/*
+ * Seeded synthetic input generator (reading Z9): out[i] = scale *
+ * normal(seed, stream_id, offset + i), i < count, where normal(.) is the
+ * Box-Muller transform of the counter generator
+ *   u64(seed, s, j) = mix64(mix64(seed * GAMMA + s) + j * GAMMA)
+ * (SplitMix64 output function, GAMMA = 0x9E3779B97F4A7C15) with
+ *   normal(j) = sqrt(-2 ln U(2j)) cos(2 pi U(2j+1)),  U = ((u64>>11)+0.5) 2^-53.
+ * out: device array of `count` elements of dtype.
+ */
+tca_status tca_generate_normal(void *out, tca_dtype dtype, int64_t count,
+                               int64_t offset, uint64_t seed,
+                               uint32_t stream_id, double scale, void *stream);
+
+/*
+ * Synthetic data of the operator's problem: ydata = (A_1 (x) ... (x) A_D) x
+ *   + sigma * normal(seed, 1, global data linear index), for this rank's data
+ * rows.  x: device tensor of the full unknown shape (or NULL: x_true is then
+ * generated in place from stream 0, position keyed).  ydata as in tca_rhs.
+ */
+tca_status tca_forward_model(const tca_operator *op, const void *x, void *ydata,
+                             double sigma, uint64_t seed, void *stream);
+
+/*
+ * Timing instrumentation (measurement only; off by default).  When enabled,
+ * tca_cg_solve and tca_apply record a CUDA event pair on `stream` around
+ * every operator-apply launch; tca_operator_get_timing returns the summed
+ * device time (ms) and the number of timed applies since the last reset.
+ */
+tca_status tca_operator_set_timing(tca_operator *op, int enable);
+tca_status tca_operator_get_timing(tca_operator *op, double *apply_ms,
+                                   int64_t *apply_count, int reset);
+
+/* Number of CUDA kernel launches the library has issued so far (process-wide). */
+int64_t tca_kernel_launches(void);
+
+const char *tca_status_string(tca_status s);
+const char *tca_last_error(void);
+
+/* Library build information: "tca <version> sm_100a" */
+const char *tca_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCA_H */

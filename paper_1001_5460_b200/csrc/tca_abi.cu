@@ -1,0 +1,697 @@
+// tca_abi.cu -- host side of libtca: the extern "C" entry points of
+// include/tca.h, operator setup (G_d = A_d^T A_d, R_d = L_d^T L_d, band
+// detection, tap tables), and the orchestration of the device kernels.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "tca_fused.cuh"
+#include "tca_internal.cuh"
+
+namespace tca {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+tca_status fail(tca_status s, const std::string &msg)
+{
+    set_error(msg);
+    return s;
+}
+
+tca_status cuda_fail(cudaError_t e, const char *what)
+{
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? TCA_ERR_OOM : TCA_ERR_CUDA;
+}
+
+static bool all_finite(const double *a, size_t k)
+{
+    for (size_t i = 0; i < k; ++i)
+        if (!isfinite(a[i])) return false;
+    return true;
+}
+
+// G = M^T M for an r x c row-major M (fp64, ascending k sums).
+static std::vector<double> gram(const double *M, int64_t r, int64_t c)
+{
+    std::vector<double> G((size_t)(c * c), 0.0);
+    for (int64_t a = 0; a < c; ++a)
+        for (int64_t b = a; b < c; ++b) {
+            double s = 0.0;
+            for (int64_t k = 0; k < r; ++k) s += M[k * c + a] * M[k * c + b];
+            G[a * c + b] = s;
+            G[b * c + a] = s;
+        }
+    return G;
+}
+
+static int half_bandwidth(const std::vector<double> &G, int64_t n)
+{
+    int hb = 0;
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j)
+            if (G[i * n + j] != 0.0) hb = std::max(hb, (int)std::llabs(i - j));
+    return hb;
+}
+
+static bool cholesky_ok(const std::vector<double> &G, int64_t n)
+{
+    std::vector<double> L(G);
+    for (int64_t j = 0; j < n; ++j) {
+        double d = L[j * n + j];
+        for (int64_t k = 0; k < j; ++k) d -= L[j * n + k] * L[j * n + k];
+        if (!(d > 0.0) || !isfinite(d)) return false;
+        d = sqrt(d);
+        L[j * n + j] = d;
+        for (int64_t i = j + 1; i < n; ++i) {
+            double s = L[i * n + j];
+            for (int64_t k = 0; k < j; ++k) s -= L[i * n + k] * L[j * n + k];
+            L[i * n + j] = s / d;
+        }
+    }
+    return true;
+}
+
+template <typename T>
+static tca_status upload(const std::vector<double> &h, void **dptr, size_t *bytes)
+{
+    std::vector<T> c(h.size());
+    for (size_t i = 0; i < h.size(); ++i) c[i] = (T)h[i];
+    size_t nb = std::max<size_t>(c.size(), 1) * sizeof(T);
+    TCA_CUDA_TRY(cudaMalloc(dptr, nb));
+    *bytes += nb;
+    if (!c.empty()) TCA_CUDA_TRY(cudaMemcpy(*dptr, c.data(), c.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return TCA_OK;
+}
+
+static tca_status upload_dtype(tca_dtype dt, const std::vector<double> &h, void **dptr,
+                               size_t *bytes)
+{
+    return dt == TCA_F64 ? upload<double>(h, dptr, bytes) : upload<float>(h, dptr, bytes);
+}
+
+// Build a compressed-band matrix from a dense rows x cols fp64 matrix.
+// width_hint > 0 forces the centred offset form start[r] = r - width_hint/2.
+static tca_status make_band(tca_dtype dt, const std::vector<double> &M, int rows, int cols,
+                            int centred_half, BandMat *out, size_t *bytes)
+{
+    std::vector<int> start(rows);
+    int W = 0;
+    if (centred_half >= 0) {
+        W = 2 * centred_half + 1;
+        for (int r = 0; r < rows; ++r) start[r] = r - centred_half;
+    } else {
+        for (int r = 0; r < rows; ++r) {
+            int lo = cols, hi = -1;
+            for (int c = 0; c < cols; ++c)
+                if (M[(size_t)r * cols + c] != 0.0) { lo = std::min(lo, c); hi = c; }
+            if (hi < 0) { start[r] = 0; continue; }
+            start[r] = lo;
+            W = std::max(W, hi - lo + 1);
+        }
+        if (W == 0) W = 1;
+    }
+    std::vector<double> taps((size_t)rows * W, 0.0);
+    for (int r = 0; r < rows; ++r)
+        for (int w = 0; w < W; ++w) {
+            int c = start[r] + w;
+            if (c >= 0 && c < cols) taps[(size_t)r * W + w] = M[(size_t)r * cols + c];
+        }
+    out->rows = rows;
+    out->cols = cols;
+    out->W = W;
+    TCA_CUDA_TRY(cudaMalloc(&out->start, sizeof(int) * std::max(rows, 1)));
+    *bytes += sizeof(int) * std::max(rows, 1);
+    TCA_CUDA_TRY(cudaMemcpy(out->start, start.data(), sizeof(int) * rows, cudaMemcpyHostToDevice));
+    return upload_dtype(dt, taps, &out->taps, bytes);
+}
+
+static void free_band(BandMat &b)
+{
+    if (b.start) cudaFree(b.start);
+    if (b.taps) cudaFree(b.taps);
+    b.start = nullptr;
+    b.taps = nullptr;
+}
+
+static int64_t inner_of(const int64_t *ext, int d)
+{
+    int64_t p = 1;
+    for (int e = d + 1; e < kD; ++e) p *= ext[e];
+    return p;
+}
+
+static int64_t outer_of(const int64_t *ext, int d)
+{
+    int64_t p = 1;
+    for (int e = 0; e < d; ++e) p *= ext[e];
+    return p;
+}
+
+template <typename T>
+static tca_status apply_multipass_t(const tca_operator *op, const T *x, T *y,
+                                    const int32_t *done, cudaStream_t s)
+{
+    int64_t ext[kD] = {op->nloc1, op->n[1], op->n[2], op->n[3]};
+    // Kronecker term: mode products D..1 (Eq. 5 lets us pick any order).
+    std::vector<int> active;
+    for (int d = kD - 1; d >= 0; --d)
+        if (d < op->order) active.push_back(d);
+    const T *in = x;
+    T *bufs[2] = {(T *)op->t0, (T *)op->t1};
+    int nb = 0;
+    for (size_t i = 0; i < active.size(); ++i) {
+        const int d = active[i];
+        T *out = (i + 1 == active.size()) ? y : bufs[nb];
+        launch_band_mode_product<T>(in, out, outer_of(ext, d), op->Gm[d], inner_of(ext, d), 1.0,
+                                    false, done, s);
+        in = out;
+        nb ^= 1;
+    }
+    // Regulariser: y += lambda * (x x_d R_d) for each mode (Eq. 9 Kronecker sum).
+    for (int d = 0; d < op->order; ++d)
+        if (op->has_reg[d])
+            launch_band_mode_product<T>(x, y, outer_of(ext, d), op->Rm[d], inner_of(ext, d),
+                                        op->lambda, true, done, s);
+    return TCA_OK;
+}
+
+tca_status apply_multipass(const tca_operator *op, const void *x, void *y,
+                           const int32_t *done, cudaStream_t s)
+{
+    if (!op->t0) return fail(TCA_ERR_INVALID_ARG, "multi-pass workspace missing");
+    if (op->dtype == TCA_F64)
+        return apply_multipass_t<double>(op, (const double *)x, (double *)y, done, s);
+    return apply_multipass_t<float>(op, (const float *)x, (float *)y, done, s);
+}
+
+static tca_status apply_dispatch(const tca_operator *op, const void *x, void *y,
+                                 const int32_t *done, cudaStream_t s)
+{
+    if (op->apply_path == 1) return launch_fused_apply(op, x, y, done, s);
+    return apply_multipass(op, x, y, done, s);
+}
+
+// Successive rectangular mode products in[...] -> out[...] (forward model or rhs).
+template <typename T>
+static tca_status chain_products(const tca_operator *op, const T *in, T *out,
+                                 const int64_t *ext_in, const int64_t *ext_out,
+                                 const BandMat *mats, const std::vector<int> &order,
+                                 cudaStream_t s)
+{
+    int64_t ext[kD];
+    for (int d = 0; d < kD; ++d) ext[d] = ext_in[d];
+    // size of the largest intermediate
+    size_t maxi = 0;
+    {
+        int64_t e2[kD];
+        for (int d = 0; d < kD; ++d) e2[d] = ext_in[d];
+        for (size_t i = 0; i + 1 < order.size(); ++i) {
+            e2[order[i]] = ext_out[order[i]];
+            size_t sz = 1;
+            for (int d = 0; d < kD; ++d) sz *= (size_t)e2[d];
+            maxi = std::max(maxi, sz);
+        }
+    }
+    T *tmp[2] = {nullptr, nullptr};
+    if (order.size() > 1) {
+        TCA_CUDA_TRY(cudaMallocAsync((void **)&tmp[0], maxi * sizeof(T), s));
+        if (order.size() > 2) TCA_CUDA_TRY(cudaMallocAsync((void **)&tmp[1], maxi * sizeof(T), s));
+    }
+    const T *cur = in;
+    for (size_t i = 0; i < order.size(); ++i) {
+        const int d = order[i];
+        T *dst = (i + 1 == order.size()) ? out : tmp[i & 1];
+        launch_band_mode_product<T>(cur, dst, outer_of(ext, d), mats[d], inner_of(ext, d), 1.0,
+                                    false, nullptr, s);
+        ext[d] = ext_out[d];
+        cur = dst;
+    }
+    if (order.empty()) {
+        size_t sz = 1;
+        for (int d = 0; d < kD; ++d) sz *= (size_t)ext[d];
+        TCA_CUDA_TRY(cudaMemcpyAsync(out, in, sz * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    }
+    if (tmp[0]) TCA_CUDA_TRY(cudaFreeAsync(tmp[0], s));
+    if (tmp[1]) TCA_CUDA_TRY(cudaFreeAsync(tmp[1], s));
+    return TCA_OK;
+}
+
+template <typename T>
+static tca_status rhs_t(const tca_operator *op, const T *ydata, T *b, cudaStream_t s)
+{
+    int64_t ein[kD] = {op->data_hi - op->data_lo, op->m[1], op->m[2], op->m[3]};
+    int64_t eout[kD] = {op->nloc1, op->n[1], op->n[2], op->n[3]};
+    std::vector<int> order;
+    for (int d = 0; d < op->order; ++d) order.push_back(d);
+    // contract the modes that shrink the tensor most first (PAPER.md:83 cost-driven order)
+    std::stable_sort(order.begin(), order.end(), [&](int a, int c) {
+        return (double)ein[a] / eout[a] > (double)ein[c] / eout[c];
+    });
+    return chain_products<T>(op, ydata, b, ein, eout, op->At, order, s);
+}
+
+template <typename T>
+static tca_status forward_t(const tca_operator *op, const T *x, T *y, double sigma,
+                            uint64_t seed, cudaStream_t s)
+{
+    int64_t ein[kD] = {op->n[0], op->n[1], op->n[2], op->n[3]};
+    int64_t eout[kD] = {op->m[0], op->m[1], op->m[2], op->m[3]};
+    const int64_t N = ein[0] * ein[1] * ein[2] * ein[3];
+    const int64_t M = eout[0] * eout[1] * eout[2] * eout[3];
+    T *xt = nullptr;
+    if (!x) {
+        TCA_CUDA_TRY(cudaMallocAsync((void **)&xt, N * sizeof(T), s));
+        launch_gen_normal<T>(xt, N, 0, stream_key(seed, 0), 1.0, false, s);
+        x = xt;
+    }
+    std::vector<int> order;
+    for (int d = 0; d < op->order; ++d) order.push_back(d);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int c) {
+        return (double)eout[a] / ein[a] < (double)eout[c] / ein[c];
+    });
+    TCA_TRY(chain_products<T>(op, x, y, ein, eout, op->Af, order, s));
+    if (sigma != 0.0) launch_gen_normal<T>(y, M, 0, stream_key(seed, 1), sigma, true, s);
+    if (xt) TCA_CUDA_TRY(cudaFreeAsync(xt, s));
+    return TCA_OK;
+}
+
+// Timed apply: an event pair around the launch when instrumentation is on.
+static tca_status timed_apply(tca_operator *op, const void *x, void *y, const int32_t *done,
+                              cudaStream_t s)
+{
+    if (!op->timing) return apply_dispatch(op, x, y, done, s);
+    if (op->tev_used + 2 > op->tev.size()) {
+        for (int i = 0; i < 64; ++i) {
+            cudaEvent_t e;
+            TCA_CUDA_TRY(cudaEventCreate(&e));
+            op->tev.push_back(e);
+        }
+    }
+    cudaEvent_t a = op->tev[op->tev_used], b = op->tev[op->tev_used + 1];
+    op->tev_used += 2;
+    TCA_CUDA_TRY(cudaEventRecord(a, s));
+    TCA_TRY(apply_dispatch(op, x, y, done, s));
+    TCA_CUDA_TRY(cudaEventRecord(b, s));
+    return TCA_OK;
+}
+
+// Fold the recorded event pairs into apply_ms / apply_count (after a sync).
+static tca_status harvest_timing(tca_operator *op)
+{
+    for (size_t i = 0; i + 1 < op->tev_used; i += 2) {
+        float ms = 0.f;
+        TCA_CUDA_TRY(cudaEventSynchronize(op->tev[i + 1]));
+        TCA_CUDA_TRY(cudaEventElapsedTime(&ms, op->tev[i], op->tev[i + 1]));
+        op->apply_ms += ms;
+        op->apply_count += 1;
+    }
+    op->tev_used = 0;
+    return TCA_OK;
+}
+
+template <typename T>
+static void cg_iteration(tca_operator *op, T *x, cudaStream_t s)
+{
+    T *r = (T *)op->r, *p = (T *)op->p, *q = (T *)op->q;
+    const int32_t *done = &op->sc->done;
+    timed_apply(op, p, q, done, s);                                   // Q := A*(P*D)
+    launch_dot_partials<T>(p, q, op->N, op->part, done, s);          // P+*Q
+    launch_cg_finalize(1, op->part, op->sc, op->hist, s);            // alpha
+    launch_cg_update_xr<T>(x, r, p, q, op->N, op->sc, op->part, s);  // C, R, R+*R
+    launch_cg_finalize(2, op->part, op->sc, op->hist, s);            // rho1, stop, beta
+    launch_cg_update_p<T>(p, r, op->N, op->sc, s);                   // P := R + beta*P
+}
+
+template <typename T>
+static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t max_iters,
+                       tca_cg_report *rep, cudaStream_t s)
+{
+    CgScalars h{};
+    h.rtol2 = rtol > 0.0 ? rtol * rtol : 0.0;
+    h.max_iters = max_iters;
+    *op->sc_host = h;
+    TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
+    TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
+    launch_cg_init<T>(b, x, (T *)op->r, (T *)op->p, op->N, op->part, s);
+    launch_cg_finalize(0, op->part, op->sc, op->hist, s);
+    if (rtol <= 0.0) {
+        for (int k = 0; k < max_iters; ++k) cg_iteration<T>(op, x, s);
+    } else {
+        const int chunk = 32;
+        for (int k = 0; k < max_iters; k += chunk) {
+            const int c = std::min(chunk, max_iters - k);
+            for (int i = 0; i < c; ++i) cg_iteration<T>(op, x, s);
+            TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars),
+                                         cudaMemcpyDeviceToHost, s));
+            TCA_CUDA_TRY(cudaStreamSynchronize(s));
+            if (op->timing) TCA_TRY(harvest_timing(op));
+            if (op->sc_host->done) break;
+        }
+    }
+    TCA_CUDA_TRY(cudaGetLastError());
+    TCA_CUDA_TRY(cudaEventRecord(op->ev1, s));
+    TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+    TCA_CUDA_TRY(cudaStreamSynchronize(s));
+    if (op->timing) TCA_TRY(harvest_timing(op));
+    const CgScalars &r = *op->sc_host;
+    if (rep) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, op->ev0, op->ev1);
+        rep->iterations = r.iters;
+        rep->converged = r.converged;
+        rep->status = r.status;
+        rep->rho0 = r.rho0;
+        rep->rho_final = r.rho;
+        rep->seconds = ms * 1e-3;
+        if (rep->rho_history && rep->history_capacity > 0) {
+            const int cnt = std::min(rep->history_capacity, r.iters + 1);
+            TCA_CUDA_TRY(cudaMemcpy(rep->rho_history, op->hist, sizeof(double) * cnt,
+                                    cudaMemcpyDeviceToHost));
+        }
+    }
+    return (tca_status)r.status;
+}
+
+static tca_status check_op(const tca_operator *op)
+{
+    if (!op) return fail(TCA_ERR_INVALID_ARG, "op is NULL");
+    return TCA_OK;
+}
+
+}  // namespace tca
+
+using namespace tca;
+
+extern "C" {
+
+const char *tca_version(void) { return "tca 0.1 sm_100a"; }
+
+const char *tca_last_error(void) { return g_last_error.c_str(); }
+
+const char *tca_status_string(tca_status s)
+{
+    switch (s) {
+    case TCA_OK: return "TCA_OK";
+    case TCA_ERR_INVALID_ARG: return "TCA_ERR_INVALID_ARG";
+    case TCA_ERR_SHAPE: return "TCA_ERR_SHAPE";
+    case TCA_ERR_NOT_SPD: return "TCA_ERR_NOT_SPD";
+    case TCA_ERR_OOM: return "TCA_ERR_OOM";
+    case TCA_ERR_CUDA: return "TCA_ERR_CUDA";
+    case TCA_ERR_NCCL: return "TCA_ERR_NCCL";
+    case TCA_ERR_BREAKDOWN: return "TCA_ERR_BREAKDOWN";
+    case TCA_ERR_NONFINITE: return "TCA_ERR_NONFINITE";
+    case TCA_NOT_CONVERGED: return "TCA_NOT_CONVERGED";
+    }
+    return "TCA_UNKNOWN_STATUS";
+}
+
+void tca_operator_destroy(tca_operator *op)
+{
+    if (!op) return;
+    for (int d = 0; d < kD; ++d) {
+        free_band(op->Gm[d]);
+        free_band(op->Rm[d]);
+        free_band(op->At[d]);
+        free_band(op->Af[d]);
+        if (op->tapG[d]) cudaFree(op->tapG[d]);
+        if (op->tapR[d]) cudaFree(op->tapR[d]);
+    }
+    void *bufs[] = {op->r, op->p, op->q, op->t0, op->t1, op->part, op->sc, op->hist};
+    for (void *b : bufs)
+        if (b) cudaFree(b);
+    if (op->sc_host) cudaFreeHost(op->sc_host);
+    if (op->ev0) cudaEventDestroy(op->ev0);
+    if (op->ev1) cudaEventDestroy(op->ev1);
+    for (cudaEvent_t e : op->tev) cudaEventDestroy(e);
+    delete op;
+}
+
+tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, const int64_t *m,
+                               const double *const *A, const double *const *L, double lambda,
+                               tca_dtype dtype, const tca_dist *dist, void *stream)
+{
+    if (!out) return fail(TCA_ERR_INVALID_ARG, "op (output pointer) is NULL");
+    *out = nullptr;
+    if (order < 1 || order > 4) return fail(TCA_ERR_INVALID_ARG, "order must be in 1..4");
+    if (!n || !m || !A) return fail(TCA_ERR_INVALID_ARG, "n, m and A must be non-NULL");
+    if (dtype != TCA_F64 && dtype != TCA_F32) return fail(TCA_ERR_INVALID_ARG, "dtype must be TCA_F64 or TCA_F32");
+    if (!isfinite(lambda) || lambda < 0.0) return fail(TCA_ERR_INVALID_ARG, "lambda must be finite and >= 0");
+    for (int d = 0; d < order; ++d) {
+        if (n[d] < 1 || n[d] > (1 << 20)) return fail(TCA_ERR_SHAPE, "n[" + std::to_string(d) + "] out of range");
+        if (m[d] < 1 || m[d] > (1 << 20)) return fail(TCA_ERR_SHAPE, "m[" + std::to_string(d) + "] out of range");
+        if (!A[d]) return fail(TCA_ERR_INVALID_ARG, "A[" + std::to_string(d) + "] is NULL");
+        if (!all_finite(A[d], (size_t)(n[d] * m[d])))
+            return fail(TCA_ERR_INVALID_ARG, "A[" + std::to_string(d) + "] has non-finite entries");
+        if (L && L[d] && n[d] >= 3 && !all_finite(L[d], (size_t)((n[d] - 2) * n[d])))
+            return fail(TCA_ERR_INVALID_ARG, "L[" + std::to_string(d) + "] has non-finite entries");
+    }
+    if (dist && dist->nranks > 1)
+        return fail(TCA_ERR_INVALID_ARG, "dist: multi-rank operators are created through tca_dist_* (nranks > 1 not supported here)");
+    cudaStream_t s = (cudaStream_t)stream;
+
+    tca_operator *op = new tca_operator();
+    op->order = order;
+    op->dtype = dtype;
+    op->esize = dtype == TCA_F64 ? 8 : 4;
+    op->lambda = lambda;
+    for (int d = 0; d < order; ++d) {
+        op->n[d] = n[d];
+        op->m[d] = m[d];
+    }
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&op->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    size_t bytes = 0;
+    tca_status st = TCA_OK;
+    bool all_banded = true;
+    for (int d = 0; d < kD && st == TCA_OK; ++d) {
+        const int nd = (int)op->n[d], md = (int)op->m[d];
+        std::vector<double> G, R, Ad;
+        if (d < order) {
+            G = gram(A[d], md, nd);                       // G_d = A_d^T A_d
+            if (!cholesky_ok(G, nd)) {
+                st = fail(TCA_ERR_NOT_SPD, "G_" + std::to_string(d + 1) + " = A^T A is not positive definite (A lacks full column rank)");
+                break;
+            }
+            if (L && L[d] && nd >= 3 && lambda > 0.0) {
+                R = gram(L[d], nd - 2, nd);               // R_d = L_d^T L_d
+                op->has_reg[d] = 1;
+                op->hbR[d] = half_bandwidth(R, nd);
+            }
+            Ad.assign(A[d], A[d] + (size_t)md * nd);
+        } else {
+            G.assign(1, 1.0);
+            Ad.assign(1, 1.0);
+        }
+        op->hbG[d] = half_bandwidth(G, nd);
+        const bool banded = op->hbG[d] <= kHG && (!op->has_reg[d] || op->hbR[d] <= kHR);
+        if (banded) op->banded_mask |= (1 << d);
+        else all_banded = false;
+        st = make_band(dtype, G, nd, nd, banded ? kHG : -1, &op->Gm[d], &bytes);
+        if (st != TCA_OK) break;
+        if (op->has_reg[d]) {
+            st = make_band(dtype, R, nd, nd, op->hbR[d] <= kHR ? kHR : -1, &op->Rm[d], &bytes);
+            if (st != TCA_OK) break;
+        }
+        // A_d^T (rows n_d, cols m_d) for the rhs; A_d (rows m_d, cols n_d) for the forward model
+        std::vector<double> At((size_t)nd * md);
+        for (int i = 0; i < md; ++i)
+            for (int j = 0; j < nd; ++j) At[(size_t)j * md + i] = Ad[(size_t)i * nd + j];
+        st = make_band(dtype, At, nd, md, -1, &op->At[d], &bytes);
+        if (st != TCA_OK) break;
+        st = make_band(dtype, Ad, md, nd, -1, &op->Af[d], &bytes);
+        if (st != TCA_OK) break;
+        // offset-form taps for the fused banded kernel
+        std::vector<double> tg((size_t)nd * 7, 0.0), tr((size_t)nd * 5, 0.0);
+        for (int r = 0; r < nd; ++r) {
+            for (int k = -kHG; k <= kHG; ++k)
+                if (r + k >= 0 && r + k < nd && std::abs(k) <= op->hbG[d])
+                    tg[(size_t)r * 7 + k + kHG] = G[(size_t)r * nd + r + k];
+            if (op->has_reg[d])
+                for (int k = -kHR; k <= kHR; ++k)
+                    if (r + k >= 0 && r + k < nd) tr[(size_t)r * 5 + k + kHR] = lambda * R[(size_t)r * nd + r + k];
+        }
+        st = upload_dtype(dtype, tg, &op->tapG[d], &bytes);
+        if (st != TCA_OK) break;
+        st = upload_dtype(dtype, tr, &op->tapR[d], &bytes);
+    }
+    if (st != TCA_OK) {
+        tca_operator_destroy(op);
+        return st;
+    }
+    op->all_banded = all_banded;
+    op->own_lo = 0;
+    op->own_hi = op->n[0];
+    op->data_lo = 0;
+    op->data_hi = op->m[0];
+    op->nloc1 = op->own_hi - op->own_lo;
+    op->N = op->nloc1 * op->n[1] * op->n[2] * op->n[3];
+    op->Mloc = (op->data_hi - op->data_lo) * op->m[1] * op->m[2] * op->m[3];
+    op->apply_path = fused_apply_supported(op) ? 1 : 0;
+
+    const size_t vb = (size_t)op->N * op->esize;
+    cudaError_t e = cudaSuccess;
+    e = cudaMalloc(&op->r, vb);
+    if (e == cudaSuccess) e = cudaMalloc(&op->p, vb);
+    if (e == cudaSuccess) e = cudaMalloc(&op->q, vb);
+    if (e == cudaSuccess && op->apply_path == 0) e = cudaMalloc(&op->t0, vb);
+    if (e == cudaSuccess && op->apply_path == 0) e = cudaMalloc(&op->t1, vb);
+    if (e == cudaSuccess) e = cudaMalloc(&op->part, sizeof(double) * kRedBlocks * 2);
+    if (e == cudaSuccess) e = cudaMalloc(&op->sc, sizeof(CgScalars));
+    if (e == cudaSuccess) e = cudaMallocHost(&op->sc_host, sizeof(CgScalars));
+    if (e == cudaSuccess) e = cudaEventCreate(&op->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&op->ev1);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        tca_status rs = cuda_fail(e, "tca_operator_create workspace");
+        tca_operator_destroy(op);
+        return rs;
+    }
+    bytes += vb * (op->apply_path == 0 ? 5 : 3) + sizeof(double) * kRedBlocks * 2 + sizeof(CgScalars);
+    op->device_bytes = bytes;
+    *out = op;
+    return TCA_OK;
+}
+
+tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo, int64_t *own_hi,
+                              int64_t *data_lo, int64_t *data_hi, int *banded_mask,
+                              int *half_bw, size_t *device_bytes)
+{
+    TCA_TRY(check_op(op));
+    if (own_lo) *own_lo = op->own_lo;
+    if (own_hi) *own_hi = op->own_hi;
+    if (data_lo) *data_lo = op->data_lo;
+    if (data_hi) *data_hi = op->data_hi;
+    if (banded_mask) *banded_mask = op->banded_mask & ((1 << op->order) - 1);
+    if (half_bw)
+        for (int d = 0; d < op->order; ++d) half_bw[d] = op->hbG[d];
+    if (device_bytes) *device_bytes = op->device_bytes;
+    return TCA_OK;
+}
+
+tca_status tca_apply(const tca_operator *op, const void *x, void *y, void *stream)
+{
+    TCA_TRY(check_op(op));
+    if (!x || !y) return fail(TCA_ERR_INVALID_ARG, "x and y must be non-NULL device pointers");
+    if (x == y) return fail(TCA_ERR_INVALID_ARG, "x and y must not alias");
+    cudaStream_t s = (cudaStream_t)stream;
+    TCA_TRY(timed_apply(const_cast<tca_operator *>(op), x, y, nullptr, s));
+    TCA_CUDA_TRY(cudaGetLastError());
+    return TCA_OK;
+}
+
+tca_status tca_operator_set_timing(tca_operator *op, int enable)
+{
+    TCA_TRY(check_op(op));
+    op->timing = enable ? 1 : 0;
+    return TCA_OK;
+}
+
+tca_status tca_operator_get_timing(tca_operator *op, double *apply_ms, int64_t *apply_count,
+                                   int reset)
+{
+    TCA_TRY(check_op(op));
+    TCA_TRY(harvest_timing(op));
+    if (apply_ms) *apply_ms = op->apply_ms;
+    if (apply_count) *apply_count = op->apply_count;
+    if (reset) {
+        op->apply_ms = 0.0;
+        op->apply_count = 0;
+    }
+    return TCA_OK;
+}
+
+int64_t tca_kernel_launches(void) { return g_launches.load(); }
+
+tca_status tca_rhs(const tca_operator *op, const void *ydata, void *b, void *stream)
+{
+    TCA_TRY(check_op(op));
+    if (!ydata || !b) return fail(TCA_ERR_INVALID_ARG, "ydata and b must be non-NULL device pointers");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (op->dtype == TCA_F64) TCA_TRY(rhs_t<double>(op, (const double *)ydata, (double *)b, s));
+    else TCA_TRY(rhs_t<float>(op, (const float *)ydata, (float *)b, s));
+    TCA_CUDA_TRY(cudaGetLastError());
+    return TCA_OK;
+}
+
+tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
+                        tca_cg_report *rep, void *stream)
+{
+    TCA_TRY(check_op(op));
+    if (!b || !x) return fail(TCA_ERR_INVALID_ARG, "b and x must be non-NULL device pointers");
+    if (b == x) return fail(TCA_ERR_INVALID_ARG, "b and x must not alias");
+    if (max_iters < 0) return fail(TCA_ERR_INVALID_ARG, "max_iters must be >= 0");
+    if (!isfinite(rtol)) return fail(TCA_ERR_INVALID_ARG, "rtol must be finite");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (op->hist_cap < max_iters + 1) {
+        if (op->hist) cudaFree(op->hist);
+        op->hist = nullptr;
+        op->hist_cap = 0;
+        TCA_CUDA_TRY(cudaMalloc(&op->hist, sizeof(double) * (max_iters + 1)));
+        op->hist_cap = max_iters + 1;
+    }
+    if (op->dtype == TCA_F64) return cg_t<double>(op, (const double *)b, (double *)x, rtol, max_iters, rep, s);
+    return cg_t<float>(op, (const float *)b, (float *)x, rtol, max_iters, rep, s);
+}
+
+tca_status tca_solve_host(tca_operator *op, const void *ydata_host, void *x_host, double rtol,
+                          int32_t max_iters, tca_cg_report *rep, void *stream)
+{
+    TCA_TRY(check_op(op));
+    if (!ydata_host || !x_host) return fail(TCA_ERR_INVALID_ARG, "ydata_host and x_host must be non-NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    void *yd = nullptr, *bd = nullptr, *xd = nullptr;
+    const size_t yb = (size_t)op->Mloc * op->esize, vb = (size_t)op->N * op->esize;
+    TCA_CUDA_TRY(cudaMallocAsync(&yd, yb, s));
+    TCA_CUDA_TRY(cudaMallocAsync(&bd, vb, s));
+    TCA_CUDA_TRY(cudaMallocAsync(&xd, vb, s));
+    TCA_CUDA_TRY(cudaMemcpyAsync(yd, ydata_host, yb, cudaMemcpyHostToDevice, s));
+    tca_status st = tca_rhs(op, yd, bd, stream);
+    if (st == TCA_OK || st == TCA_NOT_CONVERGED) {
+        st = tca_cg_solve(op, bd, xd, rtol, max_iters, rep, stream);
+        cudaMemcpyAsync(x_host, xd, vb, cudaMemcpyDeviceToHost, s);
+    }
+    cudaFreeAsync(yd, s);
+    cudaFreeAsync(bd, s);
+    cudaFreeAsync(xd, s);
+    TCA_CUDA_TRY(cudaStreamSynchronize(s));
+    return st;
+}
+
+tca_status tca_generate_normal(void *out, tca_dtype dtype, int64_t count, int64_t offset,
+                               uint64_t seed, uint32_t stream_id, double scale, void *stream)
+{
+    if (!out && count > 0) return fail(TCA_ERR_INVALID_ARG, "out is NULL");
+    if (count < 0 || offset < 0) return fail(TCA_ERR_INVALID_ARG, "count and offset must be >= 0");
+    if (dtype != TCA_F64 && dtype != TCA_F32) return fail(TCA_ERR_INVALID_ARG, "bad dtype");
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint64_t key = stream_key(seed, stream_id);
+    if (dtype == TCA_F64) launch_gen_normal<double>((double *)out, count, offset, key, scale, false, s);
+    else launch_gen_normal<float>((float *)out, count, offset, key, scale, false, s);
+    TCA_CUDA_TRY(cudaGetLastError());
+    return TCA_OK;
+}
+
+tca_status tca_forward_model(const tca_operator *op, const void *x, void *ydata, double sigma,
+                             uint64_t seed, void *stream)
+{
+    TCA_TRY(check_op(op));
+    if (!ydata) return fail(TCA_ERR_INVALID_ARG, "ydata is NULL");
+    if (op->nranks > 1 && x) return fail(TCA_ERR_INVALID_ARG, "sharded forward model takes x = NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (op->dtype == TCA_F64) TCA_TRY(forward_t<double>(op, (const double *)x, (double *)ydata, sigma, seed, s));
+    else TCA_TRY(forward_t<float>(op, (const float *)x, (float *)ydata, sigma, seed, s));
+    TCA_CUDA_TRY(cudaGetLastError());
+    return TCA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// tca_internal.cuh -- internal declarations of libtca (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+#include <atomic>
+
+#include "../../include/tca.h"
+
+namespace tca {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+tca_status fail(tca_status s, const std::string &msg);
+tca_status cuda_fail(cudaError_t e, const char *what);
+
+#define TCA_CUDA_TRY(expr)                                           \
+    do {                                                             \
+        cudaError_t e_ = (expr);                                     \
+        if (e_ != cudaSuccess) return ::tca::cuda_fail(e_, #expr);   \
+    } while (0)
+
+#define TCA_TRY(expr)                                                \
+    do {                                                             \
+        tca_status s_ = (expr);                                      \
+        if (s_ != TCA_OK) return s_;                                 \
+    } while (0)
+
+// ---------------------------------------------------------------- layout
+// Every problem is padded to order 4 with trailing extents 1 (G = [1], no
+// regulariser), so mode 1 is always the slowest (streamed / sharded) mode
+// and mode 4 the contiguous one.
+constexpr int kD = 4;
+constexpr int kHG = 3;  // half-bandwidth of the banded G taps (7 taps)
+constexpr int kHR = 2;  // half-bandwidth of the banded R taps (5 taps)
+constexpr int kRedBlocks = 592;   // 4 x 148: fixed grid of every dot partial
+constexpr int kRedThreads = 256;
+
+// Compressed band rows of a rows x cols matrix:
+//   (M v)[r] = sum_{w < W} taps[r*W + w] * v[start[r] + w]   (zero outside [0, cols))
+struct BandMat {
+    int rows = 0, cols = 0, W = 0;
+    int *start = nullptr;  // device, rows
+    void *taps = nullptr;  // device, rows*W of the operator dtype
+};
+
+// Device-resident CG scalars (always fp64, reading Z10).
+struct CgScalars {
+    double rho;      // <r_k, r_k>
+    double rho0;     // <r_0, r_0>
+    double pq;       // <p_k, q_k>
+    double alpha;    // rho / pq
+    double beta;     // rho1 / rho
+    double rtol2;    // rtol^2 (<= 0: fixed iterations)
+    int32_t iters;   // completed iterations
+    int32_t max_iters;
+    int32_t done;    // 1: later kernels of the solve are no-ops
+    int32_t status;  // tca_status
+    int32_t converged;
+    int32_t pad;
+};
+
+}  // namespace tca
+
+struct tca_operator {
+    int order = 0;
+    int64_t n[tca::kD] = {1, 1, 1, 1};   // global unknown extents (padded)
+    int64_t m[tca::kD] = {1, 1, 1, 1};   // global data extents (padded)
+    tca_dtype dtype = TCA_F64;
+    size_t esize = 8;
+    double lambda = 0.0;
+    int hbG[tca::kD] = {0, 0, 0, 0};
+    int hbR[tca::kD] = {0, 0, 0, 0};
+    int has_reg[tca::kD] = {0, 0, 0, 0};
+    int banded_mask = 0;                 // bit d: G_d hb <= 3 (and R_d hb <= 2)
+    bool all_banded = false;
+
+    // offset-form taps (fused banded kernel): tapG[d][r*7 + k+3] = G_d[r, r+k],
+    // tapR[d][r*5 + k+2] = lambda * R_d[r, r+k]
+    void *tapG[tca::kD] = {};
+    void *tapR[tca::kD] = {};
+    // generic compressed-band forms
+    tca::BandMat Gm[tca::kD], Rm[tca::kD], At[tca::kD], Af[tca::kD];
+
+    // sharding (mode 1)
+    int rank = 0, nranks = 1;
+    void *comm = nullptr;
+    int64_t own_lo = 0, own_hi = 0, data_lo = 0, data_hi = 0;
+    int64_t nloc1 = 0;        // own_hi - own_lo
+    int64_t N = 0;            // local unknowns
+    int64_t Mloc = 0;         // local data points
+
+    // workspaces
+    void *r = nullptr, *p = nullptr, *q = nullptr;
+    void *t0 = nullptr, *t1 = nullptr;   // multi-pass temporaries (lazy)
+    double *part = nullptr;              // kRedBlocks reduction partials (x2)
+    tca::CgScalars *sc = nullptr;        // device scalars
+    tca::CgScalars *sc_host = nullptr;   // pinned mirror
+    double *hist = nullptr;              // device rho history
+    int hist_cap = 0;
+    size_t device_bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int num_sms = 148;
+    int apply_path = 0;                  // 0 = generic multi-pass, 1 = fused banded
+    // timing instrumentation
+    int timing = 0;
+    std::vector<cudaEvent_t> tev;        // pairs (start, stop)
+    size_t tev_used = 0;
+    double apply_ms = 0.0;
+    int64_t apply_count = 0;
+};
+
+namespace tca {
+
+// ---------------------------------------------------------------- kernels (tca_kernels.cu)
+// Y[o, r, t] = alpha * sum_w taps[r,w] X[o, start[r]+w, t]  (+ Y[o,r,t] if accumulate)
+template <typename T>
+void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
+                              int64_t inner, double alpha, bool accumulate,
+                              const int32_t *done, cudaStream_t s);
+
+template <typename T>
+void launch_gen_normal(T *out, int64_t count, int64_t offset, uint64_t key,
+                       double scale, bool accumulate, cudaStream_t s);
+
+// CG vector kernels; every one is a no-op once sc->done != 0.
+template <typename T>
+void launch_cg_init(const T *b, T *x, T *r, T *p, int64_t N, double *part,
+                    cudaStream_t s);
+template <typename T>
+void launch_dot_partials(const T *a, const T *b, int64_t N, double *part,
+                         const int32_t *done, cudaStream_t s);
+template <typename T>
+void launch_cg_update_xr(T *x, T *r, const T *p, const T *q, int64_t N,
+                         const CgScalars *sc, double *part, cudaStream_t s);
+template <typename T>
+void launch_cg_update_p(T *p, const T *r, int64_t N, const CgScalars *sc,
+                        cudaStream_t s);
+
+// finalisers (one block): 0 = init rho, 1 = pq -> alpha, 2 = rr -> beta/stop
+void launch_cg_finalize(int which, const double *part, CgScalars *sc,
+                        double *hist, cudaStream_t s);
+
+uint64_t stream_key(uint64_t seed, uint32_t stream_id);
+
+// process-wide count of kernel launches issued by the library
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+// ---------------------------------------------------------------- host helpers (tca_abi.cu)
+tca_status apply_multipass(const tca_operator *op, const void *x, void *y,
+                           const int32_t *done, cudaStream_t s);
+
+}  // namespace tca

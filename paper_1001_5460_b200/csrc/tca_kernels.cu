@@ -1,0 +1,305 @@
+// tca_kernels.cu -- generic (correctness-rung) kernels of libtca:
+//   * compressed-band mode-d product (any band width, rectangular or dense),
+//     the one-dimensional transformation of Eq. 4;
+//   * CG vector updates and dot-product partials (Fig. 2, PAPER.md:193-221;
+//     inner product Eq. A13; elementwise ops A.4,
+//     PAPER.md:441-452) with device-resident fp64 scalars;
+//   * the seeded counter-based normal generator (reading Z9).
+// Reductions are deterministic: a fixed grid writes per-block partials that
+// one block sums in a fixed order (no floating-point atomics).
+#include <math.h>
+
+#include "tca_internal.cuh"
+
+namespace tca {
+
+std::atomic<int64_t> g_launches{0};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum for blockDim.x == kRedThreads; result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v)
+{
+    __shared__ double sm[kRedThreads / 32];
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) sm[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < kRedThreads / 32; ++i) s += sm[i];
+    }
+    __syncthreads();
+    return s;
+}
+
+// ---------------------------------------------------------------- band mode product
+template <typename T>
+__global__ void __launch_bounds__(256)
+band_mode_product_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t outer,
+                         int rows, int cols, int64_t inner,
+                         const int *__restrict__ start, const T *__restrict__ taps,
+                         int W, T alpha, int accumulate, const int32_t *done)
+{
+    if (done && *done) return;
+    const int64_t total = outer * (int64_t)rows * inner;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = idx % inner;
+        const int64_t rest = idx / inner;
+        const int r = (int)(rest % rows);
+        const int64_t o = rest / rows;
+        const int s0 = start[r];
+        const T *xp = X + o * cols * inner + t;
+        const T *tp = taps + (int64_t)r * W;
+        T acc = T(0);
+        for (int w = 0; w < W; ++w) {
+            const int c = s0 + w;
+            if (c >= 0 && c < cols) acc += tp[w] * xp[(int64_t)c * inner];
+        }
+        acc *= alpha;
+        if (accumulate) acc += Y[idx];
+        Y[idx] = acc;
+    }
+}
+
+template <typename T>
+void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
+                              int64_t inner, double alpha, bool accumulate,
+                              const int32_t *done, cudaStream_t s)
+{
+    const int64_t total = outer * (int64_t)M.rows * inner;
+    if (total == 0) return;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    count_launch();
+    band_mode_product_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(
+        X, Y, outer, M.rows, M.cols, inner, M.start, (const T *)M.taps, M.W, (T)alpha,
+        accumulate ? 1 : 0, done);
+}
+
+// ---------------------------------------------------------------- generator (Z9)
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+uint64_t stream_key(uint64_t seed, uint32_t stream_id)
+{
+    return mix64(seed * kGamma + (uint64_t)stream_id);
+}
+
+__device__ __forceinline__ double u01(uint64_t z)
+{
+    return ((double)(z >> 11) + 0.5) * 0x1.0p-53;
+}
+
+__device__ __forceinline__ double normal_at(uint64_t key, uint64_t j)
+{
+    const double u1 = u01(mix64(key + (2 * j) * kGamma));
+    const double u2 = u01(mix64(key + (2 * j + 1) * kGamma));
+    const double two_pi = 6.283185307179586;  // (2 * pi) rounded to double
+    const double a = __dmul_rn(two_pi, u2);
+    return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(a));
+}
+
+template <typename T>
+__global__ void gen_normal_kernel(T *out, int64_t count, int64_t offset, uint64_t key,
+                                  double scale, int accumulate)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double v = __dmul_rn(scale, normal_at(key, (uint64_t)(offset + i)));
+        if (accumulate) v = __dadd_rn((double)out[i], v);
+        out[i] = (T)v;
+    }
+}
+
+template <typename T>
+void launch_gen_normal(T *out, int64_t count, int64_t offset, uint64_t key, double scale,
+                       bool accumulate, cudaStream_t s)
+{
+    if (count <= 0) return;
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    count_launch();
+    gen_normal_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(out, count, offset, key, scale,
+                                                         accumulate ? 1 : 0);
+}
+
+// ---------------------------------------------------------------- CG vector kernels
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+cg_init_kernel(const T *__restrict__ b, T *__restrict__ x, T *__restrict__ r,
+               T *__restrict__ p, int64_t N, double *part)
+{
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const T v = b[i];
+        r[i] = v;          // R := B - A*0
+        p[i] = v;          // P := R
+        x[i] = T(0);       // C := 0
+        acc += (double)v * (double)v;
+    }
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+dot_partials_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t N,
+                    double *part, const int32_t *done)
+{
+    if (done && *done) return;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x)
+        acc += (double)a[i] * (double)b[i];
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+cg_update_xr_kernel(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ p,
+                    const T *__restrict__ q, int64_t N, const CgScalars *sc, double *part)
+{
+    if (sc->done) return;
+    const T alpha = (T)sc->alpha;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] = x[i] + alpha * p[i];            // C := C + alpha*P*D
+        const T rv = r[i] - alpha * q[i];      // R := R - alpha*Q
+        r[i] = rv;
+        acc += (double)rv * (double)rv;        // rho1 := R+*R (partials)
+    }
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+template <typename T>
+__global__ void cg_update_p_kernel(T *__restrict__ p, const T *__restrict__ r, int64_t N,
+                                   const CgScalars *sc)
+{
+    if (sc->done) return;
+    const T beta = (T)sc->beta;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = r[i] + beta * p[i];             // P := R + (rho1/rho)*P
+}
+
+template <typename T>
+void launch_cg_init(const T *b, T *x, T *r, T *p, int64_t N, double *part, cudaStream_t s)
+{
+    count_launch();
+    cg_init_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(b, x, r, p, N, part);
+}
+
+template <typename T>
+void launch_dot_partials(const T *a, const T *b, int64_t N, double *part,
+                         const int32_t *done, cudaStream_t s)
+{
+    count_launch();
+    dot_partials_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(a, b, N, part, done);
+}
+
+template <typename T>
+void launch_cg_update_xr(T *x, T *r, const T *p, const T *q, int64_t N,
+                         const CgScalars *sc, double *part, cudaStream_t s)
+{
+    count_launch();
+    cg_update_xr_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, q, N, sc, part);
+}
+
+template <typename T>
+void launch_cg_update_p(T *p, const T *r, int64_t N, const CgScalars *sc, cudaStream_t s)
+{
+    count_launch();
+    cg_update_p_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, r, N, sc);
+}
+
+// ---------------------------------------------------------------- finalisers
+// One block of kRedThreads sums the kRedBlocks partials in a fixed order.
+__global__ void __launch_bounds__(kRedThreads)
+cg_finalize_kernel(int which, const double *__restrict__ part, CgScalars *sc, double *hist)
+{
+    if (which != 0 && sc->done) return;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < kRedBlocks; i += kRedThreads) acc += part[i];
+    const double s = block_sum(acc);
+    if (threadIdx.x != 0) return;
+    if (which == 0) {                      // rho := R+*R
+        sc->rho = s;
+        sc->rho0 = s;
+        sc->iters = 0;
+        sc->converged = 0;
+        sc->status = TCA_OK;
+        sc->done = 0;
+        if (hist) hist[0] = s;
+        if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; }
+        else if (s == 0.0) { sc->converged = 1; sc->done = 1; }
+        else if (sc->max_iters <= 0) { sc->done = 1; if (sc->rtol2 > 0.0) sc->status = TCA_NOT_CONVERGED; }
+    } else if (which == 1) {               // alpha := rho / (P+*Q)
+        sc->pq = s;
+        if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; }
+        else if (!(s > 0.0)) { sc->status = TCA_ERR_BREAKDOWN; sc->done = 1; }
+        else sc->alpha = sc->rho / s;
+    } else {                               // rho1 := R+*R; stop test; beta
+        const int k = sc->iters + 1;
+        sc->iters = k;
+        if (hist) hist[k] = s;
+        if (!isfinite(s)) { sc->rho = s; sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
+        if (s == 0.0) { sc->rho = s; sc->converged = 1; sc->done = 1; return; }   // Z12
+        if (sc->rtol2 > 0.0 && s <= sc->rtol2 * sc->rho0) {                      // Z1, Z2
+            sc->rho = s; sc->converged = 1; sc->done = 1; return;
+        }
+        if (k >= sc->max_iters) {
+            sc->rho = s; sc->done = 1;
+            if (sc->rtol2 > 0.0) sc->status = TCA_NOT_CONVERGED;
+            return;
+        }
+        sc->beta = s / sc->rho;
+        sc->rho = s;
+    }
+}
+
+void launch_cg_finalize(int which, const double *part, CgScalars *sc, double *hist,
+                        cudaStream_t s)
+{
+    count_launch();
+    cg_finalize_kernel<<<1, kRedThreads, 0, s>>>(which, part, sc, hist);
+}
+
+// ---------------------------------------------------------------- instantiations
+#define TCA_INST(T)                                                                       \
+    template void launch_band_mode_product<T>(const T *, T *, int64_t, const BandMat &,    \
+                                              int64_t, double, bool, const int32_t *,     \
+                                              cudaStream_t);                              \
+    template void launch_gen_normal<T>(T *, int64_t, int64_t, uint64_t, double, bool,     \
+                                       cudaStream_t);                                     \
+    template void launch_cg_init<T>(const T *, T *, T *, T *, int64_t, double *,          \
+                                    cudaStream_t);                                        \
+    template void launch_dot_partials<T>(const T *, const T *, int64_t, double *,         \
+                                         const int32_t *, cudaStream_t);                  \
+    template void launch_cg_update_xr<T>(T *, T *, const T *, const T *, int64_t,         \
+                                         const CgScalars *, double *, cudaStream_t);      \
+    template void launch_cg_update_p<T>(T *, const T *, int64_t, const CgScalars *,       \
+                                        cudaStream_t);
+
+TCA_INST(double)
+TCA_INST(float)
+
+}  // namespace tca

@@ -1,0 +1,308 @@
+"""Thin ctypes binding of libtca.so (include/tca.h) -- argument marshalling only.
+
+Every numerical step runs in the library's CUDA kernels.  There is no CPU
+fallback: importing this module raises ImportError when libtca.so is missing,
+and every call raises TcaError when the library reports a failure.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtca.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libtca.so not found at {LIB_PATH}: build it with "
+        "`python -m paper_1001_5460_b200.build` (there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+TCA_F64, TCA_F32 = 0, 1
+OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_NOT_SPD, ERR_OOM, ERR_CUDA, ERR_NCCL, \
+    ERR_BREAKDOWN, ERR_NONFINITE, NOT_CONVERGED = range(10)
+
+EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
+            "tca_cg_solve", "tca_solve_host", "tca_operator_destroy", "tca_generate_normal",
+            "tca_forward_model", "tca_status_string", "tca_last_error", "tca_version",
+            "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches"]
+
+_vp = ctypes.c_void_p
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_dpp = ctypes.POINTER(ctypes.POINTER(ctypes.c_double))
+
+
+class CgReport(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("status", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("rho0", ctypes.c_double), ("rho_final", ctypes.c_double),
+                ("seconds", ctypes.c_double),
+                ("rho_history", ctypes.POINTER(ctypes.c_double)),
+                ("history_capacity", ctypes.c_int32), ("pad2", ctypes.c_int32)]
+
+
+class Dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_comm", _vp)]
+
+
+_lib.tca_operator_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _i64p, _i64p, _dpp,
+                                     _dpp, ctypes.c_double, ctypes.c_int,
+                                     ctypes.POINTER(Dist), _vp]
+_lib.tca_operator_query.argtypes = [_vp, _i64p, _i64p, _i64p, _i64p,
+                                    ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                    ctypes.POINTER(ctypes.c_size_t)]
+_lib.tca_apply.argtypes = [_vp, _vp, _vp, _vp]
+_lib.tca_rhs.argtypes = [_vp, _vp, _vp, _vp]
+_lib.tca_cg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32,
+                              ctypes.POINTER(CgReport), _vp]
+_lib.tca_solve_host.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32,
+                                ctypes.POINTER(CgReport), _vp]
+_lib.tca_operator_destroy.argtypes = [_vp]
+_lib.tca_operator_destroy.restype = None
+_lib.tca_generate_normal.argtypes = [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_uint64, ctypes.c_uint32, ctypes.c_double, _vp]
+_lib.tca_forward_model.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_uint64, _vp]
+_lib.tca_status_string.argtypes = [ctypes.c_int]
+_lib.tca_status_string.restype = ctypes.c_char_p
+_lib.tca_last_error.restype = ctypes.c_char_p
+_lib.tca_version.restype = ctypes.c_char_p
+_lib.tca_operator_set_timing.argtypes = [_vp, ctypes.c_int]
+_lib.tca_operator_get_timing.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), _i64p,
+                                         ctypes.c_int]
+_lib.tca_kernel_launches.restype = ctypes.c_int64
+for _name in ("tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
+              "tca_cg_solve", "tca_solve_host", "tca_generate_normal", "tca_forward_model",
+              "tca_operator_set_timing", "tca_operator_get_timing"):
+    getattr(_lib, _name).restype = ctypes.c_int
+
+
+class TcaError(RuntimeError):
+    def __init__(self, status, where):
+        self.status = status
+        msg = _lib.tca_last_error().decode()
+        super().__init__(f"{where}: {_lib.tca_status_string(status).decode()}: {msg}")
+
+
+def _check(st, where, allow=()):
+    if st != OK and st not in allow:
+        raise TcaError(st, where)
+    return st
+
+
+def version() -> str:
+    return _lib.tca_version().decode()
+
+
+def _dtype_code(dtype) -> int:
+    if dtype in ("f64", "float64", np.float64, TCA_F64):
+        return TCA_F64
+    if dtype in ("f32", "float32", np.float32, TCA_F32):
+        return TCA_F32
+    raise ValueError(f"unsupported dtype {dtype!r}")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        torch = _torch()
+        if not torch.cuda.is_available():
+            return 0  # legacy stream; the library reports the missing device itself
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dev_ptr(t, numel, tdtype, name):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.dtype != tdtype:
+        raise ValueError(f"{name} has dtype {t.dtype}, operator uses {tdtype}")
+    if t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {numel}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Operator:
+    """M = (kron_d A_d^T A_d) + lam * sum_d (mode-d L_d^T L_d) on the GPU.
+
+    A: list of m_d x n_d host arrays; L: list of (n_d-2) x n_d arrays or None.
+    """
+
+    def __init__(self, A, L=None, lam=0.0, dtype="f64", stream=None, dist=None):
+        self._h = _vp()
+        A = [np.ascontiguousarray(a, dtype=np.float64) for a in A]
+        D = len(A)
+        self.order = D
+        self.n = tuple(int(a.shape[1]) for a in A)
+        self.m = tuple(int(a.shape[0]) for a in A)
+        self.lam = float(lam)
+        self.dtype_code = _dtype_code(dtype)
+        self.dtype = "f64" if self.dtype_code == TCA_F64 else "f32"
+        n_arr = (ctypes.c_int64 * D)(*self.n)
+        m_arr = (ctypes.c_int64 * D)(*self.m)
+        dp = ctypes.POINTER(ctypes.c_double)
+        A_arr = (dp * D)(*[a.ctypes.data_as(dp) for a in A])
+        keep = [A]
+        L_arr = None
+        if L is not None:
+            Ls = [None if l is None else np.ascontiguousarray(l, dtype=np.float64) for l in L]
+            keep.append(Ls)
+            L_arr = (dp * D)(*[ctypes.cast(None, dp) if l is None or l.size == 0
+                               else l.ctypes.data_as(dp) for l in Ls])
+        dist_p = None
+        if dist is not None:
+            dist_p = ctypes.byref(dist)
+        st = _lib.tca_operator_create(ctypes.byref(self._h), D, n_arr, m_arr, A_arr, L_arr,
+                                      self.lam, self.dtype_code, dist_p,
+                                      _vp(_stream_ptr(stream)))
+        _check(st, "tca_operator_create")
+        q = self.query()
+        self.own_lo, self.own_hi, self.data_lo, self.data_hi = q[:4]
+        self.banded_mask, self.half_bandwidth, self.device_bytes = q[4:]
+        self.local_n = (self.own_hi - self.own_lo,) + self.n[1:]
+        self.local_m = (self.data_hi - self.data_lo,) + self.m[1:]
+        self.N = int(np.prod(self.local_n))
+        self.Mloc = int(np.prod(self.local_m))
+
+    @property
+    def torch_dtype(self):
+        torch = _torch()
+        return torch.float64 if self.dtype_code == TCA_F64 else torch.float32
+
+    def query(self):
+        vals = [ctypes.c_int64() for _ in range(4)]
+        mask = ctypes.c_int()
+        hb = (ctypes.c_int * 4)()
+        nb = ctypes.c_size_t()
+        _check(_lib.tca_operator_query(self._h, *[ctypes.byref(v) for v in vals],
+                                       ctypes.byref(mask), hb, ctypes.byref(nb)),
+               "tca_operator_query")
+        return [v.value for v in vals] + [mask.value, tuple(hb[: self.order]), nb.value]
+
+    def set_timing(self, enable=True):
+        _check(_lib.tca_operator_set_timing(self._h, 1 if enable else 0), "set_timing")
+
+    def get_timing(self, reset=True):
+        """(summed apply device ms, number of timed applies) since the last reset."""
+        ms = ctypes.c_double()
+        cnt = ctypes.c_int64()
+        _check(_lib.tca_operator_get_timing(self._h, ctypes.byref(ms), ctypes.byref(cnt),
+                                            1 if reset else 0), "get_timing")
+        return ms.value, cnt.value
+
+    def close(self):
+        if self._h:
+            _lib.tca_operator_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def empty(self, shape="unknowns"):
+        torch = _torch()
+        shp = self.local_n if shape == "unknowns" else self.local_m
+        return torch.empty(shp, dtype=self.torch_dtype, device="cuda")
+
+    def apply(self, x, y=None, stream=None):
+        """y = M x (device tensors of the local unknown shape)."""
+        if y is None:
+            y = self.empty()
+        _check(_lib.tca_apply(self._h, _dev_ptr(x, self.N, self.torch_dtype, "x"),
+                              _dev_ptr(y, self.N, self.torch_dtype, "y"),
+                              _vp(_stream_ptr(stream))), "tca_apply")
+        return y
+
+    def rhs(self, ydata, b=None, stream=None):
+        """b = (kron_d A_d^T) ydata."""
+        if b is None:
+            b = self.empty()
+        _check(_lib.tca_rhs(self._h, _dev_ptr(ydata, self.Mloc, self.torch_dtype, "ydata"),
+                            _dev_ptr(b, self.N, self.torch_dtype, "b"),
+                            _vp(_stream_ptr(stream))), "tca_rhs")
+        return b
+
+    def cg_solve(self, b, x=None, rtol=0.0, max_iters=100, history=False, stream=None,
+                 raise_on=("breakdown", "nonfinite")):
+        """Fig. 2 CG from x0 = 0.  Returns (x, report dict)."""
+        if x is None:
+            x = self.empty()
+        rep = CgReport()
+        hist = None
+        if history:
+            hist = np.zeros(max_iters + 1)
+            rep.rho_history = hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+            rep.history_capacity = max_iters + 1
+        st = _lib.tca_cg_solve(self._h, _dev_ptr(b, self.N, self.torch_dtype, "b"),
+                               _dev_ptr(x, self.N, self.torch_dtype, "x"), float(rtol),
+                               int(max_iters), ctypes.byref(rep), _vp(_stream_ptr(stream)))
+        allow = [NOT_CONVERGED]
+        if "breakdown" not in raise_on:
+            allow.append(ERR_BREAKDOWN)
+        if "nonfinite" not in raise_on:
+            allow.append(ERR_NONFINITE)
+        _check(st, "tca_cg_solve", allow=allow)
+        out = dict(iterations=rep.iterations, converged=bool(rep.converged), status=rep.status,
+                   rho0=rep.rho0, rho_final=rep.rho_final, seconds=rep.seconds)
+        if hist is not None:
+            out["rho_history"] = hist[: rep.iterations + 1]
+        return x, out
+
+    def solve_host(self, ydata_host, x_host, rtol=0.0, max_iters=100, stream=None):
+        """End-to-end solve from host buffers (torch CPU tensors, pinned recommended)."""
+        torch = _torch()
+        for t, numel, name in ((ydata_host, self.Mloc, "ydata_host"), (x_host, self.N, "x_host")):
+            if t.is_cuda or not t.is_contiguous() or t.dtype != self.torch_dtype or t.numel() != numel:
+                raise ValueError(f"{name}: expected a contiguous host tensor of {numel} {self.torch_dtype}")
+        rep = CgReport()
+        st = _lib.tca_solve_host(self._h, _vp(ydata_host.data_ptr()), _vp(x_host.data_ptr()),
+                                 float(rtol), int(max_iters), ctypes.byref(rep),
+                                 _vp(_stream_ptr(stream)))
+        _check(st, "tca_solve_host", allow=[NOT_CONVERGED])
+        del torch
+        return dict(iterations=rep.iterations, converged=bool(rep.converged), status=rep.status,
+                    rho0=rep.rho0, rho_final=rep.rho_final, seconds=rep.seconds)
+
+    def forward_model(self, x=None, ydata=None, sigma=0.01, seed=1, stream=None):
+        """ydata = (kron A_d) x + sigma * noise(seed); x None -> x_true(seed) generated on device."""
+        if ydata is None:
+            ydata = self.empty("data")
+        xp = None if x is None else _dev_ptr(x, int(np.prod(self.n)), self.torch_dtype, "x")
+        _check(_lib.tca_forward_model(self._h, xp,
+                                      _dev_ptr(ydata, self.Mloc, self.torch_dtype, "ydata"),
+                                      float(sigma), int(seed), _vp(_stream_ptr(stream))),
+               "tca_forward_model")
+        return ydata
+
+
+def kernel_launches() -> int:
+    """Process-wide count of CUDA kernel launches issued by libtca."""
+    return int(_lib.tca_kernel_launches())
+
+
+def generate_normal(out, seed, stream_id, offset=0, scale=1.0, stream=None):
+    """out[i] = scale * normal(seed, stream_id, offset + i) on the device."""
+    torch = _torch()
+    code = TCA_F64 if out.dtype == torch.float64 else TCA_F32
+    _check(_lib.tca_generate_normal(_dev_ptr(out, out.numel(), out.dtype, "out"), code,
+                                    out.numel(), int(offset), int(seed), int(stream_id),
+                                    float(scale), _vp(_stream_ptr(stream))),
+           "tca_generate_normal")
+    return out
+
+
+def exported_symbols():
+    """Names from include/tca.h that the loaded library exports."""
+    return [n for n in EXPORTED if hasattr(_lib, n)]

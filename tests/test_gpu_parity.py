@@ -1,0 +1,259 @@
+"""GPU parity: libtca (through the C ABI) vs the CPU oracle on identical
+seeded inputs from synth/.  Tolerances are BASELINE.json north_star's:
+fp64 apply <= 1e-12 relative L2, CG <= 1e-8 at matched iteration count,
+fp32 <= 1e-5; rhs (not listed there) uses the apply's 1e-12."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def tca():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1001_5460_b200 import tca as t
+    return t
+
+
+def relerr(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300)
+
+
+def to_dev(x, dtype=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype)
+
+
+def to_host(t):
+    torch.cuda.synchronize()
+    return t.double().cpu().numpy()
+
+
+# shapes: configs 0 and 2, ragged tails over several tiles, degenerate orders/extents
+APPLY_CASES = [
+    ("cfg0", (12, 12, 12), (20, 20, 20), "bspline", 1e-2),
+    ("cfg2", (32, 32, 32, 16), (64, 64, 64, 32), "bspline", 1e-2),
+    ("ragged4", (13, 11, 37, 15), (26, 22, 74, 30), "bspline", 1e-3),
+    ("ragged4b", (9, 70, 5, 7), (18, 140, 10, 14), "bspline", 0.5),
+    ("n4_32", (6, 20, 19, 32), (9, 30, 28, 48), "bspline", 1e-3),
+    ("tiny_band", (4, 3, 5, 2), (7, 5, 9, 4), "bspline", 0.3),
+    ("order1", (17,), (30,), "bspline", 0.1),
+    ("order2", (9, 14), (16, 25), "bspline", 0.1),
+    ("ones", (1, 1, 1, 1), (3, 3, 3, 3), "bspline", 0.0),
+    ("dense3", (20, 24, 16), (30, 32, 24), "gauss", 1e-3),
+    ("dense_cfg1", (48, 48, 48), (64, 64, 64), "gauss", 1e-3),
+]
+
+
+def make(case, tca, dtype="f64", seed=1):
+    name, n, m, basis, lam = case
+    A, L = synth.mode_matrices(n, m, basis=basis, seed=seed)
+    return A, L, lam, tca.Operator(A, L, lam, dtype=dtype), oracle.Operator(A, L, lam)
+
+
+@pytest.mark.parametrize("case", APPLY_CASES, ids=[c[0] for c in APPLY_CASES])
+def test_apply_f64(case, tca):
+    A, L, lam, g, o = make(case, tca)
+    x = synth.random_tensor(case[1], seed=5)
+    y = to_host(g.apply(to_dev(x)))
+    assert relerr(y, o.apply(x)) <= 1e-12
+
+
+@pytest.mark.parametrize("case", APPLY_CASES, ids=[c[0] for c in APPLY_CASES])
+def test_apply_f32(case, tca):
+    A, L, lam, g, o = make(case, tca, dtype="f32")
+    x = synth.random_tensor(case[1], seed=6)
+    y = to_host(g.apply(to_dev(x, torch.float32)))
+    assert relerr(y, o.apply(x)) <= 1e-5
+
+
+@pytest.mark.parametrize("case", APPLY_CASES[:5] + APPLY_CASES[9:], ids=[c[0] for c in APPLY_CASES[:5] + APPLY_CASES[9:]])
+def test_rhs_f64_and_f32(case, tca):
+    A, L, lam, g, o = make(case, tca)
+    yd = synth.data(A, case[1], case[2], seed=2)
+    ref = o.rhs(yd)
+    b = to_host(g.rhs(to_dev(yd)))
+    assert relerr(b, ref) <= 1e-12
+    g32 = tca.Operator(A, L, lam, dtype="f32")
+    b32 = to_host(g32.rhs(to_dev(yd, torch.float32)))
+    assert relerr(b32, ref) <= 1e-5
+
+
+def test_symmetry_and_positivity_through_gpu_apply(tca):
+    for cfg in (0, 2):
+        c = synth.CONFIGS[cfg]
+        A, L = synth.mode_matrices(c)
+        g = tca.Operator(A, L, c.lam)
+        x = synth.random_tensor(c.n, seed=21)
+        y = synth.random_tensor(c.n, seed=22, stream=8)
+        Mx, My = to_host(g.apply(to_dev(x))), to_host(g.apply(to_dev(y)))
+        a, b = oracle.dot(x, My), oracle.dot(Mx, y)
+        assert abs(a - b) <= 1e-13 * np.linalg.norm(x) * np.linalg.norm(My)
+        assert oracle.dot(x, Mx) > 0
+
+
+def test_apply_linearity_and_determinism(tca):
+    case = APPLY_CASES[2]
+    A, L, lam, g, o = make(case, tca)
+    x = synth.random_tensor(case[1], seed=3)
+    z = synth.random_tensor(case[1], seed=4, stream=8)
+    y1 = to_host(g.apply(to_dev(x)))
+    y2 = to_host(g.apply(to_dev(x)))
+    assert np.array_equal(y1, y2)
+    yz = to_host(g.apply(to_dev(z)))
+    ylin = to_host(g.apply(to_dev(2.0 * x - 3.0 * z)))
+    assert relerr(ylin, 2.0 * y1 - 3.0 * yz) <= 1e-12
+
+
+# ------------------------------------------------------------------ CG
+def _cg_pair(cfg, tca, dtype="f64", max_iters=None):
+    c = synth.CONFIGS[cfg]
+    A, L = synth.mode_matrices(c)
+    o = oracle.Operator(A, L, c.lam)
+    b = o.rhs(synth.data(A, c.n, c.m, seed=1))
+    g = tca.Operator(A, L, c.lam, dtype=dtype)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    iters = c.max_iters if max_iters is None else max_iters
+    xg, rep = g.cg_solve(to_dev(b, tdt), rtol=c.rtol, max_iters=iters, history=True)
+    return c, o, b, to_host(xg), rep
+
+
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_cg_f64_matched_iterations(cfg, tca):
+    c, o, b, xg, rep = _cg_pair(cfg, tca)
+    k = rep["iterations"]
+    if c.rtol > 0:
+        assert rep["converged"]
+        _, k_nat, _, _ = o.cg(b, rtol=c.rtol, max_iters=c.max_iters)
+        assert abs(k - k_nat) <= 1
+    else:
+        assert k == c.max_iters or rep["rho_history"][-1] == 0.0
+    xo, ko, st, hist = o.cg(b, rtol=0.0, max_iters=k)
+    assert ko == k
+    assert relerr(xg, xo) <= 1e-8
+    assert np.allclose(rep["rho_history"][: min(len(hist), 20)], hist[:20], rtol=1e-6)
+
+
+def test_cg_f64_dense_cfg1(tca):
+    c, o, b, xg, rep = _cg_pair(1, tca)
+    assert rep["converged"]
+    k = rep["iterations"]
+    xo, ko, st, hist = o.cg(b, rtol=0.0, max_iters=k)
+    assert relerr(xg, xo) <= 1e-8
+
+
+def test_cg_f32_cfg2(tca):
+    c, o, b, xg, rep = _cg_pair(2, tca, dtype="f32")
+    xo, _, _, _ = o.cg(b, rtol=0.0, max_iters=rep["iterations"])
+    assert relerr(xg, xo) <= 1e-5
+
+
+def test_cg_edge_cases(tca):
+    c = synth.CONFIGS[0]
+    A, L = synth.mode_matrices(c)
+    g = tca.Operator(A, L, c.lam)
+    xg, rep = g.cg_solve(torch.zeros(c.n, dtype=torch.float64, device="cuda"), rtol=1e-10,
+                         max_iters=10)
+    assert rep["iterations"] == 0 and rep["converged"]
+    assert torch.count_nonzero(xg).item() == 0
+    b = to_dev(synth.random_tensor(c.n, 3))
+    xg, rep = g.cg_solve(b, rtol=1e-30, max_iters=3)
+    assert rep["status"] == tca.NOT_CONVERGED and rep["iterations"] == 3
+    xg, rep = g.cg_solve(b, rtol=0.0, max_iters=0)
+    assert rep["iterations"] == 0
+    # SPEC worked example through the ABI: order 1, rho == 0 guard (Z12)
+    T = np.array([[2.0, -1, 0], [-1, 2, -1], [0, -1, 2]])
+    A1 = np.linalg.cholesky(T).T
+    g1 = tca.Operator([A1], None, 0.0)
+    xg, rep = g1.cg_solve(to_dev(np.ones(3)), rtol=1e-15, max_iters=10)
+    assert np.abs(to_host(xg) - [1.5, 2.0, 1.5]).max() <= 1e-12
+    assert rep["iterations"] <= 3 and rep["converged"]
+
+
+def test_not_spd_rejected(tca):
+    A = [synth.bspline_matrix(6, 10), np.ones((5, 3)), synth.bspline_matrix(4, 8)]
+    with pytest.raises(tca.TcaError) as ei:
+        tca.Operator(A, None, 0.0)
+    assert ei.value.status == tca.ERR_NOT_SPD
+
+
+def test_matrix_free_device_bytes(tca):
+    c = synth.CONFIGS[2]
+    A, L = synth.mode_matrices(c)
+    g = tca.Operator(A, L, c.lam)
+    assert g.device_bytes <= 6 * c.N * 8 + 10 * sum(nd * nd for nd in c.n) * 8 + (1 << 20)
+    assert g.banded_mask == 0b1111 and g.half_bandwidth == (3, 3, 3, 3)
+
+
+# ------------------------------------------------------------------ generator
+def test_generator_matches_synth(tca):
+    for dt, tol in ((torch.float64, 4e-15), (torch.float32, 1e-7)):
+        out = torch.empty(100003, dtype=dt, device="cuda")
+        tca.generate_normal(out, seed=7, stream_id=1, offset=12345, scale=0.5)
+        ref = 0.5 * synth.normals(7, 1, 100003, offset=12345)
+        got = to_host(out)
+        assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-3)) <= tol
+
+
+def test_forward_model_matches_synth(tca):
+    n, m = (9, 8, 7, 6), (18, 16, 14, 12)
+    A, L = synth.mode_matrices(n, m)
+    g = tca.Operator(A, L, 0.01)
+    yd = to_host(g.forward_model(None, sigma=0.01, seed=3))
+    ref = synth.data(A, n, m, seed=3)
+    assert relerr(yd, ref) <= 1e-13
+
+
+# ------------------------------------------------------------------ full size (cfg 3)
+@pytest.fixture(scope="module")
+def cfg3_inputs():
+    c = synth.CONFIGS[3]
+    A, L = synth.mode_matrices(c)
+    x = synth.random_tensor(c.n, seed=9)
+    return c, A, L, x
+
+
+def _sample_points(n, count, seed=0):
+    rng = np.random.default_rng(seed)
+    pts = [tuple(rng.integers(0, nd) for nd in n) for _ in range(count)]
+    # corners / faces (boundary rows of every band)
+    for corner in [(0, 0, 0, 0), tuple(nd - 1 for nd in n), (1, 2, 0, 14), (127, 0, 64, 7),
+                   (2, 127, 126, 0), (64, 1, 127, 13)]:
+        pts.append(corner)
+    return pts
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-12), ("f32", 1e-5)])
+def test_full_size_cfg3_apply_sampled(dtype, tol, tca, cfg3_inputs):
+    c, A, L, x = cfg3_inputs
+    g = tca.Operator(A, L, c.lam, dtype=dtype)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    y = to_host(g.apply(to_dev(x, tdt)))
+    o = oracle.Operator(A, L, c.lam)
+    pts = _sample_points(c.n, 200)
+    want = o.apply_points(x, pts)
+    got = np.array([y[p] for p in pts])
+    scale = np.linalg.norm(want) / np.sqrt(len(want))
+    assert np.max(np.abs(got - want)) <= tol * 10 * scale
+    assert relerr(got, want) <= tol
+
+
+def test_full_size_cfg3_cg_residual_sampled(tca, cfg3_inputs):
+    c, A, L, x = cfg3_inputs
+    g = tca.Operator(A, L, c.lam)
+    b = x  # any right-hand side; the solution must satisfy M x = b
+    xg, rep = g.cg_solve(to_dev(b), rtol=0.0, max_iters=c.max_iters)
+    assert rep["iterations"] == c.max_iters
+    xh = to_host(xg)
+    o = oracle.Operator(A, L, c.lam)
+    pts = _sample_points(c.n, 100, seed=1)
+    Mx = o.apply_points(xh, pts)
+    bb = np.array([b[p] for p in pts])
+    assert np.max(np.abs(Mx - bb)) <= 1e-6 * np.abs(b).max()
