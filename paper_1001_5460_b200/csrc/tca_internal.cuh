@@ -63,9 +63,16 @@ struct CgScalars {
     int32_t pad;
 };
 
+// A cached TMA tensor map (CUtensorMap is 128 bytes, 64-byte aligned).
+struct alignas(64) TmapSlot {
+    uint64_t map[16];
+    const void *ptr = nullptr;
+};
+
 }  // namespace tca
 
 struct tca_operator {
+    std::vector<tca::TmapSlot> tmaps;    // TMA descriptors of recent apply inputs
     int order = 0;
     int64_t n[tca::kD] = {1, 1, 1, 1};   // global unknown extents (padded)
     int64_t m[tca::kD] = {1, 1, 1, 1};   // global data extents (padded)
