@@ -182,10 +182,16 @@ static tca_status apply_multipass_t(const tca_operator *op, const T *x, T *y,
     return TCA_OK;
 }
 
-tca_status apply_multipass(const tca_operator *op, const void *x, void *y,
+tca_status apply_multipass(const tca_operator *op_c, const void *x, void *y,
                            const int32_t *done, cudaStream_t s)
 {
-    if (!op->t0) return fail(TCA_ERR_INVALID_ARG, "multi-pass workspace missing");
+    tca_operator *op = const_cast<tca_operator *>(op_c);
+    if (!op->t0) {   // lazily: only operators whose apply cannot take the fused path use it
+        const size_t vb = (size_t)op->N * op->esize;
+        TCA_CUDA_TRY(cudaMalloc(&op->t0, vb));
+        TCA_CUDA_TRY(cudaMalloc(&op->t1, vb));
+        op->device_bytes += 2 * vb;
+    }
     if (op->dtype == TCA_F64)
         return apply_multipass_t<double>(op, (const double *)x, (double *)y, done, s);
     return apply_multipass_t<float>(op, (const float *)x, (float *)y, done, s);
@@ -194,7 +200,7 @@ tca_status apply_multipass(const tca_operator *op, const void *x, void *y,
 static tca_status apply_dispatch(const tca_operator *op, const void *x, void *y,
                                  const int32_t *done, cudaStream_t s)
 {
-    if (op->apply_path == 1) return launch_fused_apply(op, x, y, done, s);
+    if (op->apply_path == 1 && fused_pointers_ok(x, y)) return launch_fused_apply(op, x, y, done, s);
     return apply_multipass(op, x, y, done, s);
 }
 
@@ -420,10 +426,8 @@ void tca_operator_destroy(tca_operator *op)
         free_band(op->Rm[d]);
         free_band(op->At[d]);
         free_band(op->Af[d]);
-        if (op->tapG[d]) cudaFree(op->tapG[d]);
-        if (op->tapR[d]) cudaFree(op->tapR[d]);
     }
-    void *bufs[] = {op->r, op->p, op->q, op->t0, op->t1, op->part, op->sc, op->hist};
+    void *bufs[] = {op->r, op->p, op->q, op->t0, op->t1, op->part, op->sc, op->hist, op->tmap_dev};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (op->sc_host) cudaFreeHost(op->sc_host);
@@ -510,19 +514,16 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
         if (st != TCA_OK) break;
         st = make_band(dtype, Ad, md, nd, -1, &op->Af[d], &bytes);
         if (st != TCA_OK) break;
-        // offset-form taps for the fused banded kernel
-        std::vector<double> tg((size_t)nd * 7, 0.0), tr((size_t)nd * 5, 0.0);
+        // symmetric band rows for the fused banded kernel
+        op->bandG[d].assign((size_t)nd * 4, 0.0);
+        op->bandR[d].assign((size_t)nd * 3, 0.0);
         for (int r = 0; r < nd; ++r) {
-            for (int k = -kHG; k <= kHG; ++k)
-                if (r + k >= 0 && r + k < nd && std::abs(k) <= op->hbG[d])
-                    tg[(size_t)r * 7 + k + kHG] = G[(size_t)r * nd + r + k];
+            for (int k = 0; k <= kHG; ++k)
+                if (r + k < nd && k <= op->hbG[d]) op->bandG[d][(size_t)r * 4 + k] = G[(size_t)r * nd + r + k];
             if (op->has_reg[d])
-                for (int k = -kHR; k <= kHR; ++k)
-                    if (r + k >= 0 && r + k < nd) tr[(size_t)r * 5 + k + kHR] = lambda * R[(size_t)r * nd + r + k];
+                for (int k = 0; k <= kHR; ++k)
+                    if (r + k < nd) op->bandR[d][(size_t)r * 3 + k] = lambda * R[(size_t)r * nd + r + k];
         }
-        st = upload_dtype(dtype, tg, &op->tapG[d], &bytes);
-        if (st != TCA_OK) break;
-        st = upload_dtype(dtype, tr, &op->tapR[d], &bytes);
     }
     if (st != TCA_OK) {
         tca_operator_destroy(op);
@@ -536,15 +537,14 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
     op->nloc1 = op->own_hi - op->own_lo;
     op->N = op->nloc1 * op->n[1] * op->n[2] * op->n[3];
     op->Mloc = (op->data_hi - op->data_lo) * op->m[1] * op->m[2] * op->m[3];
-    op->apply_path = fused_apply_supported(op) ? 1 : 0;
+    op->apply_path = fused_shape_supported(op) ? 1 : 0;
+    if (op->apply_path == 1) fused_prepare(op);
 
     const size_t vb = (size_t)op->N * op->esize;
     cudaError_t e = cudaSuccess;
     e = cudaMalloc(&op->r, vb);
     if (e == cudaSuccess) e = cudaMalloc(&op->p, vb);
     if (e == cudaSuccess) e = cudaMalloc(&op->q, vb);
-    if (e == cudaSuccess && op->apply_path == 0) e = cudaMalloc(&op->t0, vb);
-    if (e == cudaSuccess && op->apply_path == 0) e = cudaMalloc(&op->t1, vb);
     if (e == cudaSuccess) e = cudaMalloc(&op->part, sizeof(double) * kRedBlocks * 2);
     if (e == cudaSuccess) e = cudaMalloc(&op->sc, sizeof(CgScalars));
     if (e == cudaSuccess) e = cudaMallocHost(&op->sc_host, sizeof(CgScalars));
@@ -556,7 +556,7 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
         tca_operator_destroy(op);
         return rs;
     }
-    bytes += vb * (op->apply_path == 0 ? 5 : 3) + sizeof(double) * kRedBlocks * 2 + sizeof(CgScalars);
+    bytes += vb * 3 + sizeof(double) * kRedBlocks * 2 + sizeof(CgScalars);
     op->device_bytes = bytes;
     *out = op;
     return TCA_OK;

@@ -1,0 +1,223 @@
+// tca_band.cu -- host glue of the fused banded apply (tca_band_impl.cuh):
+// support check, kernel-parameter tap tables, TMA tensor maps (cached per
+// pointer) and dispatch to the per-dtype instantiation units
+// tca_band_f64.cu / tca_band_f32.cu.
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "tca_band_impl.cuh"
+#include "tca_fused.cuh"
+
+namespace tca {
+namespace band {
+extern template tca_status launch_dispatch<double>(const tca_operator *, const Params<double> &, cudaStream_t,
+                                                   const CUtensorMap *, const CUtensorMap *);
+extern template tca_status launch_dispatch<float>(const tca_operator *, const Params<float> &, cudaStream_t,
+                                                  const CUtensorMap *, const CUtensorMap *);
+extern template int t3_for<double>(int);
+extern template int t3_for<float>(int);
+extern template int boxw_for<double>(int);
+extern template int boxw_for<float>(int);
+}  // namespace band
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    });
+    return fn;
+}
+
+int t3_of(const tca_operator *op)
+{
+    return op->dtype == TCA_F64 ? band::t3_for<double>((int)op->n[3]) : band::t3_for<float>((int)op->n[3]);
+}
+
+// Rows of the four tap tables (mode 4 first so its offsets are compile-time).
+struct TableLayout {
+    int rows[kD];
+    int off[kD];
+    int total;
+};
+
+TableLayout table_layout(const tca_operator *op)
+{
+    TableLayout L{};
+    const int t3 = t3_of(op);
+    const int extra[kD] = {0, band::T2, t3, 0};
+    const int order[kD] = {3, 2, 1, 0};
+    int off = 0;
+    for (int i = 0; i < kD; ++i) {
+        const int d = order[i];
+        L.rows[d] = (int)(d == 0 ? op->nloc1 : op->n[d]) + extra[d] + 2 * band::PADR + 1;
+        L.off[d] = off;
+        off += L.rows[d];
+    }
+    L.total = off;
+    return L;
+}
+
+template <typename T>
+void build_params(const tca_operator *op, std::vector<unsigned char> &blob)
+{
+    blob.assign(sizeof(band::Params<T>), 0);
+    auto *p = reinterpret_cast<band::Params<T> *>(blob.data());
+    const TableLayout L = table_layout(op);
+    const int t3 = t3_of(op);
+    p->n1 = (int)op->nloc1;
+    p->n2 = (int)op->n[1];
+    p->n3 = (int)op->n[2];
+    p->tiles3 = (p->n3 + t3 - 1) / t3;
+    const long long tiles2 = (p->n2 + band::T2 - 1) / band::T2;
+    p->total = tiles2 * p->tiles3 * p->n1;
+    p->off1 = L.off[0];
+    p->off2 = L.off[1];
+    p->off3 = L.off[2];
+    for (int d = 0; d < kD; ++d) {
+        const int nd = (int)(d == 0 ? op->nloc1 : op->n[d]);
+        const int row0 = d == 0 ? (int)op->own_lo : 0;   // mode-1 rows of this shard
+        for (int r = 0; r < nd; ++r) {
+            T *rec = p->taps + (size_t)(L.off[d] + r + band::PADR) * band::REC;
+            for (int k = 0; k < 4; ++k) rec[k] = (T)op->bandG[d][(size_t)(row0 + r) * 4 + k];
+            for (int k = 0; k < 3; ++k) rec[4 + k] = (T)op->bandR[d][(size_t)(row0 + r) * 3 + k];
+            // a band entry G[r, r+k] with r+k beyond this shard's last row stays (the
+            // kernel never pairs it with an in-domain input: TMA zero-fills those slabs)
+        }
+    }
+}
+
+bool tables_fit(const tca_operator *op)
+{
+    const size_t es = op->esize;
+    return (size_t)table_layout(op).total * band::REC * es <= (size_t)band::TAP_BYTES;
+}
+
+tca_status make_tmap(const tca_operator *op, const void *ptr, int kind, CUtensorMap *m)
+{
+    auto encode = get_encode();
+    if (!encode) return fail(TCA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const int n4 = (int)op->n[3];
+    const int t3 = t3_of(op);
+    cuuint64_t dims[3] = {(cuuint64_t)(op->n[2] * op->n[3]), (cuuint64_t)op->n[1], (cuuint64_t)op->nloc1};
+    cuuint64_t strides[2] = {(cuuint64_t)(op->n[2] * op->n[3] * op->esize),
+                             (cuuint64_t)(op->n[1] * op->n[2] * op->n[3] * op->esize)};
+    cuuint32_t box[3];
+    if (kind == 0) {
+        const int boxw = op->dtype == TCA_F64 ? band::boxw_for<double>(n4) : band::boxw_for<float>(n4);
+        box[0] = (cuuint32_t)boxw;
+        box[1] = 1;
+        box[2] = 1;
+    } else {
+        box[0] = (cuuint32_t)(t3 * n4);
+        box[1] = band::T2;
+        box[2] = 1;
+    }
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode(m, op->dtype == TCA_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        3, const_cast<void *>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(TCA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return TCA_OK;
+}
+
+// Per-operator cache of tensor maps keyed by (pointer, kind); the descriptors
+// live in a device buffer of kTmapSlots slots (round-robin replacement).
+const CUtensorMap *cached_tmap(const tca_operator *op_c, const void *ptr, int kind, tca_status *st)
+{
+    tca_operator *op = const_cast<tca_operator *>(op_c);
+    for (auto &e : op->tmaps)
+        if (e.ptr == ptr && e.kind == kind) return reinterpret_cast<const CUtensorMap *>(op->tmap_dev) + e.slot;
+    if (!op->tmap_dev) {
+        cudaError_t e = cudaMalloc(&op->tmap_dev, sizeof(CUtensorMap) * kTmapSlots);
+        if (e != cudaSuccess) { *st = cuda_fail(e, "tensor-map buffer"); return nullptr; }
+    }
+    TmapSlot slot;
+    slot.ptr = ptr;
+    slot.kind = kind;
+    *st = make_tmap(op, ptr, kind, reinterpret_cast<CUtensorMap *>(slot.map));
+    if (*st != TCA_OK) return nullptr;
+    if ((int)op->tmaps.size() < kTmapSlots) {
+        slot.slot = (int)op->tmaps.size();
+        op->tmaps.push_back(slot);
+    } else {
+        slot.slot = op->tmap_next;
+        for (auto &e : op->tmaps)
+            if (e.slot == slot.slot) e = slot;
+        op->tmap_next = (op->tmap_next + 1) % kTmapSlots;
+    }
+    // synchronous: the slot may still be read by a kernel in flight (stream order
+    // on the legacy stream is not guaranteed), so wait for the device first
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess)
+        e = cudaMemcpy(reinterpret_cast<CUtensorMap *>(op->tmap_dev) + slot.slot, slot.map, sizeof(CUtensorMap),
+                       cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { *st = cuda_fail(e, "tensor-map upload"); return nullptr; }
+    return reinterpret_cast<const CUtensorMap *>(op->tmap_dev) + slot.slot;
+}
+
+template <typename T>
+tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_t *done, cudaStream_t s)
+{
+    tca_status st = TCA_OK;
+    const CUtensorMap *xm = cached_tmap(op, x, 0, &st);
+    if (!xm) return st;
+    const CUtensorMap *ym = cached_tmap(op, y, 1, &st);
+    if (!ym) return st;
+    // the parameter block is prebuilt at create; patch the per-call pointers
+    band::Params<T> *p = reinterpret_cast<band::Params<T> *>(const_cast<unsigned char *>(op->band_params.data()));
+    p->x = (const T *)x;
+    p->y = (T *)y;
+    p->done = done;
+    {
+        static const char *e = getenv("TCA_BAND_DEBUG");
+        p->dbg = e ? atoi(e) : 0;
+    }
+    return band::launch_dispatch<T>(op, *p, s, xm, ym);
+}
+
+}  // namespace
+
+bool fused_shape_supported(const tca_operator *op)
+{
+    if (!op->all_banded) return false;
+    const int n4 = (int)op->n[3];
+    if (t3_of(op) == 0) return false;
+    (void)n4;
+    if ((op->n[2] * op->n[3] * op->esize) % 16 != 0) return false;   // TMA global stride rule
+    if (op->nloc1 <= 0 || op->nloc1 > (1ll << 30) || op->n[1] > (1ll << 30)) return false;
+    if (!tables_fit(op)) return false;
+    return get_encode() != nullptr;
+}
+
+tca_status fused_prepare(tca_operator *op)
+{
+    if (op->dtype == TCA_F64) build_params<double>(op, op->band_params);
+    else build_params<float>(op, op->band_params);
+    return TCA_OK;
+}
+
+bool fused_pointers_ok(const void *x, const void *y)
+{
+    return ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
+}
+
+tca_status launch_fused_apply(const tca_operator *op, const void *x, void *y, const int32_t *done, cudaStream_t s)
+{
+    if (op->dtype == TCA_F64) return launch_t<double>(op, x, y, done, s);
+    return launch_t<float>(op, x, y, done, s);
+}
+
+}  // namespace tca

@@ -1,0 +1,524 @@
+// tca_band_impl.cuh -- fused banded operator apply, one HBM pass.
+// Instantiated per dtype in tca_band_f64.cu / tca_band_f32.cu.
+//
+//   q = (G_1 (x) G_2 (x) G_3 (x) G_4) p + sum_d (mode-d lambda R_d) p
+//
+// Eq. 4 applies the separable operator as successive
+// one-dimensional transformations; Eq. 5 lets us pick their
+// order; Eq. 9 gives the Kronecker-sum regulariser.  Every
+// G_d has half-bandwidth <= 3 and every R_d <= 2 (checked at create).
+//
+// B200 design:
+//   * A CTA (256 threads, 1 per SM, persistent) owns a tile of T2 = 8 mode-2
+//     rows x T3 mode-3 columns x all n4 and STREAMS mode 1: input slab j
+//     (i1 = j) is staged in shared memory once by TMA (halo 3 in i2 and i3,
+//     out-of-domain boxes zero-filled = the truncated band of reading Z15).
+//   * In-slice modes are applied in the order 2 -> 3 -> 4 (mode 2 on the
+//     halo-extended columns):
+//       pass A  column owner along i2:  U2 = G2 p, RA = lambda R2 p
+//       pass B  8 outputs along i3:     U3 = G3 U2, RB = RA + lambda R3 p
+//       pass C  E <= 8 outputs along i4 (the ring owner):
+//               S = G4 U3 + lambda R4 p + RB, then mode 1 as a 6-slot
+//               register ring over j (G1 S and lambda R1 p), and emission of
+//               the finished output slab j-3 to a staging buffer that one
+//               thread stores with a TMA bulk tensor store.
+//   * Every band loop is written in PUSH form (one input value, consecutive
+//     DFMAs into the outputs it touches) and every tap is a kernel-parameter
+//     (constant bank) operand -- compile-time offsets for mode 4, uniform
+//     runtime offsets (LDCU) for modes 1-3 -- so a DFMA reads one or two
+//     register-file operands (profiles/r01_microbench_fp64_operands.txt: three
+//     RF operands cap DFMA at ~60 % of peak).
+//   * Two CTA barriers per slab; the staged slabs are NSTAGE deep (mbarrier
+//     completion), the output staging is double-buffered.
+//   * A CTA owns a contiguous range of (tile, i1) units; a range that starts
+//     or ends inside a tile pays 6 ramp slabs (mode-1 halo).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "tca_internal.cuh"
+
+namespace tca {
+namespace band {
+
+constexpr int NTHR = 256;
+constexpr int T2 = 8;            // mode-2 rows per tile
+constexpr int PR = T2 + 6;       // staged rows (halo 3 + 3)
+constexpr int REC = 7;           // tap record per row: G[r,r..r+3], lambda R[r,r..r+2]
+constexpr int PADR = 6;          // zero rows below each table (row r at record off + r + PADR)
+constexpr int TAP_BYTES = 30 * 1024;
+
+template <typename T>
+struct Params {
+    const T *x;
+    T *y;
+    const int32_t *done;
+    long long total;       // tiles * n1 units
+    int n1, n2, n3, tiles3;
+    int off3, off2, off1;  // record offsets (rows) of the mode-3/2/1 tables; mode 4 at 0
+    int dbg;     // debug switches (0 in production)
+    int pad;
+    T taps[TAP_BYTES / sizeof(T)];
+};
+
+template <typename T, int N4>
+struct Cfg {
+    static constexpr int NSEG = (N4 + 7) / 8;        // ring segments along i4
+    static constexpr int E = (N4 + NSEG - 1) / NSEG; // elements per segment (<= 8)
+    static constexpr int T3 = 32 / NSEG;             // mode-3 columns per tile
+    static_assert(32 % NSEG == 0, "unsupported n4");
+    static constexpr int W = (T3 + 6) * N4;          // halo-extended flat columns
+    static constexpr int WI = T3 * N4;               // interior flat columns
+    static constexpr int VEC = 16 / (int)sizeof(T);  // TMA coordinate granularity (16 B)
+    static constexpr int UNIT = 128 / (int)sizeof(T);
+    static constexpr int NEED = W + VEC - 1;
+    static constexpr int boxw_for_nb(int nb) { return ((NEED + nb - 1) / nb + UNIT - 1) / UNIT * UNIT; }
+    static constexpr int pick_nb()
+    {
+        int best = 1, tot = 1 << 30;
+        for (int nb = 1; nb <= 12; ++nb) {
+            const int bw = boxw_for_nb(nb);
+            if (bw <= 256 && nb * bw < tot) { tot = nb * bw; best = nb; }
+        }
+        return best;
+    }
+    static constexpr int NB = pick_nb();
+    static constexpr int BOXW = boxw_for_nb(NB);
+    static constexpr int PP = NB * BOXW;             // staged row pitch
+    static constexpr int BL = 8;                     // pass-B outputs per item
+    static constexpr int NBLK = T3 / BL;
+    static constexpr int LPB = T2 * N4;              // pass-B lanes per block
+    static constexpr int WPB = (LPB + 31) / 32;
+    static constexpr size_t al(size_t e) { return (e * sizeof(T) + 127) / 128 * 128 / sizeof(T); }
+    static constexpr size_t U2E = al((size_t)T2 * W);    // smem buffers, each 128-B aligned
+    static constexpr size_t WIE = al((size_t)T2 * WI);
+    static constexpr size_t rest_elems = U2E + 5 * WIE;
+    static constexpr size_t stage_elems = (size_t)PR * PP;
+    static constexpr int NSTAGE = ((3 * stage_elems + rest_elems) * sizeof(T) + 256 <= 227 * 1024) ? 3 : 2;
+    static constexpr size_t smem_bytes = (NSTAGE * stage_elems + rest_elems) * sizeof(T) + 128;
+    static_assert(T3 % BL == 0, "T3");
+    static_assert(WI <= 256, "store box");
+    static_assert((PR * PP * sizeof(T)) % 128 == 0 && (BOXW * sizeof(T)) % 128 == 0, "TMA alignment");
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void *src, int c0, int c1, int c2)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];\n" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------- taps
+// rec(r) = taps + (off + r + PADR) * REC; G(r, k) = G[r, r+k], R(r, k) = lambda R[r, r+k]
+// (symmetric: G[r, r-k] = G[r-k, r]).  Tables are zero outside the domain rows.
+template <typename T>
+__device__ __forceinline__ T tapG(const Params<T> &a, int off, int r, int k)
+{
+    return k >= 0 ? a.taps[(off + r + PADR) * REC + k] : a.taps[(off + r + k + PADR) * REC - k];
+}
+template <typename T>
+__device__ __forceinline__ T tapR(const Params<T> &a, int off, int r, int k)
+{
+    return k >= 0 ? a.taps[(off + r + PADR) * REC + 4 + k] : a.taps[(off + r + k + PADR) * REC + 4 - k];
+}
+
+// ---------------------------------------------------------------- pass C + ring (per segment, per rotation)
+// 6-slot ring: output slab o lives in slot (o - j0) mod 6; at slab j the slot
+// of j-3 is emitted and reused for j+3.
+template <typename T, int E, int ROT>
+__device__ __forceinline__ void ring_step(T (&acc)[6][E], const T (&s)[E], const T (&q)[E], const T (&pc)[E],
+                                          const T (&g1)[7], const T (&r1)[5], T (&ov)[E])
+{
+    // s: in-slice Kronecker part (goes through G1), q: in-slice regulariser
+    // part (identity in mode 1: added to output j only), pc: p itself (R1).
+    constexpr int SE = (ROT + 3) % 6;   // slot of j-3 == slot of j+3
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        ov[e] = fma(g1[0], s[e], acc[SE][e]);   // o = -3: finishes output j-3
+        acc[SE][e] = g1[6] * s[e];              // o = +3: first term of output j+3
+    }
+#pragma unroll
+    for (int o = -2; o <= 2; ++o) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            T v = acc[(ROT + o + 6) % 6][e];
+            v = fma(g1[o + 3], s[e], v);
+            v = fma(r1[o + 2], pc[e], v);
+            if (o == 0) v += q[e];
+            acc[(ROT + o + 6) % 6][e] = v;
+        }
+    }
+}
+
+template <typename T, int N4, int SEG>
+__device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3, const T *RB,
+                                       const T *P, T *OUT, int pos, int rot, int j, bool live, bool emit)
+{
+    using C = Cfg<T, N4>;
+    constexpr int E = C::E;
+    constexpr int e0 = SEG * E;
+    constexpr int e1 = (e0 + E < N4) ? e0 + E : N4;
+    constexpr int NE = e1 - e0;
+    constexpr int ulo = e0 - 3 > 0 ? e0 - 3 : 0;
+    constexpr int uhi = e1 + 3 < N4 ? e1 + 3 : N4;
+    constexpr int plo = e0 - 2 > 0 ? e0 - 2 : 0;
+    constexpr int phi = e1 + 2 < N4 ? e1 + 2 : N4;
+    const int i2 = pos / C::T3, i3 = pos % C::T3;
+    T s[E], q[E], pc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { s[e] = T(0); q[e] = T(0); pc[e] = T(0); }
+    if (live) {
+        const T *u3 = U3 + i2 * C::WI + i3 * N4;
+        const T *rb = RB + i2 * C::WI + i3 * N4;
+        const T *pp = P + (i2 + 3) * C::PP + (i3 + 3) * N4;
+        T uw[uhi - ulo], pw[phi - plo];
+#pragma unroll
+        for (int k = ulo; k < uhi; ++k) uw[k - ulo] = u3[k];
+#pragma unroll
+        for (int k = plo; k < phi; ++k) pw[k - plo] = pp[k];
+#pragma unroll
+        for (int e = 0; e < NE; ++e) q[e] = rb[e0 + e];
+        // G4 U3 (push form, compile-time taps: constant-bank operands)
+#pragma unroll
+        for (int k = ulo; k < uhi; ++k)
+#pragma unroll
+            for (int e = e0; e < e1; ++e)
+                if (k - e >= -3 && k - e <= 3) s[e - e0] = fma(tapG(a, 0, e, k - e), uw[k - ulo], s[e - e0]);
+        // lambda R4 p
+#pragma unroll
+        for (int k = plo; k < phi; ++k)
+#pragma unroll
+            for (int e = e0; e < e1; ++e)
+                if (k - e >= -2 && k - e <= 2) q[e - e0] = fma(tapR(a, 0, e, k - e), pw[k - plo], q[e - e0]);
+#pragma unroll
+        for (int e = 0; e < NE; ++e) pc[e] = pw[e0 + e - plo];
+    }
+    // mode-1 taps of input slab j: G1[j+o, j], lambda R1[j+o, j]
+    T g1[7], r1[5];
+#pragma unroll
+    for (int o = -3; o <= 3; ++o) g1[o + 3] = tapG(a, a.off1, j + o, -o);
+#pragma unroll
+    for (int o = -2; o <= 2; ++o) r1[o + 2] = tapR(a, a.off1, j + o, -o);
+    T *out = OUT + (pos / C::T3) * C::WI + (pos % C::T3) * N4 + e0;
+    T ov[E];
+    switch (rot) {
+#define TCA_ROT(R)                                                  \
+    case R:                                                         \
+        ring_step<T, E, R>(acc, s, q, pc, g1, r1, ov);           \
+        break;
+        TCA_ROT(0) TCA_ROT(1) TCA_ROT(2) TCA_ROT(3) TCA_ROT(4) default: ring_step<T, E, 5>(acc, s, q, pc, g1, r1, ov);
+#undef TCA_ROT
+    }
+    if (emit) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) out[e] = ov[e];
+    }
+}
+
+template <typename T, int N4, int SEG>
+__device__ __forceinline__ void pass_c_dispatch(const Params<T> &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3,
+                                                const T *RB, const T *P, T *OUT, int seg, int pos, int rot, int j,
+                                                bool live, bool emit)
+{
+    if constexpr (SEG < Cfg<T, N4>::NSEG) {
+        if (seg == SEG) pass_c<T, N4, SEG>(a, acc, U3, RB, P, OUT, pos, rot, j, live, emit);
+        else pass_c_dispatch<T, N4, SEG + 1>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit);
+    }
+}
+
+// ---------------------------------------------------------------- kernel
+template <typename T, int N4>
+__global__ void __launch_bounds__(NTHR, 1)
+band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict__ ymp,
+                  const __grid_constant__ Params<T> a)
+{
+    using C = Cfg<T, N4>;
+    constexpr int W = C::W, WI = C::WI, PP = C::PP, T3 = C::T3, E = C::E;
+    if (a.done && *a.done) return;
+    if (a.dbg & 16) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
+    T *Pst = reinterpret_cast<T *>(smem_raw + 128);
+    T *U2 = Pst + C::NSTAGE * C::stage_elems;
+    T *RA = U2 + C::U2E;
+    T *U3 = RA + C::WIE;
+    T *RB = U3 + C::WIE;
+    T *OUTB = RB + C::WIE;   // [2][WIE]
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    // xmp/ymp: tensor maps in global memory (a descriptor in a >4 KB parameter
+    // block is not usable by the TMA unit)
+    if (tid == 0) {
+        for (int s = 0; s < C::NSTAGE; ++s) mbar_init(bar + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (a.dbg & 32) return;
+
+    const int seg = tid / (NTHR / C::NSEG);   // warp-uniform
+    const int pos = tid % (NTHR / C::NSEG);   // (i2, i3) of the ring owner
+
+    long long u0 = a.total * blockIdx.x / gridDim.x;
+    const long long u1 = a.total * (blockIdx.x + 1) / gridDim.x;
+    unsigned gi = 0, gc = 0;   // slabs issued / consumed (stage = g % NSTAGE, parity (g / NSTAGE) & 1)
+    T acc[6][E];
+    while (u0 < u1) {
+        const int tile = (int)(u0 / a.n1);
+        const int o0 = (int)(u0 % a.n1);
+        const long long rem = u1 - u0;
+        const int o1 = (int)((long long)a.n1 < o0 + rem ? (long long)a.n1 : o0 + rem);
+        u0 += o1 - o0;
+        const int a2 = (tile / a.tiles3) * T2;
+        const int a3 = (tile % a.tiles3) * T3;
+        const int ca = (a3 - 3) * N4;                              // flat column of staged column 0
+        const int delta = ((ca % C::VEC) + C::VEC) % C::VEC;       // boxes start 16-B aligned
+        const int j0 = o0 - 3, j1 = o1 + 3;
+        const int jb = j0 > 0 ? j0 : 0, je = j1 < a.n1 ? j1 : a.n1;
+#pragma unroll
+        for (int s = 0; s < 6; ++s)
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[s][e] = T(0);
+        // prologue: stage the first NSTAGE-1 in-range slabs
+        auto issue = [&](int js) {
+            if (warp == 0) {
+                const unsigned st = gi % C::NSTAGE;
+                T *dst = Pst + st * C::stage_elems;
+                if (lane == 0) mbar_arrive_expect_tx(bar + st, (unsigned)(C::NB * PR * C::BOXW * sizeof(T)));
+                __syncwarp();
+                for (int b = lane; b < C::NB * PR; b += 32) {
+                    const int r = b / C::NB, h = b % C::NB;
+                    tma_load_3d(dst + r * PP + h * C::BOXW, xmp, bar + st, ca - delta + h * C::BOXW, a2 - 3 + r, js);
+                }
+            }
+            ++gi;
+        };
+        if (!(a.dbg & 8))
+            for (int js = jb; js < je && js < jb + C::NSTAGE - 1; ++js) issue(js);
+        int next = jb + C::NSTAGE - 1;   // next slab to stage
+        int rot = 0;
+        int pending = -1;                // output slab whose staging buffer awaits its TMA store
+#pragma unroll 1
+        for (int j = j0; j < j1; ++j) {
+            const bool live = j >= 0 && j < a.n1 && !(a.dbg & 8);
+            const T *P = Pst + (gc % C::NSTAGE) * C::stage_elems + delta;
+            if (live && !(a.dbg & 128)) mbar_wait(bar + gc % C::NSTAGE, (gc / C::NSTAGE) & 1);
+
+            // ---- pass A: G2 (all halo-extended columns), lambda R2 (interior columns)
+            if (live && !(a.dbg & 4)) {
+#pragma unroll 1
+                for (int c = tid; c < W; c += NTHR) {
+                    T v[PR];
+#pragma unroll
+                    for (int s = 0; s < PR; ++s) v[s] = P[s * PP + c];
+                    T u[T2];
+#pragma unroll
+                    for (int r = 0; r < T2; ++r) u[r] = T(0);
+#pragma unroll
+                    for (int s = 0; s < PR; ++s)
+#pragma unroll
+                        for (int r = 0; r < T2; ++r)
+                            if (s - r - 3 >= -3 && s - r - 3 <= 3) u[r] = fma(tapG(a, a.off2, a2 + r, s - r - 3), v[s], u[r]);
+#pragma unroll
+                    for (int r = 0; r < T2; ++r) U2[r * W + c] = u[r];
+                    const int ci = c - 3 * N4;
+                    if (ci >= 0 && ci < WI) {
+#pragma unroll
+                        for (int r = 0; r < T2; ++r) u[r] = T(0);
+#pragma unroll
+                        for (int s = 1; s < PR - 1; ++s)
+#pragma unroll
+                            for (int r = 0; r < T2; ++r)
+                                if (s - r - 3 >= -2 && s - r - 3 <= 2)
+                                    u[r] = fma(tapR(a, a.off2, a2 + r, s - r - 3), v[s], u[r]);
+#pragma unroll
+                        for (int r = 0; r < T2; ++r) RA[r * WI + ci] = u[r];
+                    }
+                }
+            }
+            __syncthreads();   // bar1: U2/RA complete; all threads finished slab j-1
+
+            if (tid == 0) {
+                if (pending >= 0 && !(a.dbg & 1)) {
+                    // staging buffer of output slab `pending` (written in pass C of slab pending+3)
+                    tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::WIE, a3 * N4, a2, pending);
+                    bulk_commit();
+                    bulk_wait_read<1>();
+                    pending = -1;
+                }
+            }
+            if (live && next < je && !(a.dbg & 64)) {   // stage slab `next` into the stage last read in slab j-1
+                issue(next);
+                ++next;
+            }
+
+            // ---- pass B: G3 on U2, lambda R3 on p (8 outputs along i3 per item)
+            if (live && !(a.dbg & 4)) {
+#pragma unroll 1
+                for (int it = warp; it < C::NBLK * C::WPB; it += NTHR / 32) {
+                    const int b = it / C::WPB;
+                    const int l = (it % C::WPB) * 32 + lane;
+                    if (l < C::LPB) {
+                        const int i2 = l / N4, i4 = l % N4;
+                        const int h0 = b * C::BL;
+                        const T *u2 = U2 + i2 * W + h0 * N4 + i4;
+                        const T *pp = P + (i2 + 3) * PP + (h0 + 1) * N4 + i4;
+                        const int ob = i2 * WI + h0 * N4 + i4;
+                        T v[C::BL + 6], w[C::BL + 4], u[C::BL], rr[C::BL];
+#pragma unroll
+                        for (int m = 0; m < C::BL + 6; ++m) v[m] = u2[m * N4];
+#pragma unroll
+                        for (int m = 0; m < C::BL + 4; ++m) w[m] = pp[m * N4];
+#pragma unroll
+                        for (int o = 0; o < C::BL; ++o) { u[o] = T(0); rr[o] = RA[ob + o * N4]; }
+                        const int r3 = a3 + h0;
+#pragma unroll
+                        for (int m = 0; m < C::BL + 6; ++m)
+#pragma unroll
+                            for (int o = 0; o < C::BL; ++o)
+                                if (m - o - 3 >= -3 && m - o - 3 <= 3)
+                                    u[o] = fma(tapG(a, a.off3, r3 + o, m - o - 3), v[m], u[o]);
+#pragma unroll
+                        for (int m = 0; m < C::BL + 4; ++m)
+#pragma unroll
+                            for (int o = 0; o < C::BL; ++o)
+                                if (m - o - 2 >= -2 && m - o - 2 <= 2)
+                                    rr[o] = fma(tapR(a, a.off3, r3 + o, m - o - 2), w[m], rr[o]);
+#pragma unroll
+                        for (int o = 0; o < C::BL; ++o) {
+                            U3[ob + o * N4] = u[o];
+                            RB[ob + o * N4] = rr[o];
+                        }
+                    }
+                }
+            }
+            __syncthreads();   // bar2: U3/RB complete
+
+            // ---- pass C + mode-1 ring + emission of output slab j-3
+            const bool emit = (j - 3 >= o0) && (j - 3 < o1);
+            T *OUT = OUTB + (j & 1) * C::WIE;
+            if (!(a.dbg & 2)) pass_c_dispatch<T, N4, 0>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit);
+            if (emit) {
+                fence_proxy_async();
+                pending = j - 3;
+            }
+            if (live) ++gc;
+            rot = rot == 5 ? 0 : rot + 1;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (pending >= 0 && !(a.dbg & 1)) {
+                tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::WIE, a3 * N4, a2, pending);
+                bulk_commit();
+            }
+            bulk_wait<0>();
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- host side
+template <typename T, int N4>
+tca_status launch_n4(const tca_operator *op, const Params<T> &prm, cudaStream_t s, const CUtensorMap *xm,
+                     const CUtensorMap *ym)
+{
+    using C = Cfg<T, N4>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        TCA_CUDA_TRY(cudaFuncSetAttribute(band_apply_kernel<T, N4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)C::smem_bytes));
+        attr_set = true;
+    }
+    long long grid = op->num_sms;
+    if (grid > prm.total) grid = prm.total;
+    if (grid < 1) grid = 1;
+    count_launch();
+    band_apply_kernel<T, N4><<<(unsigned)grid, NTHR, C::smem_bytes, s>>>(xm, ym, prm);
+    TCA_CUDA_TRY(cudaGetLastError());
+    return TCA_OK;
+}
+
+#define TCA_BAND_N4_LIST(X) X(1) X(2) X(4) X(7) X(8) X(15) X(16) X(32)
+
+template <typename T>
+int t3_for(int n4)
+{
+    switch (n4) {
+#define TCA_CASE(n) \
+    case n: return Cfg<T, n>::T3;
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return 0;
+}
+
+template <typename T>
+int boxw_for(int n4)
+{
+    switch (n4) {
+#define TCA_CASE(n) \
+    case n: return Cfg<T, n>::BOXW;
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return 0;
+}
+
+template <typename T>
+tca_status launch_dispatch(const tca_operator *op, const Params<T> &prm, cudaStream_t s, const CUtensorMap *xm,
+                           const CUtensorMap *ym)
+{
+    switch ((int)op->n[3]) {
+#define TCA_CASE(n) \
+    case n: return launch_n4<T, n>(op, prm, s, xm, ym);
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return fail(TCA_ERR_INVALID_ARG, "band apply: unsupported n4");
+}
+
+}  // namespace band
+}  // namespace tca

@@ -67,12 +67,17 @@ struct CgScalars {
 struct alignas(64) TmapSlot {
     uint64_t map[16];
     const void *ptr = nullptr;
+    int kind = 0;   // 0: slab-load map of an apply input, 1: tile-store map of an apply output
+    int slot = 0;   // index in the operator's device descriptor buffer
 };
+constexpr int kTmapSlots = 32;
 
 }  // namespace tca
 
 struct tca_operator {
-    std::vector<tca::TmapSlot> tmaps;    // TMA descriptors of recent apply inputs
+    std::vector<tca::TmapSlot> tmaps;    // TMA descriptors of recent apply inputs/outputs
+    void *tmap_dev = nullptr;            // device copies (kTmapSlots x 128 B)
+    int tmap_next = 0;
     int order = 0;
     int64_t n[tca::kD] = {1, 1, 1, 1};   // global unknown extents (padded)
     int64_t m[tca::kD] = {1, 1, 1, 1};   // global data extents (padded)
@@ -85,10 +90,11 @@ struct tca_operator {
     int banded_mask = 0;                 // bit d: G_d hb <= 3 (and R_d hb <= 2)
     bool all_banded = false;
 
-    // offset-form taps (fused banded kernel): tapG[d][r*7 + k+3] = G_d[r, r+k],
-    // tapR[d][r*5 + k+2] = lambda * R_d[r, r+k]
-    void *tapG[tca::kD] = {};
-    void *tapR[tca::kD] = {};
+    // symmetric band rows for the fused banded kernel (host, fp64):
+    // bandG[d][r*4 + k] = G_d[r, r+k] (k = 0..3), bandR[d][r*3 + k] = lambda R_d[r, r+k] (k = 0..2)
+    std::vector<double> bandG[tca::kD];
+    std::vector<double> bandR[tca::kD];
+    std::vector<unsigned char> band_params;   // prebuilt kernel-parameter block (tap tables)
     // generic compressed-band forms
     tca::BandMat Gm[tca::kD], Rm[tca::kD], At[tca::kD], Af[tca::kD];
 
