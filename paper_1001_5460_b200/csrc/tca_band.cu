@@ -6,6 +6,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "tca_band_impl.cuh"
@@ -81,7 +82,19 @@ void build_params(const tca_operator *op, std::vector<unsigned char> &blob)
     p->n3 = (int)op->n[2];
     p->tiles3 = (p->n3 + t3 - 1) / t3;
     const long long tiles2 = (p->n2 + band::T2 - 1) / band::T2;
-    p->total = tiles2 * p->tiles3 * p->n1;
+    const long long total = tiles2 * p->tiles3 * p->n1;
+    // persistent grid: CTA b owns units [total*b/G, total*(b+1)/G) of the
+    // (tile-major, slab-minor) unit order
+    const int G = (int)std::min<long long>(std::min(op->num_sms, band::MAXG), total);
+    for (int b = 0; b < G; ++b) {
+        const long long u0 = total * b / G, u1 = total * (b + 1) / G;
+        const long long tile = u0 / p->n1;
+        p->s_tile[b].x = (short)(tile / p->tiles3);
+        p->s_tile[b].y = (short)(tile % p->tiles3);
+        p->s_o0[b] = (int)(u0 % p->n1);
+        p->s_cnt[b] = (int)(u1 - u0);
+    }
+    const_cast<tca_operator *>(op)->band_grid = G;
     p->off1 = L.off[0];
     p->off2 = L.off[1];
     p->off3 = L.off[2];

@@ -42,32 +42,38 @@
 namespace tca {
 namespace band {
 
-constexpr int NTHR = 256;
+constexpr int NTHR = 512;       // 16 warps: 4 per SMSP hide DFMA/LDS/LDCU latency
 constexpr int T2 = 8;            // mode-2 rows per tile
 constexpr int PR = T2 + 6;       // staged rows (halo 3 + 3)
 constexpr int REC = 7;           // tap record per row: G[r,r..r+3], lambda R[r,r..r+2]
 constexpr int PADR = 6;          // zero rows below each table (row r at record off + r + PADR)
-constexpr int TAP_BYTES = 30 * 1024;
+constexpr int TAP_BYTES = 29 * 1024;
+constexpr int MAXG = 160;        // max persistent CTAs (>= SM count)
 
+// Kernel parameters (constant bank).  The per-CTA schedule is precomputed on
+// the host so that every control value in the kernel is warp-uniform (no
+// integer division on device): the compiler then keeps tile coordinates in
+// uniform registers and loads taps with LDCU into uniform-register operands.
 template <typename T>
 struct Params {
     const T *x;
     T *y;
     const int32_t *done;
-    long long total;       // tiles * n1 units
     int n1, n2, n3, tiles3;
     int off3, off2, off1;  // record offsets (rows) of the mode-3/2/1 tables; mode 4 at 0
-    int dbg;     // debug switches (0 in production)
-    int pad;
+    int dbg;               // debug switches (0 in production)
+    short2 s_tile[MAXG];   // CTA b starts at tile (x = mode-2 tile, y = mode-3 tile) ...
+    int s_o0[MAXG];        // ... at output slab s_o0 ...
+    int s_cnt[MAXG];       // ... and processes s_cnt (tile, slab) units
     T taps[TAP_BYTES / sizeof(T)];
 };
 
 template <typename T, int N4>
 struct Cfg {
-    static constexpr int NSEG = (N4 + 7) / 8;        // ring segments along i4
-    static constexpr int E = (N4 + NSEG - 1) / NSEG; // elements per segment (<= 8)
-    static constexpr int T3 = 32 / NSEG;             // mode-3 columns per tile
-    static_assert(32 % NSEG == 0, "unsupported n4");
+    static constexpr int NSEG = (N4 + 3) / 4;        // ring segments along i4
+    static constexpr int E = (N4 + NSEG - 1) / NSEG; // elements per segment (<= 4: ring 24 doubles)
+    static constexpr int T3 = NTHR / (T2 * NSEG);    // mode-3 columns per tile
+    static_assert(NTHR % (T2 * NSEG) == 0, "unsupported n4");
     static constexpr int W = (T3 + 6) * N4;          // halo-extended flat columns
     static constexpr int WI = T3 * N4;               // interior flat columns
     static constexpr int VEC = 16 / (int)sizeof(T);  // TMA coordinate granularity (16 B)
@@ -86,18 +92,26 @@ struct Cfg {
     static constexpr int NB = pick_nb();
     static constexpr int BOXW = boxw_for_nb(NB);
     static constexpr int PP = NB * BOXW;             // staged row pitch
-    static constexpr int BL = 8;                     // pass-B outputs per item
+    static constexpr int BL = 4;                     // pass-B outputs per item
     static constexpr int NBLK = T3 / BL;
     static constexpr int LPB = T2 * N4;              // pass-B lanes per block
     static constexpr int WPB = (LPB + 31) / 32;
     static constexpr size_t al(size_t e) { return (e * sizeof(T) + 127) / 128 * 128 / sizeof(T); }
-    static constexpr size_t U2E = al((size_t)T2 * W);    // smem buffers, each 128-B aligned
-    static constexpr size_t WIE = al((size_t)T2 * WI);
-    static constexpr size_t rest_elems = U2E + 5 * WIE;
+    // row pitches of the intermediate tiles: congruent to N4 modulo one bank
+    // sweep (128 B) so that pass-B lanes (i2, i4) of consecutive i2 rows hit
+    // consecutive banks (conflict-free)
+    static constexpr int BANKS = 128 / (int)sizeof(T);
+    static constexpr int WP = W + (((N4 - W) % BANKS) + BANKS) % BANKS;    // U2 pitch
+    static constexpr int WIP = WI + (((N4 - WI) % BANKS) + BANKS) % BANKS; // RA/U3/RB pitch
+    static constexpr size_t U2E = al((size_t)T2 * WP);   // smem buffers, each 128-B aligned
+    static constexpr size_t WIE = al((size_t)T2 * WIP);
+    static constexpr size_t OUTE = al((size_t)T2 * WI);  // TMA store source: dense [T2][WI]
+    static constexpr size_t rest_elems = U2E + 3 * WIE + 2 * OUTE;
     static constexpr size_t stage_elems = (size_t)PR * PP;
     static constexpr int NSTAGE = ((3 * stage_elems + rest_elems) * sizeof(T) + 256 <= 227 * 1024) ? 3 : 2;
     static constexpr size_t smem_bytes = (NSTAGE * stage_elems + rest_elems) * sizeof(T) + 128;
     static_assert(T3 % BL == 0, "T3");
+    static_assert(NBLK * WPB <= NTHR / 32, "pass B: one item per warp");
     static_assert(WI <= 256, "store box");
     static_assert((PR * PP * sizeof(T)) % 128 == 0 && (BOXW * sizeof(T)) % 128 == 0, "TMA alignment");
 };
@@ -212,8 +226,8 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
 #pragma unroll
     for (int e = 0; e < E; ++e) { s[e] = T(0); q[e] = T(0); pc[e] = T(0); }
     if (live) {
-        const T *u3 = U3 + i2 * C::WI + i3 * N4;
-        const T *rb = RB + i2 * C::WI + i3 * N4;
+        const T *u3 = U3 + i2 * C::WIP + i3 * N4;
+        const T *rb = RB + i2 * C::WIP + i3 * N4;
         const T *pp = P + (i2 + 3) * C::PP + (i3 + 3) * N4;
         T uw[uhi - ulo], pw[phi - plo];
 #pragma unroll
@@ -270,6 +284,50 @@ __device__ __forceinline__ void pass_c_dispatch(const Params<T> &a, T (&acc)[6][
     }
 }
 
+// ---------------------------------------------------------------- pass B (compile-time block B)
+template <typename T, int N4, int B>
+__device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T *RA, const T *P, T *U3, T *RB,
+                                       int a3, int warp, int lane)
+{
+    using C = Cfg<T, N4>;
+    if constexpr (B < C::NBLK) {
+        if (warp / C::WPB != B) {
+            pass_b<T, N4, B + 1>(a, U2, RA, P, U3, RB, a3, warp, lane);
+            return;
+        }
+        const int l = (warp % C::WPB) * 32 + lane;
+        if (l >= C::LPB) return;
+        const int i2 = l / N4, i4 = l % N4;
+        constexpr int h0 = B * C::BL;
+        const T *u2 = U2 + i2 * C::WP + h0 * N4 + i4;
+        const T *pp = P + (i2 + 3) * C::PP + (h0 + 1) * N4 + i4;
+        const int ob = i2 * C::WIP + h0 * N4 + i4;
+        T v[C::BL + 6], w[C::BL + 4], u[C::BL], rr[C::BL];
+#pragma unroll
+        for (int m = 0; m < C::BL + 6; ++m) v[m] = u2[m * N4];
+#pragma unroll
+        for (int m = 0; m < C::BL + 4; ++m) w[m] = pp[m * N4];
+#pragma unroll
+        for (int o = 0; o < C::BL; ++o) { u[o] = T(0); rr[o] = RA[ob + o * N4]; }
+        const int r3 = a3 + h0;   // uniform
+#pragma unroll
+        for (int m = 0; m < C::BL + 6; ++m)
+#pragma unroll
+            for (int o = 0; o < C::BL; ++o)
+                if (m - o - 3 >= -3 && m - o - 3 <= 3) u[o] = fma(tapG(a, a.off3, r3 + o, m - o - 3), v[m], u[o]);
+#pragma unroll
+        for (int m = 0; m < C::BL + 4; ++m)
+#pragma unroll
+            for (int o = 0; o < C::BL; ++o)
+                if (m - o - 2 >= -2 && m - o - 2 <= 2) rr[o] = fma(tapR(a, a.off3, r3 + o, m - o - 2), w[m], rr[o]);
+#pragma unroll
+        for (int o = 0; o < C::BL; ++o) {
+            U3[ob + o * N4] = u[o];
+            RB[ob + o * N4] = rr[o];
+        }
+    }
+}
+
 // ---------------------------------------------------------------- kernel
 template <typename T, int N4>
 __global__ void __launch_bounds__(NTHR, 1)
@@ -287,7 +345,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
     T *RA = U2 + C::U2E;
     T *U3 = RA + C::WIE;
     T *RB = U3 + C::WIE;
-    T *OUTB = RB + C::WIE;   // [2][WIE]
+    T *OUTB = RB + C::WIE;   // [2][OUTE]
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     // xmp/ymp: tensor maps in global memory (a descriptor in a >4 KB parameter
@@ -302,18 +360,17 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
     const int seg = tid / (NTHR / C::NSEG);   // warp-uniform
     const int pos = tid % (NTHR / C::NSEG);   // (i2, i3) of the ring owner
 
-    long long u0 = a.total * blockIdx.x / gridDim.x;
-    const long long u1 = a.total * (blockIdx.x + 1) / gridDim.x;
+    // per-CTA schedule (uniform): tile (t2i, t3i) from slab o0, cnt units in total
+    int t2i = a.s_tile[blockIdx.x].x, t3i = a.s_tile[blockIdx.x].y;
+    int o0 = a.s_o0[blockIdx.x];
+    int cnt = a.s_cnt[blockIdx.x];
     unsigned gi = 0, gc = 0;   // slabs issued / consumed (stage = g % NSTAGE, parity (g / NSTAGE) & 1)
     T acc[6][E];
-    while (u0 < u1) {
-        const int tile = (int)(u0 / a.n1);
-        const int o0 = (int)(u0 % a.n1);
-        const long long rem = u1 - u0;
-        const int o1 = (int)((long long)a.n1 < o0 + rem ? (long long)a.n1 : o0 + rem);
-        u0 += o1 - o0;
-        const int a2 = (tile / a.tiles3) * T2;
-        const int a3 = (tile % a.tiles3) * T3;
+    for (; cnt > 0; o0 = 0, t3i = (t3i + 1 == a.tiles3) ? 0 : t3i + 1, t2i += (t3i == 0) ? 1 : 0) {
+        const int o1 = (a.n1 - o0 < cnt) ? a.n1 : o0 + cnt;
+        cnt -= o1 - o0;
+        const int a2 = __shfl_sync(0xffffffffu, t2i * T2, 0);   // provably warp-uniform
+        const int a3 = __shfl_sync(0xffffffffu, t3i * T3, 0);
         const int ca = (a3 - 3) * N4;                              // flat column of staged column 0
         const int delta = ((ca % C::VEC) + C::VEC) % C::VEC;       // boxes start 16-B aligned
         const int j0 = o0 - 3, j1 = o1 + 3;
@@ -323,15 +380,20 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
 #pragma unroll
             for (int e = 0; e < E; ++e) acc[s][e] = T(0);
         // prologue: stage the first NSTAGE-1 in-range slabs
+        // stage slab js: NB boxes per staged row, issued round-robin by lane 0 of
+        // every warp (one warp issuing all of them serialises ~30 UTMALDG)
         auto issue = [&](int js) {
-            if (warp == 0) {
-                const unsigned st = gi % C::NSTAGE;
-                T *dst = Pst + st * C::stage_elems;
-                if (lane == 0) mbar_arrive_expect_tx(bar + st, (unsigned)(C::NB * PR * C::BOXW * sizeof(T)));
-                __syncwarp();
-                for (int b = lane; b < C::NB * PR; b += 32) {
-                    const int r = b / C::NB, h = b % C::NB;
-                    tma_load_3d(dst + r * PP + h * C::BOXW, xmp, bar + st, ca - delta + h * C::BOXW, a2 - 3 + r, js);
+            const unsigned st = gi % C::NSTAGE;
+            T *dst = Pst + st * C::stage_elems;
+            if (tid == 0) mbar_arrive_expect_tx(bar + st, (unsigned)(C::NB * PR * C::BOXW * sizeof(T)));
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < (C::NB * PR + NTHR / 32 - 1) / (NTHR / 32); ++k) {
+                    const int b = warp + k * (NTHR / 32);
+                    if (b < C::NB * PR) {
+                        const int r = b / C::NB, h = b % C::NB;
+                        tma_load_3d(dst + r * PP + h * C::BOXW, xmp, bar + st, ca - delta + h * C::BOXW, a2 - 3 + r, js);
+                    }
                 }
             }
             ++gi;
@@ -363,7 +425,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                         for (int r = 0; r < T2; ++r)
                             if (s - r - 3 >= -3 && s - r - 3 <= 3) u[r] = fma(tapG(a, a.off2, a2 + r, s - r - 3), v[s], u[r]);
 #pragma unroll
-                    for (int r = 0; r < T2; ++r) U2[r * W + c] = u[r];
+                    for (int r = 0; r < T2; ++r) U2[r * C::WP + c] = u[r];
                     const int ci = c - 3 * N4;
                     if (ci >= 0 && ci < WI) {
 #pragma unroll
@@ -375,7 +437,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                                 if (s - r - 3 >= -2 && s - r - 3 <= 2)
                                     u[r] = fma(tapR(a, a.off2, a2 + r, s - r - 3), v[s], u[r]);
 #pragma unroll
-                        for (int r = 0; r < T2; ++r) RA[r * WI + ci] = u[r];
+                        for (int r = 0; r < T2; ++r) RA[r * C::WIP + ci] = u[r];
                     }
                 }
             }
@@ -384,7 +446,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             if (tid == 0) {
                 if (pending >= 0 && !(a.dbg & 1)) {
                     // staging buffer of output slab `pending` (written in pass C of slab pending+3)
-                    tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::WIE, a3 * N4, a2, pending);
+                    tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                     bulk_commit();
                     bulk_wait_read<1>();
                     pending = -1;
@@ -395,51 +457,13 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                 ++next;
             }
 
-            // ---- pass B: G3 on U2, lambda R3 on p (8 outputs along i3 per item)
-            if (live && !(a.dbg & 4)) {
-#pragma unroll 1
-                for (int it = warp; it < C::NBLK * C::WPB; it += NTHR / 32) {
-                    const int b = it / C::WPB;
-                    const int l = (it % C::WPB) * 32 + lane;
-                    if (l < C::LPB) {
-                        const int i2 = l / N4, i4 = l % N4;
-                        const int h0 = b * C::BL;
-                        const T *u2 = U2 + i2 * W + h0 * N4 + i4;
-                        const T *pp = P + (i2 + 3) * PP + (h0 + 1) * N4 + i4;
-                        const int ob = i2 * WI + h0 * N4 + i4;
-                        T v[C::BL + 6], w[C::BL + 4], u[C::BL], rr[C::BL];
-#pragma unroll
-                        for (int m = 0; m < C::BL + 6; ++m) v[m] = u2[m * N4];
-#pragma unroll
-                        for (int m = 0; m < C::BL + 4; ++m) w[m] = pp[m * N4];
-#pragma unroll
-                        for (int o = 0; o < C::BL; ++o) { u[o] = T(0); rr[o] = RA[ob + o * N4]; }
-                        const int r3 = a3 + h0;
-#pragma unroll
-                        for (int m = 0; m < C::BL + 6; ++m)
-#pragma unroll
-                            for (int o = 0; o < C::BL; ++o)
-                                if (m - o - 3 >= -3 && m - o - 3 <= 3)
-                                    u[o] = fma(tapG(a, a.off3, r3 + o, m - o - 3), v[m], u[o]);
-#pragma unroll
-                        for (int m = 0; m < C::BL + 4; ++m)
-#pragma unroll
-                            for (int o = 0; o < C::BL; ++o)
-                                if (m - o - 2 >= -2 && m - o - 2 <= 2)
-                                    rr[o] = fma(tapR(a, a.off3, r3 + o, m - o - 2), w[m], rr[o]);
-#pragma unroll
-                        for (int o = 0; o < C::BL; ++o) {
-                            U3[ob + o * N4] = u[o];
-                            RB[ob + o * N4] = rr[o];
-                        }
-                    }
-                }
-            }
+            // ---- pass B: G3 on U2, lambda R3 on p (8 outputs along i3 per item; item = warp)
+            if (live && !(a.dbg & 4)) pass_b<T, N4, 0>(a, U2, RA, P, U3, RB, a3, warp, lane);
             __syncthreads();   // bar2: U3/RB complete
 
             // ---- pass C + mode-1 ring + emission of output slab j-3
             const bool emit = (j - 3 >= o0) && (j - 3 < o1);
-            T *OUT = OUTB + (j & 1) * C::WIE;
+            T *OUT = OUTB + (j & 1) * C::OUTE;
             if (!(a.dbg & 2)) pass_c_dispatch<T, N4, 0>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit);
             if (emit) {
                 fence_proxy_async();
@@ -451,7 +475,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         __syncthreads();
         if (tid == 0) {
             if (pending >= 0 && !(a.dbg & 1)) {
-                tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::WIE, a3 * N4, a2, pending);
+                tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                 bulk_commit();
             }
             bulk_wait<0>();
@@ -472,11 +496,8 @@ tca_status launch_n4(const tca_operator *op, const Params<T> &prm, cudaStream_t 
                                           (int)C::smem_bytes));
         attr_set = true;
     }
-    long long grid = op->num_sms;
-    if (grid > prm.total) grid = prm.total;
-    if (grid < 1) grid = 1;
     count_launch();
-    band_apply_kernel<T, N4><<<(unsigned)grid, NTHR, C::smem_bytes, s>>>(xm, ym, prm);
+    band_apply_kernel<T, N4><<<(unsigned)op->band_grid, NTHR, C::smem_bytes, s>>>(xm, ym, prm);
     TCA_CUDA_TRY(cudaGetLastError());
     return TCA_OK;
 }

@@ -117,6 +117,7 @@ struct tca_operator {
     size_t device_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int num_sms = 148;
+    int band_grid = 0;                   // persistent grid of the fused banded apply
     int apply_path = 0;                  // 0 = generic multi-pass, 1 = fused banded
     // timing instrumentation
     int timing = 0;
