@@ -211,7 +211,9 @@ def run_tca(args):
             state["apply_ms"] = state.get("apply_ms", 0.0) + ms
             state["apply_cnt"] = state.get("apply_cnt", 0) + cnt
         state["iters"] = state.get("iters", 0) + rep["iterations"]
+        state["cg_s"] = state.get("cg_s", 0.0) + rep["seconds"]
         state["last_rep"] = rep
+        state["path"] = op.apply_path
         op.close()
         return x
 
@@ -238,17 +240,32 @@ def run_tca(args):
     value = total_iters / (total_ms * 1e-3)
     hbm, peak_src = peaks()
 
-    # dominant kernel: the operator apply inside CG (event pairs around every launch)
+    # dominant kernel: the operator apply inside CG (event pair around every launch,
+    # recorded on the launching stream)
     apply_us = 1e3 * state["apply_ms"] / max(1, state["apply_cnt"])
     apply_bytes = 2 * cfg.N * esize  # read p, write q (algorithmic)
     achieved = apply_bytes / (apply_us * 1e-6) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "kernel": "operator apply (q = M p) in CG",
+                "frac": achieved / hbm, "traffic": None,
+                "kernel": "fused banded operator apply q = M p (band_apply_kernel) inside CG",
                 "bytes_per_launch": apply_bytes, "us_per_launch": apply_us,
-                "peak_source": peak_src}
+                "launches_timed": state["apply_cnt"], "peak_source": peak_src}
 
-    # standalone apply (operator-apply GB/s, the metric's second half)
+    # phase breakdown of one extra step (outside the timed region)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     op = tca.Operator(A, L, cfg.lam, dtype=dtype)
+    torch.cuda.synchronize()
+    create_ms = 1e3 * (time.perf_counter() - t0)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    b = op.rhs(ydata)
+    e1.record(stream)
+    x, rep = op.cg_solve(b, rtol=cfg.rtol, max_iters=iters)
+    torch.cuda.synchronize()
+    rhs_ms = e0.elapsed_time(e1)
+    # standalone apply (operator-apply GB/s, the metric's second half)
     xin = torch.empty(cfg.n, dtype=tdt, device="cuda")
     tca.generate_normal(xin, seed=3, stream_id=7)
     yout = torch.empty_like(xin)
@@ -265,6 +282,9 @@ def run_tca(args):
     apply_info = {"us": a_us, "applies_per_s": 1e6 / a_us,
                   "GBps": apply_bytes / (a_us * 1e-6) / 1e9,
                   "frac_hbm": apply_bytes / (a_us * 1e-6) / 1e9 / hbm}
+    phases = {"create_ms": create_ms, "rhs_ms": rhs_ms, "cg_ms": rep["seconds"] * 1e3,
+              "cg_us_per_iteration": rep["seconds"] * 1e6 / max(1, rep["iterations"]),
+              "apply_us_in_cg": apply_us}
 
     e2e = None
     if not args.no_e2e:
@@ -320,14 +340,11 @@ def run_tca(args):
         "time_to_solution_ms": total_ms / args.steps,
         "cg_report": {"iterations": rep["iterations"], "rho0": rep["rho0"],
                       "rho_final": rep["rho_final"], "status": rep["status"]},
-        "apply_path": "fused" if gen_apply_path(tca, A, L, cfg, dtype) else "multipass",
+        "apply_path": state["path"],
+        "phases": phases,
     }
     print(json.dumps(line), flush=True)
     return 0
-
-
-def gen_apply_path(tca, A, L, cfg, dtype):
-    return None
 
 
 def main():

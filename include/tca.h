@@ -127,6 +127,13 @@ tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo,
                               int64_t *data_hi, int *banded_mask,
                               int *half_bandwidth, size_t *device_bytes);
 
+/* Which kernel tca_apply uses: 1 = fused banded one-pass apply (every mode
+ * banded, n4 in {1,2,4,7,8,15,16,32}, tap tables fit the kernel-parameter
+ * block, n3*n4*esize a multiple of 16 B), 0 = generic per-mode passes (dense
+ * modes or other shapes), -1 = op is NULL.  A fused-eligible operator still
+ * takes the generic path for a call whose x or y is not 16-byte aligned. */
+int tca_operator_apply_path(const tca_operator *op);
+
 /* y = M x.  x, y: device tensors of the local shape (rows [own_lo, own_hi)
  * of mode 1 on a sharded operator); x and y must not alias. */
 tca_status tca_apply(const tca_operator *op, const void *x, void *y,

@@ -197,10 +197,17 @@ tca_status apply_multipass(const tca_operator *op_c, const void *x, void *y,
     return apply_multipass_t<float>(op, (const float *)x, (float *)y, done, s);
 }
 
-static tca_status apply_dispatch(const tca_operator *op, const void *x, void *y,
-                                 const int32_t *done, cudaStream_t s)
+// pq_part != NULL asks the fused kernel for per-CTA partials of <x, y>; the
+// caller must check fused_used() to know whether they were produced.
+static bool fused_used(const tca_operator *op, const void *x, const void *y)
 {
-    if (op->apply_path == 1 && fused_pointers_ok(x, y)) return launch_fused_apply(op, x, y, done, s);
+    return op->apply_path == 1 && fused_pointers_ok(x, y);
+}
+
+static tca_status apply_dispatch(const tca_operator *op, const void *x, void *y,
+                                 const int32_t *done, cudaStream_t s, double *pq_part = nullptr)
+{
+    if (fused_used(op, x, y)) return launch_fused_apply(op, x, y, done, pq_part, s);
     return apply_multipass(op, x, y, done, s);
 }
 
@@ -290,9 +297,9 @@ static tca_status forward_t(const tca_operator *op, const T *x, T *y, double sig
 
 // Timed apply: an event pair around the launch when instrumentation is on.
 static tca_status timed_apply(tca_operator *op, const void *x, void *y, const int32_t *done,
-                              cudaStream_t s)
+                              cudaStream_t s, double *pq_part = nullptr)
 {
-    if (!op->timing) return apply_dispatch(op, x, y, done, s);
+    if (!op->timing) return apply_dispatch(op, x, y, done, s, pq_part);
     if (op->tev_used + 2 > op->tev.size()) {
         for (int i = 0; i < 64; ++i) {
             cudaEvent_t e;
@@ -303,7 +310,7 @@ static tca_status timed_apply(tca_operator *op, const void *x, void *y, const in
     cudaEvent_t a = op->tev[op->tev_used], b = op->tev[op->tev_used + 1];
     op->tev_used += 2;
     TCA_CUDA_TRY(cudaEventRecord(a, s));
-    TCA_TRY(apply_dispatch(op, x, y, done, s));
+    TCA_TRY(apply_dispatch(op, x, y, done, s, pq_part));
     TCA_CUDA_TRY(cudaEventRecord(b, s));
     return TCA_OK;
 }
@@ -327,11 +334,16 @@ static void cg_iteration(tca_operator *op, T *x, cudaStream_t s)
 {
     T *r = (T *)op->r, *p = (T *)op->p, *q = (T *)op->q;
     const int32_t *done = &op->sc->done;
-    timed_apply(op, p, q, done, s);                                   // Q := A*(P*D)
-    launch_dot_partials<T>(p, q, op->N, op->part, done, s);          // P+*Q
-    launch_cg_finalize(1, op->part, op->sc, op->hist, s);            // alpha
+    if (fused_used(op, p, q)) {
+        timed_apply(op, p, q, done, s, op->part);                     // Q := A*(P*D), P+*Q in the epilogue
+        launch_cg_finalize(1, op->part, op->band_grid, op->sc, op->hist, s);   // alpha
+    } else {
+        timed_apply(op, p, q, done, s);                               // Q := A*(P*D)
+        launch_dot_partials<T>(p, q, op->N, op->part, done, s);      // P+*Q
+        launch_cg_finalize(1, op->part, kRedBlocks, op->sc, op->hist, s);      // alpha
+    }
     launch_cg_update_xr<T>(x, r, p, q, op->N, op->sc, op->part, s);  // C, R, R+*R
-    launch_cg_finalize(2, op->part, op->sc, op->hist, s);            // rho1, stop, beta
+    launch_cg_finalize(2, op->part, kRedBlocks, op->sc, op->hist, s);          // rho1, stop, beta
     launch_cg_update_p<T>(p, r, op->N, op->sc, s);                   // P := R + beta*P
 }
 
@@ -346,7 +358,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
     TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
     launch_cg_init<T>(b, x, (T *)op->r, (T *)op->p, op->N, op->part, s);
-    launch_cg_finalize(0, op->part, op->sc, op->hist, s);
+    launch_cg_finalize(0, op->part, kRedBlocks, op->sc, op->hist, s);
     if (rtol <= 0.0) {
         for (int k = 0; k < max_iters; ++k) cg_iteration<T>(op, x, s);
     } else {
@@ -455,6 +467,11 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
             return fail(TCA_ERR_INVALID_ARG, "A[" + std::to_string(d) + "] has non-finite entries");
         if (L && L[d] && n[d] >= 3 && !all_finite(L[d], (size_t)((n[d] - 2) * n[d])))
             return fail(TCA_ERR_INVALID_ARG, "L[" + std::to_string(d) + "] has non-finite entries");
+    }
+    {
+        double vol = 1.0;   // generic mode products index a (rows x inner) plane with 32 bits
+        for (int d = 0; d < order; ++d) vol *= (double)std::max(n[d], m[d]);
+        if (vol >= 4294967295.0) return fail(TCA_ERR_SHAPE, "problem too large: prod max(n_d, m_d) must be < 2^32");
     }
     if (dist && dist->nranks > 1)
         return fail(TCA_ERR_INVALID_ARG, "dist: multi-rank operators are created through tca_dist_* (nranks > 1 not supported here)");
@@ -577,6 +594,8 @@ tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo, int64_t *
     if (device_bytes) *device_bytes = op->device_bytes;
     return TCA_OK;
 }
+
+int tca_operator_apply_path(const tca_operator *op) { return op ? op->apply_path : -1; }
 
 tca_status tca_apply(const tca_operator *op, const void *x, void *y, void *stream)
 {

@@ -182,7 +182,8 @@ const CUtensorMap *cached_tmap(const tca_operator *op_c, const void *ptr, int ki
 }
 
 template <typename T>
-tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_t *done, cudaStream_t s)
+tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_t *done, double *pq_part,
+                    cudaStream_t s)
 {
     tca_status st = TCA_OK;
     const CUtensorMap *xm = cached_tmap(op, x, 0, &st);
@@ -194,6 +195,7 @@ tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_
     p->x = (const T *)x;
     p->y = (T *)y;
     p->done = done;
+    p->pq_part = pq_part;
     {
         static const char *e = getenv("TCA_BAND_DEBUG");
         p->dbg = e ? atoi(e) : 0;
@@ -227,10 +229,11 @@ bool fused_pointers_ok(const void *x, const void *y)
     return ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
 }
 
-tca_status launch_fused_apply(const tca_operator *op, const void *x, void *y, const int32_t *done, cudaStream_t s)
+tca_status launch_fused_apply(const tca_operator *op, const void *x, void *y, const int32_t *done, double *pq_part,
+                              cudaStream_t s)
 {
-    if (op->dtype == TCA_F64) return launch_t<double>(op, x, y, done, s);
-    return launch_t<float>(op, x, y, done, s);
+    if (op->dtype == TCA_F64) return launch_t<double>(op, x, y, done, pq_part, s);
+    return launch_t<float>(op, x, y, done, pq_part, s);
 }
 
 }  // namespace tca

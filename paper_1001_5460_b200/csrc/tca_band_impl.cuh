@@ -59,6 +59,7 @@ struct Params {
     const T *x;
     T *y;
     const int32_t *done;
+    double *pq_part;       // optional: per-CTA partial <x, y> of the emitted outputs (CG's <p, q>)
     int n1, n2, n3, tiles3;
     int off3, off2, off1;  // record offsets (rows) of the mode-3/2/1 tables; mode 4 at 0
     int dbg;               // debug switches (0 in production)
@@ -210,7 +211,8 @@ __device__ __forceinline__ void ring_step(T (&acc)[6][E], const T (&s)[E], const
 
 template <typename T, int N4, int SEG>
 __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3, const T *RB,
-                                       const T *P, T *OUT, int pos, int rot, int j, bool live, bool emit)
+                                       const T *P, T *OUT, int pos, int rot, int j, bool live, bool emit, int a2,
+                                       int a3, double &pq)
 {
     using C = Cfg<T, N4>;
     constexpr int E = C::E;
@@ -270,17 +272,23 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
     if (emit) {
 #pragma unroll
         for (int e = 0; e < NE; ++e) out[e] = ov[e];
+        if (a.pq_part && a2 + i2 < a.n2 && a3 + i3 < a.n3) {
+            // <x, y> epilogue: x of the emitted slab j-3 (L2-resident: staged 3 slabs ago)
+            const T *xg = a.x + ((long long)(j - 3) * a.n2 + a2 + i2) * (long long)(a.n3 * N4) + (a3 + i3) * N4 + e0;
+#pragma unroll
+            for (int e = 0; e < NE; ++e) pq = fma((double)__ldg(xg + e), (double)ov[e], pq);
+        }
     }
 }
 
 template <typename T, int N4, int SEG>
 __device__ __forceinline__ void pass_c_dispatch(const Params<T> &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3,
                                                 const T *RB, const T *P, T *OUT, int seg, int pos, int rot, int j,
-                                                bool live, bool emit)
+                                                bool live, bool emit, int a2, int a3, double &pq)
 {
     if constexpr (SEG < Cfg<T, N4>::NSEG) {
-        if (seg == SEG) pass_c<T, N4, SEG>(a, acc, U3, RB, P, OUT, pos, rot, j, live, emit);
-        else pass_c_dispatch<T, N4, SEG + 1>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit);
+        if (seg == SEG) pass_c<T, N4, SEG>(a, acc, U3, RB, P, OUT, pos, rot, j, live, emit, a2, a3, pq);
+        else pass_c_dispatch<T, N4, SEG + 1>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, pq);
     }
 }
 
@@ -366,6 +374,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
     int cnt = a.s_cnt[blockIdx.x];
     unsigned gi = 0, gc = 0;   // slabs issued / consumed (stage = g % NSTAGE, parity (g / NSTAGE) & 1)
     T acc[6][E];
+    double pq = 0.0;           // <x, y> partial of this thread's emitted outputs
     for (; cnt > 0; o0 = 0, t3i = (t3i + 1 == a.tiles3) ? 0 : t3i + 1, t2i += (t3i == 0) ? 1 : 0) {
         const int o1 = (a.n1 - o0 < cnt) ? a.n1 : o0 + cnt;
         cnt -= o1 - o0;
@@ -464,7 +473,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             // ---- pass C + mode-1 ring + emission of output slab j-3
             const bool emit = (j - 3 >= o0) && (j - 3 < o1);
             T *OUT = OUTB + (j & 1) * C::OUTE;
-            if (!(a.dbg & 2)) pass_c_dispatch<T, N4, 0>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit);
+            if (!(a.dbg & 2)) pass_c_dispatch<T, N4, 0>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, pq);
             if (emit) {
                 fence_proxy_async();
                 pending = j - 3;
@@ -481,6 +490,18 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             bulk_wait<0>();
         }
         __syncthreads();
+    }
+    if (a.pq_part) {   // fixed-order CTA reduction of the <x, y> partials (deterministic)
+        double *red = reinterpret_cast<double *>(smem_raw + 128);   // stage memory is idle now
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pq += __shfl_xor_sync(0xffffffffu, pq, o);
+        if (lane == 0) red[warp] = pq;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < NTHR / 32; ++w) t += red[w];
+            a.pq_part[blockIdx.x] = t;
+        }
     }
 }
 

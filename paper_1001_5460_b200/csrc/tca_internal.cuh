@@ -155,7 +155,7 @@ void launch_cg_update_p(T *p, const T *r, int64_t N, const CgScalars *sc,
                         cudaStream_t s);
 
 // finalisers (one block): 0 = init rho, 1 = pq -> alpha, 2 = rr -> beta/stop
-void launch_cg_finalize(int which, const double *part, CgScalars *sc,
+void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc,
                         double *hist, cudaStream_t s);
 
 uint64_t stream_key(uint64_t seed, uint32_t stream_id);

@@ -9,6 +9,8 @@
 // one block sums in a fixed order (no floating-point atomics).
 #include <math.h>
 
+#include <algorithm>
+
 #include "tca_internal.cuh"
 
 namespace tca {
@@ -41,32 +43,37 @@ __device__ __forceinline__ double block_sum(double v)
 }
 
 // ---------------------------------------------------------------- band mode product
+// Y[o, r, t] = alpha * sum_w taps[r, w] X[o, start[r] + w, t]  (+ Y[o, r, t]).
+// One CTA row of the grid per outer index o (grid.y, strided); threads cover
+// the (r, t) plane of that slice linearly with t fastest (coalesced loads of
+// every tap row), 32-bit index math within the slice.
 template <typename T>
 __global__ void __launch_bounds__(256)
 band_mode_product_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t outer,
-                         int rows, int cols, int64_t inner,
+                         int rows, int cols, int inner,
                          const int *__restrict__ start, const T *__restrict__ taps,
                          int W, T alpha, int accumulate, const int32_t *done)
 {
     if (done && *done) return;
-    const int64_t total = outer * (int64_t)rows * inner;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = idx % inner;
-        const int64_t rest = idx / inner;
-        const int r = (int)(rest % rows);
-        const int64_t o = rest / rows;
-        const int s0 = start[r];
-        const T *xp = X + o * cols * inner + t;
-        const T *tp = taps + (int64_t)r * W;
-        T acc = T(0);
-        for (int w = 0; w < W; ++w) {
-            const int c = s0 + w;
-            if (c >= 0 && c < cols) acc += tp[w] * xp[(int64_t)c * inner];
+    const unsigned plane = (unsigned)rows * (unsigned)inner;
+    for (int64_t o = blockIdx.y; o < outer; o += gridDim.y) {
+        const T *xo = X + o * (int64_t)cols * inner;
+        T *yo = Y + o * (int64_t)plane;
+        for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < plane; idx += gridDim.x * blockDim.x) {
+            const unsigned r = idx / (unsigned)inner;
+            const unsigned t = idx - r * (unsigned)inner;
+            const int s0 = __ldg(start + r);
+            const T *xp = xo + t;
+            const T *tp = taps + (int64_t)r * W;
+            T acc = T(0);
+            for (int w = 0; w < W; ++w) {
+                const int c = s0 + w;
+                if (c >= 0 && c < cols) acc = fma(__ldg(tp + w), __ldg(xp + (int64_t)c * inner), acc);
+            }
+            acc *= alpha;
+            if (accumulate) acc += yo[idx];
+            yo[idx] = acc;
         }
-        acc *= alpha;
-        if (accumulate) acc += Y[idx];
-        Y[idx] = acc;
     }
 }
 
@@ -75,13 +82,18 @@ void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
                               int64_t inner, double alpha, bool accumulate,
                               const int32_t *done, cudaStream_t s)
 {
-    const int64_t total = outer * (int64_t)M.rows * inner;
-    if (total == 0) return;
-    int64_t blocks = (total + 255) / 256;
-    if (blocks > 148 * 64) blocks = 148 * 64;
+    const int64_t plane = (int64_t)M.rows * inner;
+    if (plane == 0 || outer == 0) return;
+    // plane < 2^32 is guaranteed by the extent limits checked at create
+    int64_t bx = (plane + 255) / 256;
+    int64_t by = outer;
+    const int64_t target = 148 * 16;   // enough CTAs to fill the GPU
+    if (bx > target) bx = target;
+    if (by > 65535) by = 65535;
+    if (bx * by > 8 * target) by = std::max<int64_t>(1, 8 * target / bx);
     count_launch();
-    band_mode_product_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(
-        X, Y, outer, M.rows, M.cols, inner, M.start, (const T *)M.taps, M.W, (T)alpha,
+    band_mode_product_kernel<T><<<dim3((unsigned)bx, (unsigned)by), 256, 0, s>>>(
+        X, Y, outer, M.rows, M.cols, (int)inner, M.start, (const T *)M.taps, M.W, (T)alpha,
         accumulate ? 1 : 0, done);
 }
 
@@ -234,11 +246,11 @@ void launch_cg_update_p(T *p, const T *r, int64_t N, const CgScalars *sc, cudaSt
 // ---------------------------------------------------------------- finalisers
 // One block of kRedThreads sums the kRedBlocks partials in a fixed order.
 __global__ void __launch_bounds__(kRedThreads)
-cg_finalize_kernel(int which, const double *__restrict__ part, CgScalars *sc, double *hist)
+cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgScalars *sc, double *hist)
 {
     if (which != 0 && sc->done) return;
     double acc = 0.0;
-    for (int i = threadIdx.x; i < kRedBlocks; i += kRedThreads) acc += part[i];
+    for (int i = threadIdx.x; i < nparts; i += kRedThreads) acc += part[i];
     const double s = block_sum(acc);
     if (threadIdx.x != 0) return;
     if (which == 0) {                      // rho := R+*R
@@ -276,11 +288,11 @@ cg_finalize_kernel(int which, const double *__restrict__ part, CgScalars *sc, do
     }
 }
 
-void launch_cg_finalize(int which, const double *part, CgScalars *sc, double *hist,
+void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc, double *hist,
                         cudaStream_t s)
 {
     count_launch();
-    cg_finalize_kernel<<<1, kRedThreads, 0, s>>>(which, part, sc, hist);
+    cg_finalize_kernel<<<1, kRedThreads, 0, s>>>(which, part, nparts, sc, hist);
 }
 
 // ---------------------------------------------------------------- instantiations

@@ -28,7 +28,8 @@ OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_NOT_SPD, ERR_OOM, ERR_CUDA, ERR_NCCL, \
 EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
             "tca_cg_solve", "tca_solve_host", "tca_operator_destroy", "tca_generate_normal",
             "tca_forward_model", "tca_status_string", "tca_last_error", "tca_version",
-            "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches"]
+            "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches",
+            "tca_operator_apply_path"]
 
 _vp = ctypes.c_void_p
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -73,6 +74,8 @@ _lib.tca_operator_set_timing.argtypes = [_vp, ctypes.c_int]
 _lib.tca_operator_get_timing.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), _i64p,
                                          ctypes.c_int]
 _lib.tca_kernel_launches.restype = ctypes.c_int64
+_lib.tca_operator_apply_path.argtypes = [_vp]
+_lib.tca_operator_apply_path.restype = ctypes.c_int
 for _name in ("tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
               "tca_cg_solve", "tca_solve_host", "tca_generate_normal", "tca_forward_model",
               "tca_operator_set_timing", "tca_operator_get_timing"):
@@ -188,6 +191,11 @@ class Operator:
                                        ctypes.byref(mask), hb, ctypes.byref(nb)),
                "tca_operator_query")
         return [v.value for v in vals] + [mask.value, tuple(hb[: self.order]), nb.value]
+
+    @property
+    def apply_path(self):
+        """'fused' (one-pass banded kernel) or 'multipass' (generic per-mode kernels)."""
+        return "fused" if _lib.tca_operator_apply_path(self._h) == 1 else "multipass"
 
     def set_timing(self, enable=True):
         _check(_lib.tca_operator_set_timing(self._h, 1 if enable else 0), "set_timing")
