@@ -182,8 +182,6 @@ def run_tca(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 or args.gpus > 1:
-        raise SystemExit("multi-GPU bench needs the sharded operator (not built yet)")
     torch.cuda.set_device(local)
     dev_index = torch.cuda.current_device()
     cfg = synth.CONFIGS[args.config]
@@ -194,18 +192,46 @@ def run_tca(args):
     A, L = synth.mode_matrices(cfg)
     stream = torch.cuda.current_stream()
 
-    gen = tca.Operator(A, L, cfg.lam, dtype=dtype)
-    ydata = gen.forward_model(None, sigma=synth.NOISE_SIGMA, seed=1)  # resident input
+    # ---- distributed plumbing: torch.distributed for the bootstrap and the
+    # timing barrier/max; the library's own NCCL communicator for the halo and
+    # dot-product exchanges of the sharded operator (mode 1 split over ranks)
+    dist_arg, comm, tdist = None, None, None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", rank=rank, world_size=world,
+                                 device_id=torch.device("cuda", local))
+        uid = bytearray(tca.NcclComm.unique_id() if rank == 0 else bytes(128))
+        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+        tdist.broadcast(t, 0)
+        comm = tca.NcclComm(world, bytes(t.cpu().tolist()), rank)
+        dist_arg = comm.dist()
+
+    def barrier():
+        if tdist is not None:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if tdist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    gen = tca.Operator(A, L, cfg.lam, dtype=dtype, dist=dist_arg)
+    ydata = gen.forward_model(None, sigma=synth.NOISE_SIGMA, seed=1)  # resident input (shard-local rows)
+    local_n, local_m = gen.local_n, gen.local_m
+    gen.close()
     torch.cuda.synchronize()
 
     state = {}
 
     def step(timing=False):
-        op = tca.Operator(A, L, cfg.lam, dtype=dtype)          # a1
+        op = tca.Operator(A, L, cfg.lam, dtype=dtype, dist=dist_arg)  # a1
         if timing:
             op.set_timing(True)
-        b = op.rhs(ydata)                                        # a2
-        x, rep = op.cg_solve(b, rtol=cfg.rtol, max_iters=iters)  # a3-a6
+        b = op.rhs(ydata)                                               # a2
+        x, rep = op.cg_solve(b, rtol=cfg.rtol, max_iters=iters)         # a3-a7
         if timing:
             ms, cnt = op.get_timing()
             state["apply_ms"] = state.get("apply_ms", 0.0) + ms
@@ -220,30 +246,31 @@ def run_tca(args):
     for _ in range(args.warmup):
         step()
     state.clear()
-    torch.cuda.synchronize()
+    barrier()
     clocks = ClockSampler(dev_index)
     clocks.start()
     time.sleep(0.3)
     launches0 = tca.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
+    barrier()
     ev0.record(stream)
     for _ in range(args.steps):
         step(timing=True)
     ev1.record(stream)
-    torch.cuda.synchronize()
+    barrier()
     launches = tca.kernel_launches() - launches0
     clk = clocks.stop()
-    total_ms = ev0.elapsed_time(ev1)
-    total_iters = state["iters"]
+    total_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    total_iters = state["iters"]            # iterations of the (global) solve
     value = total_iters / (total_ms * 1e-3)
     hbm, peak_src = peaks()
 
     # dominant kernel: the operator apply inside CG (event pair around every launch,
     # recorded on the launching stream)
+    nloc = int(np.prod(local_n))
     apply_us = 1e3 * state["apply_ms"] / max(1, state["apply_cnt"])
-    apply_bytes = 2 * cfg.N * esize  # read p, write q (algorithmic)
+    apply_bytes = 2 * nloc * esize  # read p, write q (algorithmic, this rank's shard)
     achieved = apply_bytes / (apply_us * 1e-6) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": None,
@@ -252,9 +279,9 @@ def run_tca(args):
                 "launches_timed": state["apply_cnt"], "peak_source": peak_src}
 
     # phase breakdown of one extra step (outside the timed region)
-    torch.cuda.synchronize()
+    barrier()
     t0 = time.perf_counter()
-    op = tca.Operator(A, L, cfg.lam, dtype=dtype)
+    op = tca.Operator(A, L, cfg.lam, dtype=dtype, dist=dist_arg)
     torch.cuda.synchronize()
     create_ms = 1e3 * (time.perf_counter() - t0)
     e0 = torch.cuda.Event(enable_timing=True)
@@ -266,16 +293,16 @@ def run_tca(args):
     torch.cuda.synchronize()
     rhs_ms = e0.elapsed_time(e1)
     # standalone apply (operator-apply GB/s, the metric's second half)
-    xin = torch.empty(cfg.n, dtype=tdt, device="cuda")
+    xin = torch.empty(local_n, dtype=tdt, device="cuda")
     tca.generate_normal(xin, seed=3, stream_id=7)
     yout = torch.empty_like(xin)
     for _ in range(3):
         op.apply(xin, yout)
-    torch.cuda.synchronize()
+    barrier()
     op.set_timing(True)
     for _ in range(args.apply_reps):
         op.apply(xin, yout)
-    torch.cuda.synchronize()
+    barrier()
     ams, acnt = op.get_timing()
     op.close()
     a_us = 1e3 * ams / acnt
@@ -288,40 +315,45 @@ def run_tca(args):
 
     e2e = None
     if not args.no_e2e:
-        yh = torch.empty(ydata.shape, dtype=tdt, pin_memory=True)
+        yh = torch.empty(local_m, dtype=tdt, pin_memory=True)
         yh.copy_(ydata.cpu())
-        xh = torch.empty(cfg.n, dtype=tdt, pin_memory=True)
-        for _ in range(1):
-            op = tca.Operator(A, L, cfg.lam, dtype=dtype)
-            op.solve_host(yh, xh, rtol=cfg.rtol, max_iters=iters)
-            op.close()
+        xh = torch.empty(local_n, dtype=tdt, pin_memory=True)
+        op = tca.Operator(A, L, cfg.lam, dtype=dtype, dist=dist_arg)
+        op.solve_host(yh, xh, rtol=cfg.rtol, max_iters=iters)   # warm-up
+        op.close()
         e_steps = max(1, min(args.steps, 3))
         it_sum = 0
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e_steps):
-            op = tca.Operator(A, L, cfg.lam, dtype=dtype)
-            rep = op.solve_host(yh, xh, rtol=cfg.rtol, max_iters=iters)
-            it_sum += rep["iterations"]
+            op = tca.Operator(A, L, cfg.lam, dtype=dtype, dist=dist_arg)
+            rep_e = op.solve_host(yh, xh, rtol=cfg.rtol, max_iters=iters)
+            it_sum += rep_e["iterations"]
             op.close()
         e1.record(stream)
-        torch.cuda.synchronize()
+        barrier()
         wall = time.perf_counter() - t0
-        e_ms = e0.elapsed_time(e1)
+        e_ms = max_over_ranks(e0.elapsed_time(e1))
         e2e = {"value": it_sum / (e_ms * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(cfg.Mdata * esize), "d2h_bytes_per_step": int(cfg.N * esize),
-               "wall_value": it_sum / wall, "path": "tca_solve_host (pinned host y -> x)"}
+               "h2d_bytes_per_step": int(np.prod(local_m) * esize) * world,
+               "d2h_bytes_per_step": int(nloc * esize) * world,
+               "wall_value": it_sum / wall,
+               "path": "tca_operator_create + tca_solve_host (pinned host y -> rhs -> CG -> host x)"}
 
     cpu = None
-    if not args.no_cpu_baseline and rank == 0:
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
         cpu = cpu_oracle_sample(cfg, args.cpu_seconds, dtype)
 
     rep = state["last_rep"]
+    if comm is not None:
+        comm.close()
+    if rank != 0:
+        if tdist is not None:
+            tdist.destroy_process_group()
+        return 0
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": dtype, "data": "synthetic (seeded counter RNG on device; cubic B-spline A_d)",
@@ -330,7 +362,8 @@ def run_tca(args):
                    "step": "tca_operator_create + tca_rhs + tca_cg_solve + destroy",
                    "l2": "inputs larger than L2 (each vector %d MB, y %d MB)" % (
                        cfg.N * esize >> 20, cfg.Mdata * esize >> 20),
-                   "parallelism": "single GPU"},
+                   "parallelism": "single GPU" if world == 1 else
+                   f"mode-1 sharding over {world} GPUs (NCCL halo + all-reduce)"},
         "roofline": roofline,
         "apply": apply_info,
         "cpu_baseline": cpu,
@@ -344,6 +377,8 @@ def run_tca(args):
         "phases": phases,
     }
     print(json.dumps(line), flush=True)
+    if tdist is not None:
+        tdist.destroy_process_group()
     return 0
 
 

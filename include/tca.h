@@ -63,16 +63,26 @@ typedef struct tca_operator tca_operator;
 
 /*
  * Distributed (mode-1 sharded) operator description.  NULL = single GPU.
- * nccl_comm: an ncclComm_t of nranks ranks, one per GPU, owned by the caller,
- * whose rank r holds mode-1 rows [own_lo, own_hi) of every tensor
- * (tca_operator_query).  The rhs is formed shard-locally from the data rows
- * [data_lo, data_hi) (no communication); apply exchanges 3 boundary mode-1
- * slices with each neighbour; CG all-reduces its two dot products.
+ * mode 1 (slowest) is split into nranks contiguous row
+ * blocks; rank r owns unknown rows [own_lo, own_hi) = [n1*r/P, n1*(r+1)/P)
+ * of every tensor (tca_operator_query), needs n1 >= 3*P, and reads the data
+ * rows [data_lo, data_hi) (support of its unknown rows in A_1) for tca_rhs,
+ * so the rhs is formed shard-locally without communication.  Per apply the
+ * 3 boundary mode-1 slabs are exchanged with each neighbour; CG all-reduces
+ * its two fp64 dot products.  Exactly one transport is given:
+ *   nccl_comm    an ncclComm_t of nranks ranks, one GPU each (tca_nccl_*),
+ *                owned by the caller; collectives run on the call's stream;
+ *   local_group  a tca_local_group of nranks shards driven by host threads
+ *                of one process (test transport for fewer GPUs than shards:
+ *                host-synchronised copies; every rank must call the same
+ *                entry points concurrently from its own thread).
+ * Sharded operators need the fused banded path (all modes banded).
  */
 typedef struct {
     int rank;
     int nranks;
     void *nccl_comm;
+    void *local_group;
 } tca_dist;
 
 /* CG report (SPEC.md:446-449 SolveReport).  rho_history is caller-owned,
@@ -169,6 +179,26 @@ tca_status tca_solve_host(tca_operator *op, const void *ydata_host,
                           tca_cg_report *rep, void *stream);
 
 void tca_operator_destroy(tca_operator *op);
+
+/*
+ * Shard layout (host only, no device needed): for an n1 x ... problem whose
+ * mode-1 basis A1 is m1 x n1 (row-major fp64), rank `rank` of `nranks` owns
+ * unknown rows [out4[0], out4[1]) and reads data rows [out4[2], out4[3]).
+ * TCA_ERR_SHAPE when n1 < 3 * nranks.
+ */
+tca_status tca_shard_layout(int64_t n1, int64_t m1, const double *A1, int rank,
+                            int nranks, int64_t *out4);
+
+/* NCCL bootstrap (libnccl.so.2 is loaded at first use): rank 0 creates the
+ * 128-byte unique id, the caller broadcasts it (e.g. torch.distributed), every
+ * rank creates its communicator on its current device. */
+tca_status tca_nccl_get_unique_id(void *uid128);
+tca_status tca_nccl_comm_create(void **comm, int nranks, const void *uid128, int rank);
+void tca_nccl_comm_destroy(void *comm);
+
+/* In-process shard group for the local transport (see tca_dist). */
+tca_status tca_local_group_create(void **group, int nranks);
+void tca_local_group_destroy(void *group);
 
 /*
  * Seeded synthetic input generator (reading Z9): out[i] = scale *

@@ -274,14 +274,15 @@ template <typename T>
 static tca_status forward_t(const tca_operator *op, const T *x, T *y, double sigma,
                             uint64_t seed, cudaStream_t s)
 {
-    int64_t ein[kD] = {op->n[0], op->n[1], op->n[2], op->n[3]};
-    int64_t eout[kD] = {op->m[0], op->m[1], op->m[2], op->m[3]};
+    // shard-local: data rows [data_lo, data_hi) from unknown rows [xf_lo, xf_hi)
+    int64_t ein[kD] = {op->xf_hi - op->xf_lo, op->n[1], op->n[2], op->n[3]};
+    int64_t eout[kD] = {op->data_hi - op->data_lo, op->m[1], op->m[2], op->m[3]};
     const int64_t N = ein[0] * ein[1] * ein[2] * ein[3];
     const int64_t M = eout[0] * eout[1] * eout[2] * eout[3];
     T *xt = nullptr;
-    if (!x) {
-        TCA_CUDA_TRY(cudaMallocAsync((void **)&xt, N * sizeof(T), s));
-        launch_gen_normal<T>(xt, N, 0, stream_key(seed, 0), 1.0, false, s);
+    if (!x) {   // x_true generated in place, position keyed (global unknown index)
+        TCA_CUDA_TRY(cudaMallocAsync((void **)&xt, std::max<int64_t>(N, 1) * sizeof(T), s));
+        launch_gen_normal<T>(xt, N, op->xf_lo * op->slab, stream_key(seed, 0), 1.0, false, s);
         x = xt;
     }
     std::vector<int> order;
@@ -290,7 +291,8 @@ static tca_status forward_t(const tca_operator *op, const T *x, T *y, double sig
         return (double)eout[a] / ein[a] < (double)eout[c] / ein[c];
     });
     TCA_TRY(chain_products<T>(op, x, y, ein, eout, op->Af, order, s));
-    if (sigma != 0.0) launch_gen_normal<T>(y, M, 0, stream_key(seed, 1), sigma, true, s);
+    const int64_t mslab = op->m[1] * op->m[2] * op->m[3];
+    if (sigma != 0.0) launch_gen_normal<T>(y, M, op->data_lo * mslab, stream_key(seed, 1), sigma, true, s);
     if (xt) TCA_CUDA_TRY(cudaFreeAsync(xt, s));
     return TCA_OK;
 }
@@ -329,22 +331,43 @@ static tca_status harvest_timing(tca_operator *op)
     return TCA_OK;
 }
 
-template <typename T>
-static void cg_iteration(tca_operator *op, T *x, cudaStream_t s)
+// Dot-product finalisation: single GPU one kernel; sharded: local sum, all-reduce
+// of the fp64 scalar over the shards, then the scalar update.
+static tca_status cg_reduce(tca_operator *op, int which, const double *part, int nparts, cudaStream_t s)
 {
-    T *r = (T *)op->r, *p = (T *)op->p, *q = (T *)op->q;
+    if (!op->transport) {
+        launch_cg_finalize(which, part, nparts, op->sc, op->hist, s, 0);
+        return TCA_OK;
+    }
+    launch_cg_finalize(which, part, nparts, op->sc, op->hist, s, 1);
+    TCA_TRY(op->transport->allreduce(&op->sc->red[which], 1, s));
+    launch_cg_finalize(which, part, nparts, op->sc, op->hist, s, 2);
+    return TCA_OK;
+}
+
+static tca_status halo_p(tca_operator *op, cudaStream_t s)
+{
+    if (!op->transport) return TCA_OK;
+    return op->transport->halo(0, (char *)op->p, (size_t)op->slab * op->esize, op->nloc1, s);
+}
+
+template <typename T>
+static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
+{
+    T *r = (T *)op->r, *pe = (T *)op->p, *p = (T *)op->p_own, *q = (T *)op->q;
     const int32_t *done = &op->sc->done;
-    if (fused_used(op, p, q)) {
-        timed_apply(op, p, q, done, s, op->part);                     // Q := A*(P*D), P+*Q in the epilogue
-        launch_cg_finalize(1, op->part, op->band_grid, op->sc, op->hist, s);   // alpha
+    if (fused_used(op, pe, q)) {
+        TCA_TRY(timed_apply(op, pe, q, done, s, op->part));           // Q := A*(P*D), P+*Q in the epilogue
+        TCA_TRY(cg_reduce(op, 1, op->part, op->band_grid, s));       // alpha
     } else {
-        timed_apply(op, p, q, done, s);                               // Q := A*(P*D)
+        TCA_TRY(timed_apply(op, pe, q, done, s));                     // Q := A*(P*D)
         launch_dot_partials<T>(p, q, op->N, op->part, done, s);      // P+*Q
-        launch_cg_finalize(1, op->part, kRedBlocks, op->sc, op->hist, s);      // alpha
+        TCA_TRY(cg_reduce(op, 1, op->part, kRedBlocks, s));          // alpha
     }
     launch_cg_update_xr<T>(x, r, p, q, op->N, op->sc, op->part, s);  // C, R, R+*R
-    launch_cg_finalize(2, op->part, kRedBlocks, op->sc, op->hist, s);          // rho1, stop, beta
+    TCA_TRY(cg_reduce(op, 2, op->part, kRedBlocks, s));              // rho1, stop, beta
     launch_cg_update_p<T>(p, r, op->N, op->sc, s);                   // P := R + beta*P
+    return halo_p(op, s);                                             // ghost slabs of P
 }
 
 template <typename T>
@@ -357,15 +380,16 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     *op->sc_host = h;
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
     TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
-    launch_cg_init<T>(b, x, (T *)op->r, (T *)op->p, op->N, op->part, s);
-    launch_cg_finalize(0, op->part, kRedBlocks, op->sc, op->hist, s);
+    launch_cg_init<T>(b, x, (T *)op->r, (T *)op->p_own, op->N, op->part, s);
+    TCA_TRY(cg_reduce(op, 0, op->part, kRedBlocks, s));
+    TCA_TRY(halo_p(op, s));
     if (rtol <= 0.0) {
-        for (int k = 0; k < max_iters; ++k) cg_iteration<T>(op, x, s);
+        for (int k = 0; k < max_iters; ++k) TCA_TRY(cg_iteration<T>(op, x, s));
     } else {
         const int chunk = 32;
         for (int k = 0; k < max_iters; k += chunk) {
             const int c = std::min(chunk, max_iters - k);
-            for (int i = 0; i < c; ++i) cg_iteration<T>(op, x, s);
+            for (int i = 0; i < c; ++i) TCA_TRY(cg_iteration<T>(op, x, s));
             TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars),
                                          cudaMemcpyDeviceToHost, s));
             TCA_CUDA_TRY(cudaStreamSynchronize(s));
@@ -439,7 +463,8 @@ void tca_operator_destroy(tca_operator *op)
         free_band(op->At[d]);
         free_band(op->Af[d]);
     }
-    void *bufs[] = {op->r, op->p, op->q, op->t0, op->t1, op->part, op->sc, op->hist, op->tmap_dev};
+    delete op->transport;
+    void *bufs[] = {op->r, op->p, op->q, op->t0, op->t1, op->part, op->sc, op->hist, op->tmap_dev, op->x_ext};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (op->sc_host) cudaFreeHost(op->sc_host);
@@ -473,11 +498,43 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
         for (int d = 0; d < order; ++d) vol *= (double)std::max(n[d], m[d]);
         if (vol >= 4294967295.0) return fail(TCA_ERR_SHAPE, "problem too large: prod max(n_d, m_d) must be < 2^32");
     }
-    if (dist && dist->nranks > 1)
-        return fail(TCA_ERR_INVALID_ARG, "dist: multi-rank operators are created through tca_dist_* (nranks > 1 not supported here)");
+    int64_t layout[4] = {0, n[0], 0, m[0]};   // own_lo, own_hi, data_lo, data_hi
+    const bool sharded = dist && dist->nranks > 1;
+    if (dist) {
+        if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks)
+            return fail(TCA_ERR_INVALID_ARG, "dist: rank must be in [0, nranks)");
+        if (sharded && !dist->nccl_comm && !dist->local_group)
+            return fail(TCA_ERR_INVALID_ARG, "dist: a sharded operator needs nccl_comm or local_group");
+        if (sharded && dist->nccl_comm && dist->local_group)
+            return fail(TCA_ERR_INVALID_ARG, "dist: give exactly one of nccl_comm and local_group");
+        if (sharded) TCA_TRY(shard_layout(n[0], A[0], m[0], dist->rank, dist->nranks, layout));
+    }
     cudaStream_t s = (cudaStream_t)stream;
 
     tca_operator *op = new tca_operator();
+    op->own_lo = layout[0];
+    op->own_hi = layout[1];
+    op->data_lo = layout[2];
+    op->data_hi = layout[3];
+    if (sharded) {
+        op->rank = dist->rank;
+        op->nranks = dist->nranks;
+        op->comm = dist->nccl_comm;
+        op->ghost = kHG;
+        // unknown rows the shard's data rows touch (forward model, x NULL)
+        op->xf_lo = n[0];
+        op->xf_hi = 0;
+        for (int64_t k = op->data_lo; k < op->data_hi; ++k)
+            for (int64_t c = 0; c < n[0]; ++c)
+                if (A[0][k * n[0] + c] != 0.0) {
+                    op->xf_lo = std::min(op->xf_lo, c);
+                    op->xf_hi = std::max(op->xf_hi, c + 1);
+                }
+        if (op->xf_hi <= op->xf_lo) { op->xf_lo = 0; op->xf_hi = 0; }
+    } else {
+        op->xf_lo = 0;
+        op->xf_hi = n[0];
+    }
     op->order = order;
     op->dtype = dtype;
     op->esize = dtype == TCA_F64 ? 8 : 4;
@@ -523,14 +580,28 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
             st = make_band(dtype, R, nd, nd, op->hbR[d] <= kHR ? kHR : -1, &op->Rm[d], &bytes);
             if (st != TCA_OK) break;
         }
-        // A_d^T (rows n_d, cols m_d) for the rhs; A_d (rows m_d, cols n_d) for the forward model
-        std::vector<double> At((size_t)nd * md);
-        for (int i = 0; i < md; ++i)
-            for (int j = 0; j < nd; ++j) At[(size_t)j * md + i] = Ad[(size_t)i * nd + j];
-        st = make_band(dtype, At, nd, md, -1, &op->At[d], &bytes);
-        if (st != TCA_OK) break;
-        st = make_band(dtype, Ad, md, nd, -1, &op->Af[d], &bytes);
-        if (st != TCA_OK) break;
+        // A_d^T (rows n_d, cols m_d) for the rhs; A_d (rows m_d, cols n_d) for the
+        // forward model.  Mode 1 of a shard: A_1^T rows [own_lo, own_hi) over data
+        // columns [data_lo, data_hi); A_1 rows [data_lo, data_hi) over unknown
+        // columns [xf_lo, xf_hi) (shard-local rhs and data, no communication).
+        {
+            const int64_t rlo = d == 0 ? op->own_lo : 0, rhi = d == 0 ? op->own_hi : nd;
+            const int64_t clo = d == 0 ? op->data_lo : 0, chi = d == 0 ? op->data_hi : md;
+            const int tr = (int)(rhi - rlo), tc = (int)(chi - clo);
+            std::vector<double> At((size_t)tr * tc);
+            for (int i = 0; i < tc; ++i)
+                for (int j = 0; j < tr; ++j) At[(size_t)j * tc + i] = Ad[(size_t)(clo + i) * nd + rlo + j];
+            st = make_band(dtype, At, tr, tc, -1, &op->At[d], &bytes);
+            if (st != TCA_OK) break;
+            const int64_t frlo = clo, frhi = chi;
+            const int64_t fclo = d == 0 ? op->xf_lo : 0, fchi = d == 0 ? op->xf_hi : nd;
+            const int fr = (int)(frhi - frlo), fc = (int)(fchi - fclo);
+            std::vector<double> Af((size_t)fr * fc);
+            for (int i = 0; i < fr; ++i)
+                for (int j = 0; j < fc; ++j) Af[(size_t)i * fc + j] = Ad[(size_t)(frlo + i) * nd + fclo + j];
+            st = make_band(dtype, Af, fr, fc, -1, &op->Af[d], &bytes);
+            if (st != TCA_OK) break;
+        }
         // symmetric band rows for the fused banded kernel
         op->bandG[d].assign((size_t)nd * 4, 0.0);
         op->bandR[d].assign((size_t)nd * 3, 0.0);
@@ -547,20 +618,27 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
         return st;
     }
     op->all_banded = all_banded;
-    op->own_lo = 0;
-    op->own_hi = op->n[0];
-    op->data_lo = 0;
-    op->data_hi = op->m[0];
     op->nloc1 = op->own_hi - op->own_lo;
-    op->N = op->nloc1 * op->n[1] * op->n[2] * op->n[3];
+    op->slab = op->n[1] * op->n[2] * op->n[3];
+    op->N = op->nloc1 * op->slab;
     op->Mloc = (op->data_hi - op->data_lo) * op->m[1] * op->m[2] * op->m[3];
     op->apply_path = fused_shape_supported(op) ? 1 : 0;
+    if (sharded && op->apply_path != 1) {
+        tca_operator_destroy(op);
+        return fail(TCA_ERR_INVALID_ARG,
+                    "dist: sharded operators need the fused banded path (all modes banded, supported n4, "
+                    "n3*n4*esize a multiple of 16 B)");
+    }
     if (op->apply_path == 1) fused_prepare(op);
+    if (sharded) op->transport = make_transport(dist);
 
     const size_t vb = (size_t)op->N * op->esize;
+    const size_t pb = (size_t)(op->nloc1 + 2 * op->ghost) * op->slab * op->esize;   // ghosted p
     cudaError_t e = cudaSuccess;
     e = cudaMalloc(&op->r, vb);
-    if (e == cudaSuccess) e = cudaMalloc(&op->p, vb);
+    if (e == cudaSuccess) e = cudaMalloc(&op->p, pb);
+    if (e == cudaSuccess) e = cudaMemsetAsync(op->p, 0, pb, s);   // ghosts beyond the domain stay 0
+    if (e == cudaSuccess) op->p_own = (char *)op->p + (size_t)op->ghost * op->slab * op->esize;
     if (e == cudaSuccess) e = cudaMalloc(&op->q, vb);
     if (e == cudaSuccess) e = cudaMalloc(&op->part, sizeof(double) * kRedBlocks * 2);
     if (e == cudaSuccess) e = cudaMalloc(&op->sc, sizeof(CgScalars));
@@ -573,7 +651,7 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
         tca_operator_destroy(op);
         return rs;
     }
-    bytes += vb * 3 + sizeof(double) * kRedBlocks * 2 + sizeof(CgScalars);
+    bytes += vb * 2 + pb + sizeof(double) * kRedBlocks * 2 + sizeof(CgScalars);
     op->device_bytes = bytes;
     *out = op;
     return TCA_OK;
@@ -603,7 +681,22 @@ tca_status tca_apply(const tca_operator *op, const void *x, void *y, void *strea
     if (!x || !y) return fail(TCA_ERR_INVALID_ARG, "x and y must be non-NULL device pointers");
     if (x == y) return fail(TCA_ERR_INVALID_ARG, "x and y must not alias");
     cudaStream_t s = (cudaStream_t)stream;
-    TCA_TRY(timed_apply(const_cast<tca_operator *>(op), x, y, nullptr, s));
+    tca_operator *o = const_cast<tca_operator *>(op);
+    if (o->transport) {   // sharded: ghosted copy of x, halo exchange, then the apply
+        const size_t sb = (size_t)o->slab * o->esize;
+        const size_t xb = (size_t)(o->nloc1 + 2 * o->ghost) * sb;
+        if (!o->x_ext) {
+            TCA_CUDA_TRY(cudaMalloc(&o->x_ext, xb));
+            TCA_CUDA_TRY(cudaMemsetAsync(o->x_ext, 0, xb, s));
+            o->device_bytes += xb;
+        }
+        TCA_CUDA_TRY(cudaMemcpyAsync((char *)o->x_ext + (size_t)o->ghost * sb, x, (size_t)o->nloc1 * sb,
+                                     cudaMemcpyDeviceToDevice, s));
+        TCA_TRY(o->transport->halo(1, (char *)o->x_ext, sb, o->nloc1, s));
+        TCA_TRY(timed_apply(o, o->x_ext, y, nullptr, s));
+    } else {
+        TCA_TRY(timed_apply(o, x, y, nullptr, s));
+    }
     TCA_CUDA_TRY(cudaGetLastError());
     return TCA_OK;
 }

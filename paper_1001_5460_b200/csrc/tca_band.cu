@@ -95,18 +95,22 @@ void build_params(const tca_operator *op, std::vector<unsigned char> &blob)
         p->s_cnt[b] = (int)(u1 - u0);
     }
     const_cast<tca_operator *>(op)->band_grid = G;
+    p->xoff = op->ghost;
+    p->nin = (int)op->nloc1 + 2 * op->ghost;
     p->off1 = L.off[0];
     p->off2 = L.off[1];
     p->off3 = L.off[2];
     for (int d = 0; d < kD; ++d) {
         const int nd = (int)(d == 0 ? op->nloc1 : op->n[d]);
-        const int row0 = d == 0 ? (int)op->own_lo : 0;   // mode-1 rows of this shard
-        for (int r = 0; r < nd; ++r) {
+        const int row0 = d == 0 ? (int)op->own_lo : 0;   // global row of local row 0 (mode 1 of a shard)
+        // mode 1 of a shard also needs the rows of its ghost slabs (neighbours' rows)
+        const int rlo = d == 0 ? -band::PADR : 0, rhi = d == 0 ? nd + band::PADR : nd;
+        for (int r = rlo; r < rhi; ++r) {
+            const int64_t g = row0 + r;
+            if (g < 0 || g >= op->n[d]) continue;   // outside the domain: zero rows
             T *rec = p->taps + (size_t)(L.off[d] + r + band::PADR) * band::REC;
-            for (int k = 0; k < 4; ++k) rec[k] = (T)op->bandG[d][(size_t)(row0 + r) * 4 + k];
-            for (int k = 0; k < 3; ++k) rec[4 + k] = (T)op->bandR[d][(size_t)(row0 + r) * 3 + k];
-            // a band entry G[r, r+k] with r+k beyond this shard's last row stays (the
-            // kernel never pairs it with an in-domain input: TMA zero-fills those slabs)
+            for (int k = 0; k < 4; ++k) rec[k] = (T)op->bandG[d][(size_t)g * 4 + k];
+            for (int k = 0; k < 3; ++k) rec[4 + k] = (T)op->bandR[d][(size_t)g * 3 + k];
         }
     }
 }
@@ -123,7 +127,9 @@ tca_status make_tmap(const tca_operator *op, const void *ptr, int kind, CUtensor
     if (!encode) return fail(TCA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const int n4 = (int)op->n[3];
     const int t3 = t3_of(op);
-    cuuint64_t dims[3] = {(cuuint64_t)(op->n[2] * op->n[3]), (cuuint64_t)op->n[1], (cuuint64_t)op->nloc1};
+    // loads read a ghosted input (nloc1 + 2 ghost slabs), stores write the local output
+    const int64_t slabs = kind == 0 ? op->nloc1 + 2 * op->ghost : op->nloc1;
+    cuuint64_t dims[3] = {(cuuint64_t)(op->n[2] * op->n[3]), (cuuint64_t)op->n[1], (cuuint64_t)slabs};
     cuuint64_t strides[2] = {(cuuint64_t)(op->n[2] * op->n[3] * op->esize),
                              (cuuint64_t)(op->n[1] * op->n[2] * op->n[3] * op->esize)};
     cuuint32_t box[3];

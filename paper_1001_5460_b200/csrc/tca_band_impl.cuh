@@ -60,9 +60,10 @@ struct Params {
     T *y;
     const int32_t *done;
     double *pq_part;       // optional: per-CTA partial <x, y> of the emitted outputs (CG's <p, q>)
-    int n1, n2, n3, tiles3;
-    int off3, off2, off1;  // record offsets (rows) of the mode-3/2/1 tables; mode 4 at 0
-    int dbg;               // debug switches (0 in production)
+    int n1, n2, n3, tiles3;   // n1: output slabs (local rows of a sharded operator)
+    int xoff, nin;            // input slab j lives at slab j + xoff of an input of nin slabs (ghosts)
+    int off3, off2, off1;     // record offsets (rows) of the mode-3/2/1 tables; mode 4 at 0
+    int dbg;                  // debug switches (0 in production)
     short2 s_tile[MAXG];   // CTA b starts at tile (x = mode-2 tile, y = mode-3 tile) ...
     int s_o0[MAXG];        // ... at output slab s_o0 ...
     int s_cnt[MAXG];       // ... and processes s_cnt (tile, slab) units
@@ -274,7 +275,7 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
         for (int e = 0; e < NE; ++e) out[e] = ov[e];
         if (a.pq_part && a2 + i2 < a.n2 && a3 + i3 < a.n3) {
             // <x, y> epilogue: x of the emitted slab j-3 (L2-resident: staged 3 slabs ago)
-            const T *xg = a.x + ((long long)(j - 3) * a.n2 + a2 + i2) * (long long)(a.n3 * N4) + (a3 + i3) * N4 + e0;
+            const T *xg = a.x + ((long long)(j - 3 + a.xoff) * a.n2 + a2 + i2) * (long long)(a.n3 * N4) + (a3 + i3) * N4 + e0;
 #pragma unroll
             for (int e = 0; e < NE; ++e) pq = fma((double)__ldg(xg + e), (double)ov[e], pq);
         }
@@ -383,7 +384,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         const int ca = (a3 - 3) * N4;                              // flat column of staged column 0
         const int delta = ((ca % C::VEC) + C::VEC) % C::VEC;       // boxes start 16-B aligned
         const int j0 = o0 - 3, j1 = o1 + 3;
-        const int jb = j0 > 0 ? j0 : 0, je = j1 < a.n1 ? j1 : a.n1;
+        const int jb = j0 > -a.xoff ? j0 : -a.xoff, je = j1 < a.nin - a.xoff ? j1 : a.nin - a.xoff;
 #pragma unroll
         for (int s = 0; s < 6; ++s)
 #pragma unroll
@@ -401,7 +402,8 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     const int b = warp + k * (NTHR / 32);
                     if (b < C::NB * PR) {
                         const int r = b / C::NB, h = b % C::NB;
-                        tma_load_3d(dst + r * PP + h * C::BOXW, xmp, bar + st, ca - delta + h * C::BOXW, a2 - 3 + r, js);
+                        tma_load_3d(dst + r * PP + h * C::BOXW, xmp, bar + st, ca - delta + h * C::BOXW, a2 - 3 + r,
+                                    js + a.xoff);
                     }
                 }
             }
@@ -414,7 +416,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         int pending = -1;                // output slab whose staging buffer awaits its TMA store
 #pragma unroll 1
         for (int j = j0; j < j1; ++j) {
-            const bool live = j >= 0 && j < a.n1 && !(a.dbg & 8);
+            const bool live = j >= jb && j < je && !(a.dbg & 8);
             const T *P = Pst + (gc % C::NSTAGE) * C::stage_elems + delta;
             if (live && !(a.dbg & 128)) mbar_wait(bar + gc % C::NSTAGE, (gc / C::NSTAGE) & 1);
 

@@ -61,7 +61,22 @@ struct CgScalars {
     int32_t status;  // tca_status
     int32_t converged;
     int32_t pad;
+    double red[3];   // reduced dot products (stage sum -> all-reduce -> stage apply)
 };
+
+// Exchange steps of a mode-1 sharded operator (tca_dist.cu).
+class Transport {
+  public:
+    virtual ~Transport() {}
+    // in-place sum over ranks of `count` fp64 values in device memory
+    virtual tca_status allreduce(double *dev, int count, cudaStream_t s) = 0;
+    // fill the 3 ghost slabs on each side of a ghosted buffer
+    //   ext = [3 ghost | nloc own | 3 ghost] slabs of slab_bytes each
+    // from the neighbours' boundary slabs; which = 0 (CG p) or 1 (apply input)
+    virtual tca_status halo(int which, char *ext, size_t slab_bytes, int64_t nloc, cudaStream_t s) = 0;
+};
+Transport *make_transport(const tca_dist *d);
+tca_status shard_layout(int64_t n1, const double *A1, int64_t m1, int rank, int nranks, int64_t out[4]);
 
 // A cached TMA tensor map (CUtensorMap is 128 bytes, 64-byte aligned).
 struct alignas(64) TmapSlot {
@@ -101,13 +116,20 @@ struct tca_operator {
     // sharding (mode 1)
     int rank = 0, nranks = 1;
     void *comm = nullptr;
+    tca::Transport *transport = nullptr;
+    int ghost = 0;            // ghost slabs on each side of p / x_ext (3 when sharded)
+    int64_t slab = 0;         // elements per mode-1 slab (n2 n3 n4)
+    void *x_ext = nullptr;    // ghosted copy of a tca_apply input (sharded, lazy)
     int64_t own_lo = 0, own_hi = 0, data_lo = 0, data_hi = 0;
+    int64_t xf_lo = 0, xf_hi = 0;   // unknown rows read by the shard-local forward model
     int64_t nloc1 = 0;        // own_hi - own_lo
     int64_t N = 0;            // local unknowns
     int64_t Mloc = 0;         // local data points
 
     // workspaces
-    void *r = nullptr, *p = nullptr, *q = nullptr;
+    void *r = nullptr, *q = nullptr;
+    void *p = nullptr;        // ghosted: [ghost | nloc1 own | ghost] slabs
+    void *p_own = nullptr;    // p + ghost slabs
     void *t0 = nullptr, *t1 = nullptr;   // multi-pass temporaries (lazy)
     double *part = nullptr;              // kRedBlocks reduction partials (x2)
     tca::CgScalars *sc = nullptr;        // device scalars
@@ -155,8 +177,10 @@ void launch_cg_update_p(T *p, const T *r, int64_t N, const CgScalars *sc,
                         cudaStream_t s);
 
 // finalisers (one block): 0 = init rho, 1 = pq -> alpha, 2 = rr -> beta/stop
+// stage: 0 = sum the partials and apply (single GPU), 1 = sum into sc->red[which]
+// only, 2 = apply from sc->red[which] (after the all-reduce)
 void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc,
-                        double *hist, cudaStream_t s);
+                        double *hist, cudaStream_t s, int stage = 0);
 
 uint64_t stream_key(uint64_t seed, uint32_t stream_id);
 

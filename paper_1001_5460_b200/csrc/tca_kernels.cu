@@ -246,13 +246,23 @@ void launch_cg_update_p(T *p, const T *r, int64_t N, const CgScalars *sc, cudaSt
 // ---------------------------------------------------------------- finalisers
 // One block of kRedThreads sums the kRedBlocks partials in a fixed order.
 __global__ void __launch_bounds__(kRedThreads)
-cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgScalars *sc, double *hist)
+cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgScalars *sc, double *hist, int stage)
 {
     if (which != 0 && sc->done) return;
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += kRedThreads) acc += part[i];
-    const double s = block_sum(acc);
-    if (threadIdx.x != 0) return;
+    double s = 0.0;
+    if (stage != 2) {
+        double acc = 0.0;
+        for (int i = threadIdx.x; i < nparts; i += kRedThreads) acc += part[i];
+        s = block_sum(acc);
+        if (threadIdx.x != 0) return;
+        if (stage == 1) {   // local sum only; the all-reduce and stage 2 follow
+            sc->red[which] = s;
+            return;
+        }
+    } else {
+        if (threadIdx.x != 0) return;
+        s = sc->red[which];
+    }
     if (which == 0) {                      // rho := R+*R
         sc->rho = s;
         sc->rho0 = s;
@@ -289,10 +299,10 @@ cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgSca
 }
 
 void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc, double *hist,
-                        cudaStream_t s)
+                        cudaStream_t s, int stage)
 {
     count_launch();
-    cg_finalize_kernel<<<1, kRedThreads, 0, s>>>(which, part, nparts, sc, hist);
+    cg_finalize_kernel<<<1, stage == 2 ? 32 : kRedThreads, 0, s>>>(which, part, nparts, sc, hist, stage);
 }
 
 // ---------------------------------------------------------------- instantiations

@@ -29,7 +29,9 @@ EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
             "tca_cg_solve", "tca_solve_host", "tca_operator_destroy", "tca_generate_normal",
             "tca_forward_model", "tca_status_string", "tca_last_error", "tca_version",
             "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches",
-            "tca_operator_apply_path"]
+            "tca_operator_apply_path", "tca_shard_layout", "tca_nccl_get_unique_id",
+            "tca_nccl_comm_create", "tca_nccl_comm_destroy", "tca_local_group_create",
+            "tca_local_group_destroy"]
 
 _vp = ctypes.c_void_p
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -46,7 +48,9 @@ class CgReport(ctypes.Structure):
 
 
 class Dist(ctypes.Structure):
-    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_comm", _vp)]
+    """tca_dist: mode-1 sharding over nranks (exactly one transport)."""
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_comm", _vp),
+                ("local_group", _vp)]
 
 
 _lib.tca_operator_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _i64p, _i64p, _dpp,
@@ -74,6 +78,19 @@ _lib.tca_operator_set_timing.argtypes = [_vp, ctypes.c_int]
 _lib.tca_operator_get_timing.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), _i64p,
                                          ctypes.c_int]
 _lib.tca_kernel_launches.restype = ctypes.c_int64
+_lib.tca_shard_layout.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
+                                  ctypes.c_int, ctypes.c_int, _i64p]
+_lib.tca_shard_layout.restype = ctypes.c_int
+_lib.tca_nccl_get_unique_id.argtypes = [_vp]
+_lib.tca_nccl_get_unique_id.restype = ctypes.c_int
+_lib.tca_nccl_comm_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _vp, ctypes.c_int]
+_lib.tca_nccl_comm_create.restype = ctypes.c_int
+_lib.tca_nccl_comm_destroy.argtypes = [_vp]
+_lib.tca_nccl_comm_destroy.restype = None
+_lib.tca_local_group_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_int]
+_lib.tca_local_group_create.restype = ctypes.c_int
+_lib.tca_local_group_destroy.argtypes = [_vp]
+_lib.tca_local_group_destroy.restype = None
 _lib.tca_operator_apply_path.argtypes = [_vp]
 _lib.tca_operator_apply_path.restype = ctypes.c_int
 for _name in ("tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
@@ -309,6 +326,61 @@ def generate_normal(out, seed, stream_id, offset=0, scale=1.0, stream=None):
                                     float(scale), _vp(_stream_ptr(stream))),
            "tca_generate_normal")
     return out
+
+
+def shard_layout(n1, A1, rank, nranks):
+    """(own_lo, own_hi, data_lo, data_hi) of a mode-1 shard (host-only library call)."""
+    A1 = np.ascontiguousarray(A1, dtype=np.float64)
+    m1, n1_ = A1.shape
+    assert n1_ == n1
+    out = (ctypes.c_int64 * 4)()
+    _check(_lib.tca_shard_layout(n1, m1, A1.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                 rank, nranks, out), "tca_shard_layout")
+    return tuple(int(v) for v in out)
+
+
+class NcclComm:
+    """NCCL communicator of the library (bootstrap: rank 0's unique id is broadcast
+    by the caller, e.g. over torch.distributed)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(_lib.tca_nccl_get_unique_id(buf), "tca_nccl_get_unique_id")
+        return buf.raw
+
+    def __init__(self, nranks, uid: bytes, rank):
+        self.handle = _vp()
+        buf = ctypes.create_string_buffer(uid, 128)
+        _check(_lib.tca_nccl_comm_create(ctypes.byref(self.handle), nranks, buf, rank),
+               "tca_nccl_comm_create")
+        self.nranks, self.rank = nranks, rank
+
+    def dist(self):
+        return Dist(self.rank, self.nranks, self.handle, None)
+
+    def close(self):
+        if self.handle:
+            _lib.tca_nccl_comm_destroy(self.handle)
+            self.handle = _vp()
+
+
+class LocalGroup:
+    """In-process shard group (local transport): shards driven by host threads."""
+
+    def __init__(self, nranks):
+        self.handle = _vp()
+        _check(_lib.tca_local_group_create(ctypes.byref(self.handle), nranks),
+               "tca_local_group_create")
+        self.nranks = nranks
+
+    def dist(self, rank):
+        return Dist(rank, self.nranks, None, self.handle)
+
+    def close(self):
+        if self.handle:
+            _lib.tca_local_group_destroy(self.handle)
+            self.handle = _vp()
 
 
 def exported_symbols():
