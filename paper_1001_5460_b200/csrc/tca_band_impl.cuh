@@ -273,12 +273,6 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
     if (emit) {
 #pragma unroll
         for (int e = 0; e < NE; ++e) out[e] = ov[e];
-        if (a.pq_part && a2 + i2 < a.n2 && a3 + i3 < a.n3) {
-            // <x, y> epilogue: x of the emitted slab j-3 (L2-resident: staged 3 slabs ago)
-            const T *xg = a.x + ((long long)(j - 3 + a.xoff) * a.n2 + a2 + i2) * (long long)(a.n3 * N4) + (a3 + i3) * N4 + e0;
-#pragma unroll
-            for (int e = 0; e < NE; ++e) pq = fma((double)__ldg(xg + e), (double)ov[e], pq);
-        }
     }
 }
 
@@ -291,6 +285,25 @@ __device__ __forceinline__ void pass_c_dispatch(const Params<T> &a, T (&acc)[6][
         if (seg == SEG) pass_c<T, N4, SEG>(a, acc, U3, RB, P, OUT, pos, rot, j, live, emit, a2, a3, pq);
         else pass_c_dispatch<T, N4, SEG + 1>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, pq);
     }
+}
+
+// <x, y> contribution of one finished output tile: the staged output slab
+// (shared memory, dense [T2][WI]) against x of the same slab (global, L2-resident:
+// it was staged three slabs ago), coalesced over the whole CTA.
+template <typename T, int N4>
+__device__ __forceinline__ double tile_dot(const Params<T> &a, const T *outb, int oslab, int a2, int a3)
+{
+    using C = Cfg<T, N4>;
+    double d = 0.0;
+    const long long row = (long long)a.n3 * N4;
+    const T *xs = a.x + ((long long)(oslab + a.xoff) * a.n2 + a2) * row + (long long)a3 * N4;
+    const int nr = a.n2 - a2 < T2 ? a.n2 - a2 : T2;
+    const int nc = (a.n3 - a3) * N4 < C::WI ? (a.n3 - a3) * N4 : C::WI;
+    for (int e = threadIdx.x; e < T2 * C::WI; e += NTHR) {
+        const int r = e / C::WI, c = e - r * C::WI;
+        if (r < nr && c < nc) d = fma((double)__ldg(xs + r * row + c), (double)outb[e], d);
+    }
+    return d;
 }
 
 // ---------------------------------------------------------------- pass B (compile-time block B)
@@ -454,14 +467,15 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             }
             __syncthreads();   // bar1: U2/RA complete; all threads finished slab j-1
 
-            if (tid == 0) {
-                if (pending >= 0 && !(a.dbg & 1)) {
+            if (pending >= 0) {   // uniform: every thread tracks the same pending slab
+                if (a.pq_part) pq += tile_dot<T, N4>(a, OUTB + ((pending + 3) & 1) * C::OUTE, pending, a2, a3);
+                if (tid == 0 && !(a.dbg & 1)) {
                     // staging buffer of output slab `pending` (written in pass C of slab pending+3)
                     tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                     bulk_commit();
                     bulk_wait_read<1>();
-                    pending = -1;
                 }
+                pending = -1;
             }
             if (live && next < je && !(a.dbg & 64)) {   // stage slab `next` into the stage last read in slab j-1
                 issue(next);
@@ -484,13 +498,15 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             rot = rot == 5 ? 0 : rot + 1;
         }
         __syncthreads();
-        if (tid == 0) {
-            if (pending >= 0 && !(a.dbg & 1)) {
+        if (pending >= 0) {
+            if (a.pq_part) pq += tile_dot<T, N4>(a, OUTB + ((pending + 3) & 1) * C::OUTE, pending, a2, a3);
+            if (tid == 0 && !(a.dbg & 1)) {
                 tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                 bulk_commit();
             }
-            bulk_wait<0>();
+            pending = -1;
         }
+        if (tid == 0) bulk_wait<0>();   // the next segment rewrites the staging buffers
         __syncthreads();
     }
     if (a.pq_part) {   // fixed-order CTA reduction of the <x, y> partials (deterministic)
