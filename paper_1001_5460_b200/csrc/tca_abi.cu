@@ -3,6 +3,7 @@
 // detection, tap tables), and the orchestration of the device kernels.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -356,7 +357,8 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
 {
     T *r = (T *)op->r, *pe = (T *)op->p, *p = (T *)op->p_own, *q = (T *)op->q;
     const int32_t *done = &op->sc->done;
-    if (fused_used(op, pe, q)) {
+    static const bool no_fused_dot = getenv("TCA_NO_FUSED_DOT") != nullptr;   // measurement switch
+    if (fused_used(op, pe, q) && !no_fused_dot) {
         TCA_TRY(timed_apply(op, pe, q, done, s, op->part));           // Q := A*(P*D), P+*Q in the epilogue
         TCA_TRY(cg_reduce(op, 1, op->part, op->band_grid, s));       // alpha
     } else {

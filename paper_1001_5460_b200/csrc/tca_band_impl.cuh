@@ -187,7 +187,7 @@ __device__ __forceinline__ T tapR(const Params<T> &a, int off, int r, int k)
 // of j-3 is emitted and reused for j+3.
 template <typename T, int E, int ROT>
 __device__ __forceinline__ void ring_step(T (&acc)[6][E], const T (&s)[E], const T (&q)[E], const T (&pc)[E],
-                                          const T (&g1)[7], const T (&r1)[5], T (&ov)[E])
+                                          const T (&g1)[7], const T (&r1)[5], T (&ov)[E], bool dot, double &pq)
 {
     // s: in-slice Kronecker part (goes through G1), q: in-slice regulariser
     // part (identity in mode 1: added to output j only), pc: p itself (R1).
@@ -202,9 +202,17 @@ __device__ __forceinline__ void ring_step(T (&acc)[6][E], const T (&s)[E], const
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             T v = acc[(ROT + o + 6) % 6][e];
+            if (o == 0 && dot) pq = fma((double)pc[e], (double)v, pq);   // <p_j, old> (see below)
             v = fma(g1[o + 3], s[e], v);
             v = fma(r1[o + 2], pc[e], v);
-            if (o == 0) v += q[e];
+            if (o == 0) {
+                v += q[e];
+                // <p, Mp> without a p history: M is block-symmetric along mode 1,
+                // so <p, Mp> = sum_j <p_j, M_jj p_j + 2 sum_{j'<j} M_jj' p_j'> and the
+                // slot of output j holds exactly sum_{j'<j} M_jj' p_j' before slab j
+                // is added:  contribution = <p_j, old> + <p_j, new>
+                if (dot) pq = fma((double)pc[e], (double)v, pq);
+            }
             acc[(ROT + o + 6) % 6][e] = v;
         }
     }
@@ -213,7 +221,7 @@ __device__ __forceinline__ void ring_step(T (&acc)[6][E], const T (&s)[E], const
 template <typename T, int N4, int SEG>
 __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3, const T *RB,
                                        const T *P, T *OUT, int pos, int rot, int j, bool live, bool emit, int a2,
-                                       int a3, double &pq)
+                                       int a3, int o0, int o1, double &pq)
 {
     using C = Cfg<T, N4>;
     constexpr int E = C::E;
@@ -256,18 +264,20 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
     }
     // mode-1 taps of input slab j: G1[j+o, j], lambda R1[j+o, j]
     T g1[7], r1[5];
+    const int b1 = __shfl_sync(0xffffffffu, a.off1 + j, 0);   // uniform table row base (LDCU, UR operands)
 #pragma unroll
-    for (int o = -3; o <= 3; ++o) g1[o + 3] = tapG(a, a.off1, j + o, -o);
+    for (int o = -3; o <= 3; ++o) g1[o + 3] = tapG(a, 0, b1 + o, -o);
 #pragma unroll
-    for (int o = -2; o <= 2; ++o) r1[o + 2] = tapR(a, a.off1, j + o, -o);
+    for (int o = -2; o <= 2; ++o) r1[o + 2] = tapR(a, 0, b1 + o, -o);
     T *out = OUT + (pos / C::T3) * C::WI + (pos % C::T3) * N4 + e0;
     T ov[E];
+    const bool dot = a.pq_part != nullptr && j >= o0 && j < o1;   // input slab j is one of this CTA's
     switch (rot) {
 #define TCA_ROT(R)                                                  \
     case R:                                                         \
-        ring_step<T, E, R>(acc, s, q, pc, g1, r1, ov);           \
+        ring_step<T, E, R>(acc, s, q, pc, g1, r1, ov, dot, pq);     \
         break;
-        TCA_ROT(0) TCA_ROT(1) TCA_ROT(2) TCA_ROT(3) TCA_ROT(4) default: ring_step<T, E, 5>(acc, s, q, pc, g1, r1, ov);
+        TCA_ROT(0) TCA_ROT(1) TCA_ROT(2) TCA_ROT(3) TCA_ROT(4) default: ring_step<T, E, 5>(acc, s, q, pc, g1, r1, ov, dot, pq);
 #undef TCA_ROT
     }
     if (emit) {
@@ -279,31 +289,12 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
 template <typename T, int N4, int SEG>
 __device__ __forceinline__ void pass_c_dispatch(const Params<T> &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3,
                                                 const T *RB, const T *P, T *OUT, int seg, int pos, int rot, int j,
-                                                bool live, bool emit, int a2, int a3, double &pq)
+                                                bool live, bool emit, int a2, int a3, int o0, int o1, double &pq)
 {
     if constexpr (SEG < Cfg<T, N4>::NSEG) {
-        if (seg == SEG) pass_c<T, N4, SEG>(a, acc, U3, RB, P, OUT, pos, rot, j, live, emit, a2, a3, pq);
-        else pass_c_dispatch<T, N4, SEG + 1>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, pq);
+        if (seg == SEG) pass_c<T, N4, SEG>(a, acc, U3, RB, P, OUT, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
+        else pass_c_dispatch<T, N4, SEG + 1>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
     }
-}
-
-// <x, y> contribution of one finished output tile: the staged output slab
-// (shared memory, dense [T2][WI]) against x of the same slab (global, L2-resident:
-// it was staged three slabs ago), coalesced over the whole CTA.
-template <typename T, int N4>
-__device__ __forceinline__ double tile_dot(const Params<T> &a, const T *outb, int oslab, int a2, int a3)
-{
-    using C = Cfg<T, N4>;
-    double d = 0.0;
-    const long long row = (long long)a.n3 * N4;
-    const T *xs = a.x + ((long long)(oslab + a.xoff) * a.n2 + a2) * row + (long long)a3 * N4;
-    const int nr = a.n2 - a2 < T2 ? a.n2 - a2 : T2;
-    const int nc = (a.n3 - a3) * N4 < C::WI ? (a.n3 - a3) * N4 : C::WI;
-    for (int e = threadIdx.x; e < T2 * C::WI; e += NTHR) {
-        const int r = e / C::WI, c = e - r * C::WI;
-        if (r < nr && c < nc) d = fma((double)__ldg(xs + r * row + c), (double)outb[e], d);
-    }
-    return d;
 }
 
 // ---------------------------------------------------------------- pass B (compile-time block B)
@@ -317,6 +308,8 @@ __device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T 
             pass_b<T, N4, B + 1>(a, U2, RA, P, U3, RB, a3, warp, lane);
             return;
         }
+        constexpr int h0b = B * C::BL;
+        const int r3 = __shfl_sync(0xffffffffu, a.off3 + a3 + h0b, 0);   // uniform table row base (all lanes)
         const int l = (warp % C::WPB) * 32 + lane;
         if (l >= C::LPB) return;
         const int i2 = l / N4, i4 = l % N4;
@@ -331,17 +324,16 @@ __device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T 
         for (int m = 0; m < C::BL + 4; ++m) w[m] = pp[m * N4];
 #pragma unroll
         for (int o = 0; o < C::BL; ++o) { u[o] = T(0); rr[o] = RA[ob + o * N4]; }
-        const int r3 = a3 + h0;   // uniform
 #pragma unroll
         for (int m = 0; m < C::BL + 6; ++m)
 #pragma unroll
             for (int o = 0; o < C::BL; ++o)
-                if (m - o - 3 >= -3 && m - o - 3 <= 3) u[o] = fma(tapG(a, a.off3, r3 + o, m - o - 3), v[m], u[o]);
+                if (m - o - 3 >= -3 && m - o - 3 <= 3) u[o] = fma(tapG(a, 0, r3 + o, m - o - 3), v[m], u[o]);
 #pragma unroll
         for (int m = 0; m < C::BL + 4; ++m)
 #pragma unroll
             for (int o = 0; o < C::BL; ++o)
-                if (m - o - 2 >= -2 && m - o - 2 <= 2) rr[o] = fma(tapR(a, a.off3, r3 + o, m - o - 2), w[m], rr[o]);
+                if (m - o - 2 >= -2 && m - o - 2 <= 2) rr[o] = fma(tapR(a, 0, r3 + o, m - o - 2), w[m], rr[o]);
 #pragma unroll
         for (int o = 0; o < C::BL; ++o) {
             U3[ob + o * N4] = u[o];
@@ -394,6 +386,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         cnt -= o1 - o0;
         const int a2 = __shfl_sync(0xffffffffu, t2i * T2, 0);   // provably warp-uniform
         const int a3 = __shfl_sync(0xffffffffu, t3i * T3, 0);
+        const int b2 = __shfl_sync(0xffffffffu, a.off2 + t2i * T2, 0);   // uniform mode-2 table row base
         const int ca = (a3 - 3) * N4;                              // flat column of staged column 0
         const int delta = ((ca % C::VEC) + C::VEC) % C::VEC;       // boxes start 16-B aligned
         const int j0 = o0 - 3, j1 = o1 + 3;
@@ -402,6 +395,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         for (int s = 0; s < 6; ++s)
 #pragma unroll
             for (int e = 0; e < E; ++e) acc[s][e] = T(0);
+
         // prologue: stage the first NSTAGE-1 in-range slabs
         // stage slab js: NB boxes per staged row, issued round-robin by lane 0 of
         // every warp (one warp issuing all of them serialises ~30 UTMALDG)
@@ -447,7 +441,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     for (int s = 0; s < PR; ++s)
 #pragma unroll
                         for (int r = 0; r < T2; ++r)
-                            if (s - r - 3 >= -3 && s - r - 3 <= 3) u[r] = fma(tapG(a, a.off2, a2 + r, s - r - 3), v[s], u[r]);
+                            if (s - r - 3 >= -3 && s - r - 3 <= 3) u[r] = fma(tapG(a, 0, b2 + r, s - r - 3), v[s], u[r]);
 #pragma unroll
                     for (int r = 0; r < T2; ++r) U2[r * C::WP + c] = u[r];
                     const int ci = c - 3 * N4;
@@ -459,7 +453,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
 #pragma unroll
                             for (int r = 0; r < T2; ++r)
                                 if (s - r - 3 >= -2 && s - r - 3 <= 2)
-                                    u[r] = fma(tapR(a, a.off2, a2 + r, s - r - 3), v[s], u[r]);
+                                    u[r] = fma(tapR(a, 0, b2 + r, s - r - 3), v[s], u[r]);
 #pragma unroll
                         for (int r = 0; r < T2; ++r) RA[r * C::WIP + ci] = u[r];
                     }
@@ -468,7 +462,6 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             __syncthreads();   // bar1: U2/RA complete; all threads finished slab j-1
 
             if (pending >= 0) {   // uniform: every thread tracks the same pending slab
-                if (a.pq_part) pq += tile_dot<T, N4>(a, OUTB + ((pending + 3) & 1) * C::OUTE, pending, a2, a3);
                 if (tid == 0 && !(a.dbg & 1)) {
                     // staging buffer of output slab `pending` (written in pass C of slab pending+3)
                     tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
@@ -489,7 +482,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             // ---- pass C + mode-1 ring + emission of output slab j-3
             const bool emit = (j - 3 >= o0) && (j - 3 < o1);
             T *OUT = OUTB + (j & 1) * C::OUTE;
-            if (!(a.dbg & 2)) pass_c_dispatch<T, N4, 0>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, pq);
+            if (!(a.dbg & 2)) pass_c_dispatch<T, N4, 0>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
             if (emit) {
                 fence_proxy_async();
                 pending = j - 3;
@@ -499,7 +492,6 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         }
         __syncthreads();
         if (pending >= 0) {
-            if (a.pq_part) pq += tile_dot<T, N4>(a, OUTB + ((pending + 3) & 1) * C::OUTE, pending, a2, a3);
             if (tid == 0 && !(a.dbg & 1)) {
                 tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                 bulk_commit();
