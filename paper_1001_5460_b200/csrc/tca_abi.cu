@@ -470,6 +470,9 @@ void tca_operator_destroy(tca_operator *op)
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (op->sc_host) cudaFreeHost(op->sc_host);
+    if (op->tmap_host) cudaFreeHost(op->tmap_host);
+    for (cudaEvent_t e : op->tmap_ev)
+        if (e) cudaEventDestroy(e);
     if (op->ev0) cudaEventDestroy(op->ev0);
     if (op->ev1) cudaEventDestroy(op->ev1);
     for (cudaEvent_t e : op->tev) cudaEventDestroy(e);
@@ -549,6 +552,14 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&op->num_sms, cudaDevAttrMultiProcessorCount, dev);
+        // rhs / forward-model / host-solve temporaries are stream-ordered
+        // allocations of up to several GB: keep freed blocks in the device's
+        // default pool (no unmap/remap of GBs at every synchronisation)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
     }
     size_t bytes = 0;
     tca_status st = TCA_OK;

@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 
 #include "tca_band_impl.cuh"
@@ -154,13 +155,20 @@ tca_status make_tmap(const tca_operator *op, const void *ptr, int kind, CUtensor
 
 // Per-operator cache of tensor maps keyed by (pointer, kind); the descriptors
 // live in a device buffer of kTmapSlots slots (round-robin replacement).
-const CUtensorMap *cached_tmap(const tca_operator *op_c, const void *ptr, int kind, tca_status *st)
+const CUtensorMap *cached_tmap(const tca_operator *op_c, const void *ptr, int kind, cudaStream_t s, tca_status *st,
+                               int *slot_out)
 {
     tca_operator *op = const_cast<tca_operator *>(op_c);
     for (auto &e : op->tmaps)
-        if (e.ptr == ptr && e.kind == kind) return reinterpret_cast<const CUtensorMap *>(op->tmap_dev) + e.slot;
+        if (e.ptr == ptr && e.kind == kind) {
+            *slot_out = e.slot;
+            return reinterpret_cast<const CUtensorMap *>(op->tmap_dev) + e.slot;
+        }
     if (!op->tmap_dev) {
         cudaError_t e = cudaMalloc(&op->tmap_dev, sizeof(CUtensorMap) * kTmapSlots);
+        if (e == cudaSuccess) e = cudaMallocHost(&op->tmap_host, sizeof(CUtensorMap) * kTmapSlots);
+        for (int i = 0; i < kTmapSlots && e == cudaSuccess; ++i)
+            e = cudaEventCreateWithFlags(&op->tmap_ev[i], cudaEventDisableTiming);
         if (e != cudaSuccess) { *st = cuda_fail(e, "tensor-map buffer"); return nullptr; }
     }
     TmapSlot slot;
@@ -176,14 +184,17 @@ const CUtensorMap *cached_tmap(const tca_operator *op_c, const void *ptr, int ki
         for (auto &e : op->tmaps)
             if (e.slot == slot.slot) e = slot;
         op->tmap_next = (op->tmap_next + 1) % kTmapSlots;
+        // a recycled slot may still be read by an earlier launch: wait for it
+        cudaError_t e = cudaEventSynchronize(op->tmap_ev[slot.slot]);
+        if (e != cudaSuccess) { *st = cuda_fail(e, "tensor-map slot event"); return nullptr; }
     }
-    // synchronous: the slot may still be read by a kernel in flight (stream order
-    // on the legacy stream is not guaranteed), so wait for the device first
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e == cudaSuccess)
-        e = cudaMemcpy(reinterpret_cast<CUtensorMap *>(op->tmap_dev) + slot.slot, slot.map, sizeof(CUtensorMap),
-                       cudaMemcpyHostToDevice);
+    // stream-ordered upload from a host copy that lives as long as the operator
+    std::memcpy(op->tmap_host + (size_t)slot.slot * 16, slot.map, sizeof(CUtensorMap));
+    cudaError_t e = cudaMemcpyAsync(reinterpret_cast<CUtensorMap *>(op->tmap_dev) + slot.slot,
+                                    op->tmap_host + (size_t)slot.slot * 16, sizeof(CUtensorMap),
+                                    cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) { *st = cuda_fail(e, "tensor-map upload"); return nullptr; }
+    *slot_out = slot.slot;
     return reinterpret_cast<const CUtensorMap *>(op->tmap_dev) + slot.slot;
 }
 
@@ -192,9 +203,10 @@ tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_
                     cudaStream_t s)
 {
     tca_status st = TCA_OK;
-    const CUtensorMap *xm = cached_tmap(op, x, 0, &st);
+    int xs = 0, ys = 0;
+    const CUtensorMap *xm = cached_tmap(op, x, 0, s, &st, &xs);
     if (!xm) return st;
-    const CUtensorMap *ym = cached_tmap(op, y, 1, &st);
+    const CUtensorMap *ym = cached_tmap(op, y, 1, s, &st, &ys);
     if (!ym) return st;
     // the parameter block is prebuilt at create; patch the per-call pointers
     band::Params<T> *p = reinterpret_cast<band::Params<T> *>(const_cast<unsigned char *>(op->band_params.data()));
@@ -206,7 +218,11 @@ tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_
         static const char *e = getenv("TCA_BAND_DEBUG");
         p->dbg = e ? atoi(e) : 0;
     }
-    return band::launch_dispatch<T>(op, *p, s, xm, ym);
+    TCA_TRY(band::launch_dispatch<T>(op, *p, s, xm, ym));
+    // the slots are in use until this launch completes
+    TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[xs], s));
+    TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[ys], s));
+    return TCA_OK;
 }
 
 }  // namespace

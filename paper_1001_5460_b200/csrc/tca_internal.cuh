@@ -92,6 +92,8 @@ constexpr int kTmapSlots = 32;
 struct tca_operator {
     std::vector<tca::TmapSlot> tmaps;    // TMA descriptors of recent apply inputs/outputs
     void *tmap_dev = nullptr;            // device copies (kTmapSlots x 128 B)
+    uint64_t *tmap_host = nullptr;       // pinned host staging of the descriptors
+    cudaEvent_t tmap_ev[tca::kTmapSlots] = {};   // last launch reading each slot
     int tmap_next = 0;
     int order = 0;
     int64_t n[tca::kD] = {1, 1, 1, 1};   // global unknown extents (padded)
