@@ -127,6 +127,9 @@ static tca_status make_band(tca_dtype dt, const std::vector<double> &M, int rows
     out->rows = rows;
     out->cols = cols;
     out->W = W;
+    out->dense = (W == cols);
+    for (int r = 0; r < rows && out->dense; ++r)
+        if (start[r] != 0) out->dense = false;
     TCA_CUDA_TRY(cudaMalloc(&out->start, sizeof(int) * std::max(rows, 1)));
     *bytes += sizeof(int) * std::max(rows, 1);
     TCA_CUDA_TRY(cudaMemcpy(out->start, start.data(), sizeof(int) * rows, cudaMemcpyHostToDevice));
@@ -155,6 +158,22 @@ static int64_t outer_of(const int64_t *ext, int d)
     return p;
 }
 
+// One mode product: dense fp64 factors run on the FP64 tensor cores (DMMA),
+// everything else on the compressed-band kernel.
+template <typename T>
+static void mode_product(const T *X, T *Y, int64_t outer, const BandMat &M, int64_t inner, double alpha,
+                         bool accumulate, const int32_t *done, cudaStream_t s)
+{
+    if constexpr (sizeof(T) == 8) {
+        if (M.dense && M.rows >= 8 && M.cols >= 8) {
+            launch_dense_mode_product_dmma((const double *)X, (double *)Y, outer, M.rows, M.cols, inner,
+                                           (const double *)M.taps, alpha, accumulate, done, s);
+            return;
+        }
+    }
+    launch_band_mode_product<T>(X, Y, outer, M, inner, alpha, accumulate, done, s);
+}
+
 template <typename T>
 static tca_status apply_multipass_t(const tca_operator *op, const T *x, T *y,
                                     const int32_t *done, cudaStream_t s)
@@ -170,8 +189,7 @@ static tca_status apply_multipass_t(const tca_operator *op, const T *x, T *y,
     for (size_t i = 0; i < active.size(); ++i) {
         const int d = active[i];
         T *out = (i + 1 == active.size()) ? y : bufs[nb];
-        launch_band_mode_product<T>(in, out, outer_of(ext, d), op->Gm[d], inner_of(ext, d), 1.0,
-                                    false, done, s);
+        mode_product<T>(in, out, outer_of(ext, d), op->Gm[d], inner_of(ext, d), 1.0, false, done, s);
         in = out;
         nb ^= 1;
     }
@@ -242,8 +260,7 @@ static tca_status chain_products(const tca_operator *op, const T *in, T *out,
     for (size_t i = 0; i < order.size(); ++i) {
         const int d = order[i];
         T *dst = (i + 1 == order.size()) ? out : tmp[i & 1];
-        launch_band_mode_product<T>(cur, dst, outer_of(ext, d), mats[d], inner_of(ext, d), 1.0,
-                                    false, nullptr, s);
+        mode_product<T>(cur, dst, outer_of(ext, d), mats[d], inner_of(ext, d), 1.0, false, nullptr, s);
         ext[d] = ext_out[d];
         cur = dst;
     }

@@ -45,6 +45,7 @@ struct BandMat {
     int rows = 0, cols = 0, W = 0;
     int *start = nullptr;  // device, rows
     void *taps = nullptr;  // device, rows*W of the operator dtype
+    bool dense = false;    // W == cols and start == 0: taps is the dense row-major matrix
 };
 
 // Device-resident CG scalars (always fp64, reading Z10).
@@ -159,6 +160,11 @@ template <typename T>
 void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
                               int64_t inner, double alpha, bool accumulate,
                               const int32_t *done, cudaStream_t s);
+
+// dense fp64 mode product on the FP64 tensor cores (DMMA); M row-major rows x cols
+void launch_dense_mode_product_dmma(const double *X, double *Y, int64_t outer, int rows, int cols,
+                                    int64_t inner, const double *M, double alpha, bool accumulate,
+                                    const int32_t *done, cudaStream_t s);
 
 template <typename T>
 void launch_gen_normal(T *out, int64_t count, int64_t offset, uint64_t key,

@@ -97,6 +97,82 @@ void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
         accumulate ? 1 : 0, done);
 }
 
+// ---------------------------------------------------------------- dense mode product on FP64 tensor cores
+// Y[o, r, t] = alpha * sum_c M[r, c] X[o, c, t] (+ Y) for a dense M (rows x cols):
+// per fibre f = (o, t) a GEMM  Y[r, f] = M[r, :] X[:, f].  One warp computes
+// 8 x 8 output tiles (8 rows of M x 8 consecutive fibres) with
+// mma.sync.m8n8k4.f64 (DMMA: tcgen05 has no f64 kind, SURVEY.md reading Z14),
+// K stepped by 4 over the columns of M; fragments are read straight from
+// global memory (M is at most a few hundred rows; X fibres are coalesced over
+// t).  Used for dense modes (config 1's Gaussian A_d) in fp64.
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256)
+dense_mode_product_dmma_kernel(const double *__restrict__ X, double *__restrict__ Y, int64_t nfib, int rows,
+                               int cols, int64_t inner, const double *__restrict__ M, double alpha, int accumulate,
+                               const int32_t *done)
+{
+    if (done && *done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int rtiles = (rows + 7) / 8;
+    const int64_t ftiles = (nfib + 7) / 8;
+    const int ar = lane >> 2, ak = lane & 3;          // A fragment: M[r0 + ar][k + ak]
+    const int bk = lane & 3, bn = lane >> 2;          // B fragment: X[k + bk][f0 + bn]
+    const int dr = lane >> 2, dn = 2 * (lane & 3);    // D fragment: Y[r0 + dr][f0 + dn + {0,1}]
+    for (int64_t tile = warp; tile < (int64_t)rtiles * ftiles; tile += nwarps) {
+        const int r0 = (int)(tile % rtiles) * 8;
+        const int64_t f0 = (tile / rtiles) * 8;
+        const int64_t fb = f0 + bn;
+        const bool bvalid = fb < nfib;
+        const int64_t ob = bvalid ? fb / inner : 0, tb = bvalid ? fb - ob * inner : 0;
+        const double *xb = X + ob * (int64_t)cols * inner + tb;
+        const int ra = r0 + ar;
+        const double *ma = M + (int64_t)(ra < rows ? ra : 0) * cols;
+        double d0 = 0.0, d1 = 0.0;
+        for (int k = 0; k < cols; k += 4) {
+            const int ka = k + ak, kb = k + bk;
+            const double a = (ra < rows && ka < cols) ? __ldg(ma + ka) : 0.0;
+            const double b = (bvalid && kb < cols) ? __ldg(xb + (int64_t)kb * inner) : 0.0;
+            dmma884(d0, d1, a, b);
+        }
+        const int r = r0 + dr;
+        if (r < rows) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t f = f0 + dn + h;
+                if (f < nfib) {
+                    const int64_t o = f / inner, t = f - o * inner;
+                    double *yp = Y + (o * rows + r) * inner + t;
+                    double v = alpha * (h ? d1 : d0);
+                    if (accumulate) v += *yp;
+                    *yp = v;
+                }
+            }
+        }
+    }
+}
+
+void launch_dense_mode_product_dmma(const double *X, double *Y, int64_t outer, int rows, int cols,
+                                    int64_t inner, const double *M, double alpha, bool accumulate,
+                                    const int32_t *done, cudaStream_t s)
+{
+    const int64_t nfib = outer * inner;
+    if (nfib == 0 || rows == 0) return;
+    const int64_t tiles = (int64_t)((rows + 7) / 8) * ((nfib + 7) / 8);
+    int64_t blocks = (tiles + 7) / 8;   // 8 warps per block, one tile per warp per pass
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    count_launch();
+    dense_mode_product_dmma_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, Y, nfib, rows, cols, inner, M, alpha,
+                                                                    accumulate ? 1 : 0, done);
+}
+
 // ---------------------------------------------------------------- generator (Z9)
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
 
