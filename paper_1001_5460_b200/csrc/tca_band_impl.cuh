@@ -63,7 +63,7 @@ struct Params {
     int n1, n2, n3, tiles3;   // n1: output slabs (local rows of a sharded operator)
     int xoff, nin;            // input slab j lives at slab j + xoff of an input of nin slabs (ghosts)
     int off3, off2, off1;     // record offsets (rows) of the mode-3/2/1 tables; mode 4 at 0
-    int dbg;                  // debug switches (0 in production)
+    int dbg;                  // phase switches for bisecting (TCA_BAND_DEBUG; 0 in production)
     short2 s_tile[MAXG];   // CTA b starts at tile (x = mode-2 tile, y = mode-3 tile) ...
     int s_o0[MAXG];        // ... at output slab s_o0 ...
     int s_cnt[MAXG];       // ... and processes s_cnt (tile, slab) units
@@ -171,11 +171,6 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // ---------------------------------------------------------------- taps
 // rec(r) = taps + (off + r + PADR) * REC; G(r, k) = G[r, r+k], R(r, k) = lambda R[r, r+k]
 // (symmetric: G[r, r-k] = G[r-k, r]).  Tables are zero outside the domain rows.
-#ifdef TCA_FAKE_TAPS   // timing experiment only: modes 2/3 taps at compile-time offsets (wrong results)
-#define TCA_ROW(base, r) (20 + (r))
-#else
-#define TCA_ROW(base, r) ((base) + (r))
-#endif
 template <typename T>
 __device__ __forceinline__ T tapG(const Params<T> &a, int off, int r, int k)
 {
@@ -333,12 +328,12 @@ __device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T 
         for (int m = 0; m < C::BL + 6; ++m)
 #pragma unroll
             for (int o = 0; o < C::BL; ++o)
-                if (m - o - 3 >= -3 && m - o - 3 <= 3) u[o] = fma(tapG(a, 0, TCA_ROW(r3, o), m - o - 3), v[m], u[o]);
+                if (m - o - 3 >= -3 && m - o - 3 <= 3) u[o] = fma(tapG(a, 0, r3 + o, m - o - 3), v[m], u[o]);
 #pragma unroll
         for (int m = 0; m < C::BL + 4; ++m)
 #pragma unroll
             for (int o = 0; o < C::BL; ++o)
-                if (m - o - 2 >= -2 && m - o - 2 <= 2) rr[o] = fma(tapR(a, 0, TCA_ROW(r3, o), m - o - 2), w[m], rr[o]);
+                if (m - o - 2 >= -2 && m - o - 2 <= 2) rr[o] = fma(tapR(a, 0, r3 + o, m - o - 2), w[m], rr[o]);
 #pragma unroll
         for (int o = 0; o < C::BL; ++o) {
             U3[ob + o * N4] = u[o];
@@ -446,7 +441,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     for (int s = 0; s < PR; ++s)
 #pragma unroll
                         for (int r = 0; r < T2; ++r)
-                            if (s - r - 3 >= -3 && s - r - 3 <= 3) u[r] = fma(tapG(a, 0, TCA_ROW(b2, r), s - r - 3), v[s], u[r]);
+                            if (s - r - 3 >= -3 && s - r - 3 <= 3) u[r] = fma(tapG(a, 0, b2 + r, s - r - 3), v[s], u[r]);
 #pragma unroll
                     for (int r = 0; r < T2; ++r) U2[r * C::WP + c] = u[r];
                     const int ci = c - 3 * N4;
@@ -458,7 +453,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
 #pragma unroll
                             for (int r = 0; r < T2; ++r)
                                 if (s - r - 3 >= -2 && s - r - 3 <= 2)
-                                    u[r] = fma(tapR(a, 0, TCA_ROW(b2, r), s - r - 3), v[s], u[r]);
+                                    u[r] = fma(tapR(a, 0, b2 + r, s - r - 3), v[s], u[r]);
 #pragma unroll
                         for (int r = 0; r < T2; ++r) RA[r * C::WIP + ci] = u[r];
                     }
