@@ -276,8 +276,16 @@ def run_tca(args):
     apply_us = 1e3 * state["apply_ms"] / max(1, state["apply_cnt"])
     apply_bytes = 2 * nloc * esize  # read p, write q (algorithmic, this rank's shard)
     achieved = apply_bytes / (apply_us * 1e-6) / 1e9
+    traffic = None
+    try:   # DRAM bytes per launch from the committed ncu --set full capture (tools/ncu_traffic.py)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(f"{cfg.index}-{dtype}")
+        if tr and world == 1:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None,
+                "frac": achieved / hbm, "traffic": traffic,
                 "kernel": "fused banded operator apply q = M p (band_apply_kernel) inside CG",
                 "bytes_per_launch": apply_bytes, "us_per_launch": apply_us,
                 "launches_timed": state["apply_cnt"], "peak_source": peak_src}

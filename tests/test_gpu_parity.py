@@ -49,7 +49,20 @@ APPLY_CASES = [
     ("ones", (1, 1, 1, 1), (3, 3, 3, 3), "bspline", 0.0),
     ("dense3", (20, 24, 16), (30, 32, 24), "gauss", 1e-3),
     ("dense_cfg1", (48, 48, 48), (64, 64, 64), "gauss", 1e-3),
+    # fused-path shapes (n3*n4 a multiple of 4: TMA row stride for both dtypes):
+    # ragged mode-2/3 tiles, tiles shared by several CTAs (ramp slabs), every n4 class
+    ("fused_ragged15", (13, 11, 36, 15), (26, 22, 72, 30), "bspline", 1e-3),
+    ("fused_many_tiles", (40, 30, 48, 15), (80, 60, 96, 30), "bspline", 1e-2),
+    ("fused_n4_7", (9, 70, 16, 7), (18, 140, 32, 14), "bspline", 0.5),
+    ("fused_n4_8", (7, 9, 33, 8), (14, 18, 66, 16), "bspline", 1e-2),
+    ("fused_n4_4", (11, 6, 21, 4), (22, 12, 42, 8), "bspline", 1e-2),
+    ("fused_n4_32", (6, 20, 20, 32), (9, 30, 30, 48), "bspline", 1e-3),
+    ("fused_d3_n3_4", (14, 13, 12), (28, 26, 24), "bspline", 1e-2),
 ]
+
+# shapes whose banded operator must take the fused one-pass kernel
+FUSED_IDS = {"cfg0", "cfg2", "fused_ragged15", "fused_many_tiles", "fused_n4_7", "fused_n4_8",
+             "fused_n4_4", "fused_n4_32", "fused_d3_n3_4", "n4_32"}
 
 
 def make(case, tca, dtype="f64", seed=1):
@@ -61,6 +74,8 @@ def make(case, tca, dtype="f64", seed=1):
 @pytest.mark.parametrize("case", APPLY_CASES, ids=[c[0] for c in APPLY_CASES])
 def test_apply_f64(case, tca):
     A, L, lam, g, o = make(case, tca)
+    if case[0] in FUSED_IDS:
+        assert g.apply_path == "fused"
     x = synth.random_tensor(case[1], seed=5)
     y = to_host(g.apply(to_dev(x)))
     assert relerr(y, o.apply(x)) <= 1e-12
