@@ -245,16 +245,47 @@ cg_init_kernel(const T *__restrict__ b, T *__restrict__ x, T *__restrict__ r,
     if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// 16-byte vector views (2 doubles or 4 floats) for the streaming CG kernels:
+// each thread moves VW elements per access; a scalar tail covers N % VW.
+template <typename T> struct Vec;
+template <> struct Vec<double> { using V = double2; static constexpr int W = 2; };
+template <> struct Vec<float> { using V = float4; static constexpr int W = 4; };
+
+template <typename V> __device__ __forceinline__ double vdot(const V &a, const V &b);
+template <> __device__ __forceinline__ double vdot<double2>(const double2 &a, const double2 &b)
+{
+    return fma(a.x, b.x, a.y * b.y);
+}
+template <> __device__ __forceinline__ double vdot<float4>(const float4 &a, const float4 &b)
+{
+    return (double)a.x * b.x + (double)a.y * b.y + (double)a.z * b.z + (double)a.w * b.w;
+}
+__device__ __forceinline__ double2 vaxpy(double2 y, double a, double2 x) { return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y)); }
+__device__ __forceinline__ float4 vaxpy(float4 y, float a, float4 x)
+{
+    return make_float4(fmaf(a, x.x, y.x), fmaf(a, x.y, y.y), fmaf(a, x.z, y.z), fmaf(a, x.w, y.w));
+}
+
+template <typename T>
+__device__ __forceinline__ bool aligned16(const T *p) { return ((uintptr_t)p & 15) == 0; }
+
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads)
 dot_partials_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t N,
                     double *part, const int32_t *done)
 {
     if (done && *done) return;
+    using V = typename Vec<T>::V;
+    constexpr int VW = Vec<T>::W;
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
-         i += (int64_t)gridDim.x * blockDim.x)
-        acc += (double)a[i] * (double)b[i];
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    int64_t nv = 0;
+    if (aligned16(a) && aligned16(b)) {
+        nv = N / VW;
+        const V *av = reinterpret_cast<const V *>(a), *bv = reinterpret_cast<const V *>(b);
+        for (int64_t i = tid; i < nv; i += nth) acc += vdot(__ldcs(av + i), __ldcs(bv + i));
+    }
+    for (int64_t i = nv * VW + tid; i < N; i += nth) acc += (double)a[i] * (double)b[i];
     const double s = block_sum(acc);
     if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
@@ -265,28 +296,52 @@ cg_update_xr_kernel(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ 
                     const T *__restrict__ q, int64_t N, const CgScalars *sc, double *part)
 {
     if (sc->done) return;
+    using V = typename Vec<T>::V;
+    constexpr int VW = Vec<T>::W;
     const T alpha = (T)sc->alpha;
     double acc = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        x[i] = x[i] + alpha * p[i];            // C := C + alpha*P*D
-        const T rv = r[i] - alpha * q[i];      // R := R - alpha*Q
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    int64_t nv = 0;
+    if (aligned16(x) && aligned16(r) && aligned16(p) && aligned16(q)) {
+        nv = N / VW;
+        V *xv = reinterpret_cast<V *>(x), *rv = reinterpret_cast<V *>(r);
+        const V *pv = reinterpret_cast<const V *>(p), *qv = reinterpret_cast<const V *>(q);
+        for (int64_t i = tid; i < nv; i += nth) {
+            const V pi = __ldcs(pv + i), qi = __ldcs(qv + i);
+            const V xi = __ldcs(xv + i), ri = __ldcs(rv + i);
+            __stcs(xv + i, vaxpy(xi, alpha, pi));        // C := C + alpha*P*D
+            const V rn = vaxpy(ri, -alpha, qi);          // R := R - alpha*Q
+            __stcs(rv + i, rn);
+            acc += vdot(rn, rn);                         // rho1 := R+*R (partials)
+        }
+    }
+    for (int64_t i = nv * VW + tid; i < N; i += nth) {
+        x[i] = x[i] + alpha * p[i];
+        const T rv = r[i] - alpha * q[i];
         r[i] = rv;
-        acc += (double)rv * (double)rv;        // rho1 := R+*R (partials)
+        acc += (double)rv * (double)rv;
     }
     const double s = block_sum(acc);
     if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
 template <typename T>
-__global__ void cg_update_p_kernel(T *__restrict__ p, const T *__restrict__ r, int64_t N,
-                                   const CgScalars *sc)
+__global__ void __launch_bounds__(kRedThreads)
+cg_update_p_kernel(T *__restrict__ p, const T *__restrict__ r, int64_t N, const CgScalars *sc)
 {
     if (sc->done) return;
+    using V = typename Vec<T>::V;
+    constexpr int VW = Vec<T>::W;
     const T beta = (T)sc->beta;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
-         i += (int64_t)gridDim.x * blockDim.x)
-        p[i] = r[i] + beta * p[i];             // P := R + (rho1/rho)*P
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    int64_t nv = 0;
+    if (aligned16(p) && aligned16(r)) {
+        nv = N / VW;
+        V *pv = reinterpret_cast<V *>(p);
+        const V *rv = reinterpret_cast<const V *>(r);
+        for (int64_t i = tid; i < nv; i += nth) __stcs(pv + i, vaxpy(__ldcs(rv + i), beta, __ldcs(pv + i)));   // P := R + beta*P
+    }
+    for (int64_t i = nv * VW + tid; i < N; i += nth) p[i] = r[i] + beta * p[i];
 }
 
 template <typename T>
