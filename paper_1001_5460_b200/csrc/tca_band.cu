@@ -23,6 +23,8 @@ extern template int t3_for<double>(int);
 extern template int t3_for<float>(int);
 extern template int boxw_for<double>(int);
 extern template int boxw_for<float>(int);
+extern template int minb_for<double>(int);
+extern template int minb_for<float>(int);
 }  // namespace band
 
 namespace {
@@ -86,7 +88,8 @@ void build_params(const tca_operator *op, std::vector<unsigned char> &blob)
     const long long total = tiles2 * p->tiles3 * p->n1;
     // persistent grid: CTA b owns units [total*b/G, total*(b+1)/G) of the
     // (tile-major, slab-minor) unit order
-    const int G = (int)std::min<long long>(std::min(op->num_sms, band::MAXG), total);
+    const int minb = op->dtype == TCA_F64 ? band::minb_for<double>((int)op->n[3]) : band::minb_for<float>((int)op->n[3]);
+    const int G = (int)std::min<long long>(std::min(op->num_sms * minb, band::MAXG), total);
     for (int b = 0; b < G; ++b) {
         const long long u0 = total * b / G, u1 = total * (b + 1) / G;
         const long long tile = u0 / p->n1;

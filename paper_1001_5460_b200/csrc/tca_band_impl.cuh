@@ -42,13 +42,16 @@
 namespace tca {
 namespace band {
 
-constexpr int NTHR = 512;       // 16 warps: 4 per SMSP hide DFMA/LDS/LDCU latency
+// CTA shape per (dtype, n4) (Cfg): NTHR threads, MINB CTAs per SM.  fp32 with
+// n4 <= 16: two 256-thread CTAs per SM (each with its own barriers and TMA
+// pipeline, so one CTA's barrier/memory phases overlap the other's compute);
+// fp64 and n4 = 32: one 512-thread CTA.
 constexpr int T2 = 8;            // mode-2 rows per tile
 constexpr int PR = T2 + 6;       // staged rows (halo 3 + 3)
 constexpr int REC = 7;           // tap record per row: G[r,r..r+3], lambda R[r,r..r+2]
 constexpr int PADR = 6;          // zero rows below each table (row r at record off + r + PADR)
-constexpr int TAP_BYTES = 29 * 1024;
-constexpr int MAXG = 160;        // max persistent CTAs (>= SM count)
+constexpr int TAP_BYTES = 27 * 1024;
+constexpr int MAXG = 320;        // max persistent CTAs (>= 2 x SM count)
 
 // Kernel parameters (constant bank).  The per-CTA schedule is precomputed on
 // the host so that every control value in the kernel is warp-uniform (no
@@ -74,6 +77,11 @@ template <typename T, int N4>
 struct Cfg {
     static constexpr int NSEG = (N4 + 3) / 4;        // ring segments along i4
     static constexpr int E = (N4 + NSEG - 1) / NSEG; // elements per segment (<= 4: ring 24 doubles)
+    // fp64: one 512-thread CTA per SM (T3 = 16: pass-C lanes span 2 mode-2 rows,
+    // conflict-free on the TMA-pitched slab); fp32 (half the shared memory):
+    // two 256-thread CTAs per SM
+    static constexpr int NTHR = (N4 > 16 || sizeof(T) == 8) ? 512 : 256;
+    static constexpr int MINB = NTHR == 512 ? 1 : 2;  // CTAs per SM
     static constexpr int T3 = NTHR / (T2 * NSEG);    // mode-3 columns per tile
     static_assert(NTHR % (T2 * NSEG) == 0, "unsupported n4");
     static constexpr int W = (T3 + 6) * N4;          // halo-extended flat columns
@@ -110,7 +118,8 @@ struct Cfg {
     static constexpr size_t OUTE = al((size_t)T2 * WI);  // TMA store source: dense [T2][WI]
     static constexpr size_t rest_elems = U2E + 3 * WIE + 2 * OUTE;
     static constexpr size_t stage_elems = (size_t)PR * PP;
-    static constexpr int NSTAGE = ((3 * stage_elems + rest_elems) * sizeof(T) + 256 <= 227 * 1024) ? 3 : 2;
+    static constexpr size_t SMEM_CAP = MINB == 1 ? 227 * 1024 : 113 * 1024;   // per CTA
+    static constexpr int NSTAGE = ((3 * stage_elems + rest_elems) * sizeof(T) + 256 <= SMEM_CAP) ? 3 : 2;
     static constexpr size_t smem_bytes = (NSTAGE * stage_elems + rest_elems) * sizeof(T) + 128;
     static_assert(T3 % BL == 0, "T3");
     static_assert(NBLK * WPB <= NTHR / 32, "pass B: one item per warp");
@@ -344,12 +353,12 @@ __device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T 
 
 // ---------------------------------------------------------------- kernel
 template <typename T, int N4>
-__global__ void __launch_bounds__(NTHR, 1)
+__global__ void __launch_bounds__(Cfg<T, N4>::NTHR, Cfg<T, N4>::MINB)
 band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict__ ymp,
                   const __grid_constant__ Params<T> a)
 {
     using C = Cfg<T, N4>;
-    constexpr int W = C::W, WI = C::WI, PP = C::PP, T3 = C::T3, E = C::E;
+    constexpr int W = C::W, WI = C::WI, PP = C::PP, T3 = C::T3, E = C::E, NTHR = C::NTHR;
     if (a.done && *a.done) return;
     if (a.dbg & 16) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -400,6 +409,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         // stage slab js: NB boxes per staged row, issued round-robin by lane 0 of
         // every warp (one warp issuing all of them serialises ~30 UTMALDG)
         auto issue = [&](int js) {
+            if (a.dbg & 256) { ++gi; return; }   // compute-only timing: no loads
             const unsigned st = gi % C::NSTAGE;
             T *dst = Pst + st * C::stage_elems;
             if (tid == 0) mbar_arrive_expect_tx(bar + st, (unsigned)(C::NB * PR * C::BOXW * sizeof(T)));
@@ -425,7 +435,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         for (int j = j0; j < j1; ++j) {
             const bool live = j >= jb && j < je && !(a.dbg & 8);
             const T *P = Pst + (gc % C::NSTAGE) * C::stage_elems + delta;
-            if (live && !(a.dbg & 128)) mbar_wait(bar + gc % C::NSTAGE, (gc / C::NSTAGE) & 1);
+            if (live && !(a.dbg & (128 | 256))) mbar_wait(bar + gc % C::NSTAGE, (gc / C::NSTAGE) & 1);
 
             // ---- pass A: G2 (all halo-extended columns), lambda R2 (interior columns)
             if (live && !(a.dbg & 4)) {
@@ -462,7 +472,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             __syncthreads();   // bar1: U2/RA complete; all threads finished slab j-1
 
             if (pending >= 0) {   // uniform: every thread tracks the same pending slab
-                if (tid == 0 && !(a.dbg & 1)) {
+                if (tid == 0 && !(a.dbg & (1 | 256))) {
                     // staging buffer of output slab `pending` (written in pass C of slab pending+3)
                     tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                     bulk_commit();
@@ -492,7 +502,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         }
         __syncthreads();
         if (pending >= 0) {
-            if (tid == 0 && !(a.dbg & 1)) {
+            if (tid == 0 && !(a.dbg & (1 | 256))) {
                 tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                 bulk_commit();
             }
@@ -528,7 +538,7 @@ tca_status launch_n4(const tca_operator *op, const Params<T> &prm, cudaStream_t 
         attr_set = true;
     }
     count_launch();
-    band_apply_kernel<T, N4><<<(unsigned)op->band_grid, NTHR, C::smem_bytes, s>>>(xm, ym, prm);
+    band_apply_kernel<T, N4><<<(unsigned)op->band_grid, C::NTHR, C::smem_bytes, s>>>(xm, ym, prm);
     TCA_CUDA_TRY(cudaGetLastError());
     return TCA_OK;
 }
@@ -545,6 +555,18 @@ int t3_for(int n4)
 #undef TCA_CASE
     }
     return 0;
+}
+
+template <typename T>
+int minb_for(int n4)
+{
+    switch (n4) {
+#define TCA_CASE(n) \
+    case n: return Cfg<T, n>::MINB;
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return 1;
 }
 
 template <typename T>
