@@ -333,16 +333,15 @@ __device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T 
         for (int m = 0; m < C::BL + 4; ++m) w[m] = pp[m * N4];
 #pragma unroll
         for (int o = 0; o < C::BL; ++o) { u[o] = T(0); rr[o] = RA[ob + o * N4]; }
+        // pull form, one output row at a time: the row's 12 taps can be loaded
+        // (uniform) ahead of its 12 DFMAs; same summation order as the push form
 #pragma unroll
-        for (int m = 0; m < C::BL + 6; ++m)
+        for (int o = 0; o < C::BL; ++o) {
 #pragma unroll
-            for (int o = 0; o < C::BL; ++o)
-                if (m - o - 3 >= -3 && m - o - 3 <= 3) u[o] = fma(tapG(a, 0, r3 + o, m - o - 3), v[m], u[o]);
+            for (int k = -3; k <= 3; ++k) u[o] = fma(tapG(a, 0, r3 + o, k), v[o + 3 + k], u[o]);
 #pragma unroll
-        for (int m = 0; m < C::BL + 4; ++m)
-#pragma unroll
-            for (int o = 0; o < C::BL; ++o)
-                if (m - o - 2 >= -2 && m - o - 2 <= 2) rr[o] = fma(tapR(a, 0, r3 + o, m - o - 2), w[m], rr[o]);
+            for (int k = -2; k <= 2; ++k) rr[o] = fma(tapR(a, 0, r3 + o, k), w[o + 2 + k], rr[o]);
+        }
 #pragma unroll
         for (int o = 0; o < C::BL; ++o) {
             U3[ob + o * N4] = u[o];
@@ -448,10 +447,9 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
 #pragma unroll
                     for (int r = 0; r < T2; ++r) u[r] = T(0);
 #pragma unroll
-                    for (int s = 0; s < PR; ++s)
+                    for (int r = 0; r < T2; ++r)
 #pragma unroll
-                        for (int r = 0; r < T2; ++r)
-                            if (s - r - 3 >= -3 && s - r - 3 <= 3) u[r] = fma(tapG(a, 0, b2 + r, s - r - 3), v[s], u[r]);
+                        for (int k = -3; k <= 3; ++k) u[r] = fma(tapG(a, 0, b2 + r, k), v[r + 3 + k], u[r]);
 #pragma unroll
                     for (int r = 0; r < T2; ++r) U2[r * C::WP + c] = u[r];
                     const int ci = c - 3 * N4;
@@ -459,11 +457,9 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
 #pragma unroll
                         for (int r = 0; r < T2; ++r) u[r] = T(0);
 #pragma unroll
-                        for (int s = 1; s < PR - 1; ++s)
+                        for (int r = 0; r < T2; ++r)
 #pragma unroll
-                            for (int r = 0; r < T2; ++r)
-                                if (s - r - 3 >= -2 && s - r - 3 <= 2)
-                                    u[r] = fma(tapR(a, 0, b2 + r, s - r - 3), v[s], u[r]);
+                            for (int k = -2; k <= 2; ++k) u[r] = fma(tapR(a, 0, b2 + r, k), v[r + 3 + k], u[r]);
 #pragma unroll
                         for (int r = 0; r < T2; ++r) RA[r * C::WIP + ci] = u[r];
                     }
