@@ -144,6 +144,12 @@ struct tca_operator {
     int num_sms = 148;
     int band_grid = 0;                   // persistent grid of the fused banded apply
     int apply_path = 0;                  // 0 = generic multi-pass, 1 = fused banded
+    // CUDA-graph replay of CG chunks
+    cudaStream_t gstream = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    const void *gx = nullptr;
+    int gtiming = -1;
+    cudaEvent_t gfork = nullptr, gjoin = nullptr;
     // timing instrumentation
     int timing = 0;
     std::vector<cudaEvent_t> tev;        // pairs (start, stop)
