@@ -183,6 +183,11 @@ const CUtensorMap *cached_tmap(const tca_operator *op_c, const void *ptr, int ki
         slot.slot = (int)op->tmaps.size();
         op->tmaps.push_back(slot);
     } else {
+        int tries = 0;   // round-robin over the slots not pinned by a captured graph
+        while ((op->tmap_pinned >> op->tmap_next) & 1u) {
+            op->tmap_next = (op->tmap_next + 1) % kTmapSlots;
+            if (++tries > kTmapSlots) { *st = fail(TCA_ERR_INVALID_ARG, "tensor-map slots exhausted"); return nullptr; }
+        }
         slot.slot = op->tmap_next;
         for (auto &e : op->tmaps)
             if (e.slot == slot.slot) e = slot;
@@ -222,9 +227,17 @@ tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_
         p->dbg = e ? atoi(e) : 0;
     }
     TCA_TRY(band::launch_dispatch<T>(op, *p, s, xm, ym));
-    // the slots are in use until this launch completes
-    TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[xs], s));
-    TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[ys], s));
+    // the slots are in use until this launch completes; a launch captured into a
+    // CUDA graph keeps using them for the graph's lifetime: pin them instead
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TCA_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+    tca_operator *o = const_cast<tca_operator *>(op);
+    if (cs != cudaStreamCaptureStatusNone) {
+        o->tmap_pinned |= (1u << xs) | (1u << ys);
+    } else {
+        TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[xs], s));
+        TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[ys], s));
+    }
     return TCA_OK;
 }
 

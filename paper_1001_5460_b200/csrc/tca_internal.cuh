@@ -96,6 +96,7 @@ struct tca_operator {
     uint64_t *tmap_host = nullptr;       // pinned host staging of the descriptors
     cudaEvent_t tmap_ev[tca::kTmapSlots] = {};   // last launch reading each slot
     int tmap_next = 0;
+    uint32_t tmap_pinned = 0;            // bit i: slot i is referenced by a captured CUDA graph
     int order = 0;
     int64_t n[tca::kD] = {1, 1, 1, 1};   // global unknown extents (padded)
     int64_t m[tca::kD] = {1, 1, 1, 1};   // global data extents (padded)
@@ -148,7 +149,6 @@ struct tca_operator {
     cudaStream_t gstream = nullptr;
     cudaGraphExec_t gexec = nullptr;
     const void *gx = nullptr;
-    int gtiming = -1;
     cudaEvent_t gfork = nullptr, gjoin = nullptr;
     // timing instrumentation
     int timing = 0;
