@@ -242,6 +242,14 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
     constexpr int plo = e0 - 2 > 0 ? e0 - 2 : 0;
     constexpr int phi = e1 + 2 < N4 ? e1 + 2 : N4;
     const int i2 = pos / C::T3, i3 = pos % C::T3;
+    // mode-1 taps of input slab j: G1[j+o, j], lambda R1[j+o, j] -- fetched first so
+    // their latency hides behind the window loads and the mode-4 products
+    T g1[7], r1[5];
+    const int b1 = __shfl_sync(0xffffffffu, a.off1 + j, 0);   // uniform table row base (LDCU, UR operands)
+#pragma unroll
+    for (int o = -3; o <= 3; ++o) g1[o + 3] = tapG(a, 0, b1 + o, -o);
+#pragma unroll
+    for (int o = -2; o <= 2; ++o) r1[o + 2] = tapR(a, 0, b1 + o, -o);
     T s[E], q[E], pc[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) { s[e] = T(0); q[e] = T(0); pc[e] = T(0); }
@@ -271,13 +279,6 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
 #pragma unroll
         for (int e = 0; e < NE; ++e) pc[e] = pw[e0 + e - plo];
     }
-    // mode-1 taps of input slab j: G1[j+o, j], lambda R1[j+o, j]
-    T g1[7], r1[5];
-    const int b1 = __shfl_sync(0xffffffffu, a.off1 + j, 0);   // uniform table row base (LDCU, UR operands)
-#pragma unroll
-    for (int o = -3; o <= 3; ++o) g1[o + 3] = tapG(a, 0, b1 + o, -o);
-#pragma unroll
-    for (int o = -2; o <= 2; ++o) r1[o + 2] = tapR(a, 0, b1 + o, -o);
     T *out = OUT + (pos / C::T3) * C::WI + (pos % C::T3) * N4 + e0;
     T ov[E];
     const bool dot = a.pq_part != nullptr && j >= o0 && j < o1;   // input slab j is one of this CTA's
@@ -335,12 +336,25 @@ __device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T 
         for (int o = 0; o < C::BL; ++o) { u[o] = T(0); rr[o] = RA[ob + o * N4]; }
         // pull form, one output row at a time: the row's 12 taps can be loaded
         // (uniform) ahead of its 12 DFMAs; same summation order as the push form
+        // taps of row o+1 are fetched while row o computes (hand pipelining:
+        // the scheduler otherwise issues each LDCU right before its DFMA)
+        T tg[2][7], tr[2][5];
+#pragma unroll
+        for (int k = -3; k <= 3; ++k) tg[0][k + 3] = tapG(a, 0, r3, k);
+#pragma unroll
+        for (int k = -2; k <= 2; ++k) tr[0][k + 2] = tapR(a, 0, r3, k);
 #pragma unroll
         for (int o = 0; o < C::BL; ++o) {
+            if (o + 1 < C::BL) {
 #pragma unroll
-            for (int k = -3; k <= 3; ++k) u[o] = fma(tapG(a, 0, r3 + o, k), v[o + 3 + k], u[o]);
+                for (int k = -3; k <= 3; ++k) tg[(o + 1) & 1][k + 3] = tapG(a, 0, r3 + o + 1, k);
 #pragma unroll
-            for (int k = -2; k <= 2; ++k) rr[o] = fma(tapR(a, 0, r3 + o, k), w[o + 2 + k], rr[o]);
+                for (int k = -2; k <= 2; ++k) tr[(o + 1) & 1][k + 2] = tapR(a, 0, r3 + o + 1, k);
+            }
+#pragma unroll
+            for (int k = -3; k <= 3; ++k) u[o] = fma(tg[o & 1][k + 3], v[o + 3 + k], u[o]);
+#pragma unroll
+            for (int k = -2; k <= 2; ++k) rr[o] = fma(tr[o & 1][k + 2], w[o + 2 + k], rr[o]);
         }
 #pragma unroll
         for (int o = 0; o < C::BL; ++o) {
@@ -446,20 +460,38 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     T u[T2];
 #pragma unroll
                     for (int r = 0; r < T2; ++r) u[r] = T(0);
+                    {   // taps of row r+1 fetched while row r computes (see pass B)
+                        T tg[2][7];
 #pragma unroll
-                    for (int r = 0; r < T2; ++r)
+                        for (int k = -3; k <= 3; ++k) tg[0][k + 3] = tapG(a, 0, b2, k);
 #pragma unroll
-                        for (int k = -3; k <= 3; ++k) u[r] = fma(tapG(a, 0, b2 + r, k), v[r + 3 + k], u[r]);
+                        for (int r = 0; r < T2; ++r) {
+                            if (r + 1 < T2) {
+#pragma unroll
+                                for (int k = -3; k <= 3; ++k) tg[(r + 1) & 1][k + 3] = tapG(a, 0, b2 + r + 1, k);
+                            }
+#pragma unroll
+                            for (int k = -3; k <= 3; ++k) u[r] = fma(tg[r & 1][k + 3], v[r + 3 + k], u[r]);
+                        }
+                    }
 #pragma unroll
                     for (int r = 0; r < T2; ++r) U2[r * C::WP + c] = u[r];
                     const int ci = c - 3 * N4;
                     if (ci >= 0 && ci < WI) {
 #pragma unroll
                         for (int r = 0; r < T2; ++r) u[r] = T(0);
+                        T tr[2][5];
 #pragma unroll
-                        for (int r = 0; r < T2; ++r)
+                        for (int k = -2; k <= 2; ++k) tr[0][k + 2] = tapR(a, 0, b2, k);
 #pragma unroll
-                            for (int k = -2; k <= 2; ++k) u[r] = fma(tapR(a, 0, b2 + r, k), v[r + 3 + k], u[r]);
+                        for (int r = 0; r < T2; ++r) {
+                            if (r + 1 < T2) {
+#pragma unroll
+                                for (int k = -2; k <= 2; ++k) tr[(r + 1) & 1][k + 2] = tapR(a, 0, b2 + r + 1, k);
+                            }
+#pragma unroll
+                            for (int k = -2; k <= 2; ++k) u[r] = fma(tr[r & 1][k + 2], v[r + 3 + k], u[r]);
+                        }
 #pragma unroll
                         for (int r = 0; r < T2; ++r) RA[r * C::WIP + ci] = u[r];
                     }
