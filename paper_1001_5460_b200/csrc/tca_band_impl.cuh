@@ -104,8 +104,12 @@ struct Cfg {
     static constexpr int PP = NB * BOXW;             // staged row pitch
     static constexpr int BL = 4;                     // pass-B outputs per item
     static constexpr int NBLK = T3 / BL;
-    static constexpr int LPB = T2 * N4;              // pass-B lanes per block
-    static constexpr int WPB = (LPB + 31) / 32;
+    // pass B: each warp covers whole mode-2 rows of the block (RPW rows of N4
+    // lanes) so its 32 lanes never put three rows on one bank pair of the
+    // 128-B-aligned (TMA) slab rows
+    static constexpr int RPW = (32 / N4 < T2) ? (32 / N4 > 0 ? 32 / N4 : 1) : T2;
+    static constexpr int WPB = (T2 + RPW - 1) / RPW;  // warps per block
+    static_assert(N4 <= 32, "pass B lane map");
     static constexpr size_t al(size_t e) { return (e * sizeof(T) + 127) / 128 * 128 / sizeof(T); }
     // row pitches of the intermediate tiles: congruent to N4 modulo one bank
     // sweep (128 B) so that pass-B lanes (i2, i4) of consecutive i2 rows hit
@@ -320,9 +324,9 @@ __device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T 
         }
         constexpr int h0b = B * C::BL;
         const int r3 = __shfl_sync(0xffffffffu, a.off3 + a3 + h0b, 0);   // uniform table row base (all lanes)
-        const int l = (warp % C::WPB) * 32 + lane;
-        if (l >= C::LPB) return;
-        const int i2 = l / N4, i4 = l % N4;
+        if (lane >= C::RPW * N4) return;
+        const int i2 = (warp % C::WPB) * C::RPW + lane / N4, i4 = lane % N4;
+        if (i2 >= T2) return;
         constexpr int h0 = B * C::BL;
         const T *u2 = U2 + i2 * C::WP + h0 * N4 + i4;
         const T *pp = P + (i2 + 3) * C::PP + (h0 + 1) * N4 + i4;
