@@ -88,7 +88,13 @@ struct Cfg {
     static constexpr int WI = T3 * N4;               // interior flat columns
     static constexpr int VEC = 16 / (int)sizeof(T);  // TMA coordinate granularity (16 B)
     static constexpr int UNIT = 128 / (int)sizeof(T);
-    static constexpr int NEED = W + VEC - 1;
+    // fp32 two-CTA tiles: staged row r is shifted right by SH(r) = 8 pi(r mod 4)
+    // elements (pi = 0,1,3,2) inside its 128-B-aligned TMA row, so the 4 mode-2
+    // rows one pass-C warp reads, and the 2 rows one pass-B warp reads, land on
+    // distinct banks (the TMA rows themselves must stay 128-B aligned)
+    static constexpr bool SHIFTED = sizeof(T) == 4 && (N4 > 16 ? 512 : 256) == 256;
+    static constexpr int SHMAX = SHIFTED ? 24 : 0;
+    static constexpr int NEED = W + VEC - 1 + SHMAX;
     static constexpr int boxw_for_nb(int nb) { return ((NEED + nb - 1) / nb + UNIT - 1) / UNIT * UNIT; }
     static constexpr int pick_nb()
     {
@@ -181,6 +187,13 @@ template <int N>
 __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
+// in-row shift of staged slab row r (elements), see Cfg::SHIFTED
+template <typename T, int N4>
+__host__ __device__ constexpr int row_shift(int r)
+{
+    return Cfg<T, N4>::SHIFTED ? 8 * ((r & 3) == 2 ? 3 : (r & 3) == 3 ? 2 : (r & 3)) : 0;
+}
+
 // ---------------------------------------------------------------- taps
 // rec(r) = taps + (off + r + PADR) * REC; G(r, k) = G[r, r+k], R(r, k) = lambda R[r, r+k]
 // (symmetric: G[r, r-k] = G[r-k, r]).  Tables are zero outside the domain rows.
@@ -260,7 +273,7 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
     if (live) {
         const T *u3 = U3 + i2 * C::WIP + i3 * N4;
         const T *rb = RB + i2 * C::WIP + i3 * N4;
-        const T *pp = P + (i2 + 3) * C::PP + (i3 + 3) * N4;
+        const T *pp = P + (i2 + 3) * C::PP + row_shift<T, N4>(i2 + 3) + (i3 + 3) * N4;
         T uw[uhi - ulo], pw[phi - plo];
 #pragma unroll
         for (int k = ulo; k < uhi; ++k) uw[k - ulo] = u3[k];
@@ -329,7 +342,7 @@ __device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T 
         if (i2 >= T2) return;
         constexpr int h0 = B * C::BL;
         const T *u2 = U2 + i2 * C::WP + h0 * N4 + i4;
-        const T *pp = P + (i2 + 3) * C::PP + (h0 + 1) * N4 + i4;
+        const T *pp = P + (i2 + 3) * C::PP + row_shift<T, N4>(i2 + 3) + (h0 + 1) * N4 + i4;
         const int ob = i2 * C::WIP + h0 * N4 + i4;
         T v[C::BL + 6], w[C::BL + 4], u[C::BL], rr[C::BL];
 #pragma unroll
@@ -436,7 +449,8 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     const int b = warp + k * (NTHR / 32);
                     if (b < C::NB * PR) {
                         const int r = b / C::NB, h = b % C::NB;
-                        tma_load_3d(dst + r * PP + h * C::BOXW, xmp, bar + st, ca - delta + h * C::BOXW, a2 - 3 + r,
+                        tma_load_3d(dst + r * PP + h * C::BOXW, xmp, bar + st,
+                                    ca - delta - row_shift<T, N4>(r) + h * C::BOXW, a2 - 3 + r,
                                     js + a.xoff);
                     }
                 }
@@ -460,7 +474,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                 for (int c = tid; c < W; c += NTHR) {
                     T v[PR];
 #pragma unroll
-                    for (int s = 0; s < PR; ++s) v[s] = P[s * PP + c];
+                    for (int s = 0; s < PR; ++s) v[s] = P[s * PP + row_shift<T, N4>(s) + c];
                     T u[T2];
 #pragma unroll
                     for (int r = 0; r < T2; ++r) u[r] = T(0);
