@@ -76,7 +76,8 @@ typedef struct tca_operator tca_operator;
  *                of one process (test transport for fewer GPUs than shards:
  *                host-synchronised copies; every rank must call the same
  *                entry points concurrently from its own thread).
- * Sharded operators need the fused banded path (all modes banded).
+ * Sharded operators need the fused banded path (all modes banded).  nranks = 1
+ * with a transport is allowed (the whole domain, empty halos).
  */
 typedef struct {
     int rank;

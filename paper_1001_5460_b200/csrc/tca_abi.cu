@@ -595,7 +595,9 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
         if (vol >= 4294967295.0) return fail(TCA_ERR_SHAPE, "problem too large: prod max(n_d, m_d) must be < 2^32");
     }
     int64_t layout[4] = {0, n[0], 0, m[0]};   // own_lo, own_hi, data_lo, data_hi
-    const bool sharded = dist && dist->nranks > 1;
+    // sharded = a transport is given (nranks >= 1; one rank is the whole domain
+    // with empty halos -- the single-GPU case of the distributed code path)
+    const bool sharded = dist && (dist->nranks > 1 || dist->nccl_comm || dist->local_group);
     if (dist) {
         if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks)
             return fail(TCA_ERR_INVALID_ARG, "dist: rank must be in [0, nranks)");

@@ -226,7 +226,7 @@ class LocalTransport final : public Transport {
 
 Transport *make_transport(const tca_dist *d)
 {
-    if (!d || d->nranks <= 1) return nullptr;
+    if (!d || (!d->nccl_comm && !d->local_group)) return nullptr;
     if (d->local_group) {
         auto *g = reinterpret_cast<LocalGroup *>(d->local_group);
         return new LocalTransport(g, d->rank);

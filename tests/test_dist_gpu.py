@@ -120,3 +120,30 @@ def test_sharded_forward_model_matches_single_gpu(tca):
     for dlo, dhi, yd in out:
         # position-keyed generator; mode-product order may differ from the global chain
         assert rel(yd, y_all[dlo:dhi]) <= 1e-14
+
+
+def test_nccl_transport_single_rank_cg_matches_oracle(tca):
+    """The NCCL transport (dlopen'd libnccl, unique id, communicator, grouped
+    send/recv and all-reduce on the CG stream) on a one-rank communicator: the
+    whole domain with empty halos.  Only one GPU is available to the tests, so
+    this exercises the NCCL code path; multi-rank halos are covered by the
+    local-transport tests above."""
+    n, m, lam = (32, 32, 32, 16), (64, 64, 64, 32), 1e-2
+    A, L = synth.mode_matrices(n, m, basis="bspline", seed=1)
+    o = oracle.Operator(A, L, lam)
+    uid = tca.NcclComm.unique_id()
+    comm = tca.NcclComm(1, uid, 0)
+    try:
+        op = tca.Operator(A, L, lam, dist=comm.dist())
+        assert op.apply_path == "fused"
+        y = synth.data(A, n, m, seed=1)
+        b = op.rhs(torch.from_numpy(y).cuda())
+        xs, rep = op.cg_solve(b, rtol=0.0, max_iters=30)
+        x_ref, k, st, _ = o.cg(o.rhs(y), rtol=0.0, max_iters=30)
+        assert rel(xs.cpu().numpy(), x_ref) <= 1e-8
+        xin = synth.random_tensor(n, seed=5)
+        q = op.apply(torch.from_numpy(xin).cuda()).cpu().numpy()
+        assert rel(q, o.apply(xin)) <= 1e-12
+        op.close()
+    finally:
+        comm.close()
