@@ -226,14 +226,17 @@ tca_status tca_forward_model(const tca_operator *op, const void *x, void *ydata,
 /*
  * Timing instrumentation (measurement only; off by default).  When enabled,
  * tca_cg_solve and tca_apply record a CUDA event pair on `stream` around
- * every operator-apply launch; tca_operator_get_timing returns the summed
- * device time (ms) and the number of timed applies since the last reset.
+ * every operator-apply launch (inside CG's graph chunks: external event
+ * nodes of the captured graph, two alternating instances so that one is read
+ * while the other runs); tca_operator_get_timing returns the summed device
+ * time (ms) and the number of timed applies since the last reset.
  */
 tca_status tca_operator_set_timing(tca_operator *op, int enable);
 tca_status tca_operator_get_timing(tca_operator *op, double *apply_ms,
                                    int64_t *apply_count, int reset);
 
-/* Number of CUDA kernel launches the library has issued so far (process-wide). */
+/* Number of CUDA kernel launches the library has issued so far (process-wide;
+   the kernels of a replayed CG graph chunk count at every replay). */
 int64_t tca_kernel_launches(void);
 
 const char *tca_status_string(tca_status s);

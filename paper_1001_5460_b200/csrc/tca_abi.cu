@@ -326,10 +326,23 @@ static tca_status forward_t(const tca_operator *op, const T *x, T *y, double sig
 }
 
 // Timed apply: an event pair around the launch when instrumentation is on.
+// Inside a CUDA-graph capture the pair is recorded as external event nodes of
+// the graph (real timestamps at every replay), harvested per graph instance.
 static tca_status timed_apply(tca_operator *op, const void *x, void *y, const int32_t *done,
                               cudaStream_t s, double *pq_part = nullptr)
 {
     if (!op->timing) return apply_dispatch(op, x, y, done, s, pq_part);
+    if (op->cap_ev) {
+        cudaEvent_t a, b;
+        TCA_CUDA_TRY(cudaEventCreate(&a));
+        op->cap_ev->push_back(a);
+        TCA_CUDA_TRY(cudaEventCreate(&b));
+        op->cap_ev->push_back(b);
+        TCA_CUDA_TRY(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
+        TCA_TRY(apply_dispatch(op, x, y, done, s, pq_part));
+        TCA_CUDA_TRY(cudaEventRecordWithFlags(b, s, cudaEventRecordExternal));
+        return TCA_OK;
+    }
     if (op->tev_used + 2 > op->tev.size()) {
         for (int i = 0; i < 64; ++i) {
             cudaEvent_t e;
@@ -345,16 +358,31 @@ static tca_status timed_apply(tca_operator *op, const void *x, void *y, const in
     return TCA_OK;
 }
 
-// Fold the recorded event pairs into apply_ms / apply_count (after a sync).
-static tca_status harvest_timing(tca_operator *op)
+static tca_status harvest_pairs(tca_operator *op, const cudaEvent_t *ev, size_t n)
 {
-    for (size_t i = 0; i + 1 < op->tev_used; i += 2) {
+    for (size_t i = 0; i + 1 < n; i += 2) {
         float ms = 0.f;
-        TCA_CUDA_TRY(cudaEventSynchronize(op->tev[i + 1]));
-        TCA_CUDA_TRY(cudaEventElapsedTime(&ms, op->tev[i], op->tev[i + 1]));
+        TCA_CUDA_TRY(cudaEventSynchronize(ev[i + 1]));
+        TCA_CUDA_TRY(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
         op->apply_ms += ms;
         op->apply_count += 1;
     }
+    return TCA_OK;
+}
+
+// Event pairs of the last replay of graph instance g.
+static tca_status harvest_graph(tca_operator *op, int g)
+{
+    if (!op->gpend[g]) return TCA_OK;
+    op->gpend[g] = false;
+    return harvest_pairs(op, op->gev[g].data(), op->gev[g].size());
+}
+
+// Fold the recorded event pairs into apply_ms / apply_count (after a sync).
+static tca_status harvest_timing(tca_operator *op)
+{
+    for (int g = 0; g < 2; ++g) TCA_TRY(harvest_graph(op, g));
+    TCA_TRY(harvest_pairs(op, op->tev.data(), op->tev_used));
     op->tev_used = 0;
     return TCA_OK;
 }
@@ -407,6 +435,43 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
 // (device `done` flag), so the returned x is exactly x_k.
 constexpr int kGraphChunk = 32;
 
+static void destroy_graphs(tca_operator *op)
+{
+    for (int g = 0; g < 2; ++g) {
+        if (op->gexec[g]) cudaGraphExecDestroy(op->gexec[g]);
+        op->gexec[g] = nullptr;
+        op->gpend[g] = false;
+        for (cudaEvent_t e : op->gev[g]) cudaEventDestroy(e);
+        op->gev[g].clear();
+    }
+    op->gx = nullptr;
+}
+
+template <typename T>
+static tca_status capture_chunk(tca_operator *op, T *x, int g)
+{
+    cudaGraph_t graph = nullptr;
+    op->cap_ev = op->timing ? &op->gev[g] : nullptr;
+    TCA_CUDA_TRY(cudaStreamBeginCapture(op->gstream, cudaStreamCaptureModeThreadLocal));
+    tca_status st = TCA_OK;
+    const int64_t k0 = g_launches.load();
+    for (int i = 0; i < kGraphChunk && st == TCA_OK; ++i) st = cg_iteration<T>(op, x, op->gstream);
+    cudaError_t e = cudaStreamEndCapture(op->gstream, &graph);
+    op->cap_ev = nullptr;
+    // captured launches run at each replay, not now (single-threaded per operator)
+    op->gkernels[g] = g_launches.load() - k0;
+    count_launch(-op->gkernels[g]);
+    if (st != TCA_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    TCA_CUDA_TRY(e);
+    e = cudaGraphInstantiate(&op->gexec[g], graph, 0);
+    cudaGraphDestroy(graph);
+    TCA_CUDA_TRY(e);
+    return TCA_OK;
+}
+
 template <typename T>
 static tca_status cg_graph_loop(tca_operator *op, T *x, double rtol, int32_t max_iters, cudaStream_t s)
 {
@@ -417,28 +482,24 @@ static tca_status cg_graph_loop(tca_operator *op, T *x, double rtol, int32_t max
         TCA_CUDA_TRY(cudaEventCreateWithFlags(&op->gfork, cudaEventDisableTiming));
         TCA_CUDA_TRY(cudaEventCreateWithFlags(&op->gjoin, cudaEventDisableTiming));
     }
-    if (!op->gexec || op->gx != (const void *)x) {
-        if (op->gexec) cudaGraphExecDestroy(op->gexec);
-        op->gexec = nullptr;
-        cudaGraph_t g = nullptr;
-        TCA_CUDA_TRY(cudaStreamBeginCapture(op->gstream, cudaStreamCaptureModeThreadLocal));
-        tca_status st = TCA_OK;
-        for (int i = 0; i < kGraphChunk && st == TCA_OK; ++i) st = cg_iteration<T>(op, x, op->gstream);
-        cudaError_t e = cudaStreamEndCapture(op->gstream, &g);
-        if (st != TCA_OK) {
-            if (g) cudaGraphDestroy(g);
-            return st;
-        }
-        TCA_CUDA_TRY(e);
-        e = cudaGraphInstantiate(&op->gexec, g, 0);
-        cudaGraphDestroy(g);
-        TCA_CUDA_TRY(e);
+    // with timing, two instances alternate: instance g's events are read while
+    // the other instance is queued behind it, so the GPU never drains
+    const int ng = op->timing ? 2 : 1;
+    if (!op->gexec[0] || op->gx != (const void *)x || op->gtimed != op->timing) {
+        TCA_TRY(harvest_timing(op));
+        destroy_graphs(op);
+        for (int g = 0; g < ng; ++g) TCA_TRY(capture_chunk<T>(op, x, g));
         op->gx = x;
+        op->gtimed = op->timing;
     }
     TCA_CUDA_TRY(cudaEventRecord(op->gfork, s));
     TCA_CUDA_TRY(cudaStreamWaitEvent(op->gstream, op->gfork, 0));
+    int g = 0;
     while (done_iters + kGraphChunk <= max_iters) {
-        TCA_CUDA_TRY(cudaGraphLaunch(op->gexec, op->gstream));
+        TCA_TRY(harvest_graph(op, g));   // its previous replay (the other instance is queued)
+        TCA_CUDA_TRY(cudaGraphLaunch(op->gexec[g], op->gstream));
+        count_launch(op->gkernels[g]);
+        op->gpend[g] = op->timing != 0;
         done_iters += kGraphChunk;
         if (rtol > 0.0) {   // tolerance stop: check the device flag once per chunk
             TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost,
@@ -446,6 +507,7 @@ static tca_status cg_graph_loop(tca_operator *op, T *x, double rtol, int32_t max
             TCA_CUDA_TRY(cudaStreamSynchronize(op->gstream));
             if (op->sc_host->done) break;
         }
+        g = (g + 1) % ng;
     }
     if (!op->sc_host->done || rtol <= 0.0)
         for (; done_iters < max_iters; ++done_iters) TCA_TRY(cg_iteration<T>(op, x, op->gstream));
@@ -468,9 +530,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     TCA_TRY(cg_reduce(op, 0, op->part, kRedBlocks, s));
     TCA_TRY(halo_p(op, s));
     static const bool no_graph = getenv("TCA_NO_GRAPH") != nullptr;   // measurement switch
-    // graphs are not used with the per-apply timing instrumentation (its event
-    // pairs must be real records on the launching stream)
-    if (!op->transport && !no_graph && !op->timing && max_iters > 1) {
+    if (!op->transport && !no_graph && max_iters > 1) {
         TCA_TRY(cg_graph_loop<T>(op, x, rtol, max_iters, s));
     } else if (rtol <= 0.0) {
         for (int k = 0; k < max_iters; ++k) TCA_TRY(cg_iteration<T>(op, x, s));
@@ -553,7 +613,7 @@ void tca_operator_destroy(tca_operator *op)
         free_band(op->Af[d]);
     }
     delete op->transport;
-    if (op->gexec) cudaGraphExecDestroy(op->gexec);
+    destroy_graphs(op);
     if (op->gstream) cudaStreamDestroy(op->gstream);
     if (op->gfork) cudaEventDestroy(op->gfork);
     if (op->gjoin) cudaEventDestroy(op->gjoin);

@@ -23,6 +23,10 @@ extern template int t3_for<double>(int);
 extern template int t3_for<float>(int);
 extern template int boxw_for<double>(int);
 extern template int boxw_for<float>(int);
+extern template int pp_for<double>(int);
+extern template int pp_for<float>(int);
+extern template int onebox_for<double>(int);
+extern template int onebox_for<float>(int);
 extern template int minb_for<double>(int);
 extern template int minb_for<float>(int);
 }  // namespace band
@@ -47,6 +51,18 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 int t3_of(const tca_operator *op)
 {
     return op->dtype == TCA_F64 ? band::t3_for<double>((int)op->n[3]) : band::t3_for<float>((int)op->n[3]);
+}
+
+// One TMA box per staged slab (Cfg::ONEBOX): the input is viewed as
+// (UNIT, n3 n4 / UNIT, n2, slabs) with 128-B inner chunks, which needs n3 n4 to
+// be a multiple of UNIT; otherwise each staged row is NB boxes of a 3-D view.
+bool onebox_of(const tca_operator *op)
+{
+    const int n4 = (int)op->n[3];
+    const int unit = 128 / (int)op->esize;
+    const int ob = op->dtype == TCA_F64 ? band::onebox_for<double>(n4) : band::onebox_for<float>(n4);
+    const int pp = op->dtype == TCA_F64 ? band::pp_for<double>(n4) : band::pp_for<float>(n4);
+    return ob && (op->n[2] * op->n[3]) % unit == 0 && pp / unit <= 256;
 }
 
 // Rows of the four tap tables (mode 4 first so its offsets are compile-time).
@@ -81,6 +97,7 @@ void build_params(const tca_operator *op, std::vector<unsigned char> &blob)
     const TableLayout L = table_layout(op);
     const int t3 = t3_of(op);
     p->n1 = (int)op->nloc1;
+    p->onebox = onebox_of(op) ? 1 : 0;
     p->n2 = (int)op->n[1];
     p->n3 = (int)op->n[2];
     p->tiles3 = (p->n3 + t3 - 1) / t3;
@@ -147,7 +164,22 @@ tca_status make_tmap(const tca_operator *op, const void *ptr, int kind, CUtensor
         box[1] = band::T2;
         box[2] = 1;
     }
-    cuuint32_t es[3] = {1, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (kind == 0 && onebox_of(op)) {   // whole staged slab (PR rows x PP elements) as one box
+        const cuuint64_t unit = 128 / op->esize;
+        const cuuint64_t F = (cuuint64_t)(op->n[2] * op->n[3]);
+        const int pp = op->dtype == TCA_F64 ? band::pp_for<double>(n4) : band::pp_for<float>(n4);
+        cuuint64_t d4[4] = {unit, F / unit, (cuuint64_t)op->n[1], (cuuint64_t)slabs};
+        cuuint64_t s4[3] = {unit * op->esize, F * op->esize, F * (cuuint64_t)op->n[1] * op->esize};
+        cuuint32_t b4[4] = {(cuuint32_t)unit, (cuuint32_t)(pp / unit), (cuuint32_t)band::PR, 1};
+        CUresult r = encode(m, op->dtype == TCA_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                            4, const_cast<void *>(ptr), d4, s4, b4, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return fail(TCA_ERR_CUDA, "cuTensorMapEncodeTiled (4-D) failed (" + std::to_string((int)r) + ")");
+        return TCA_OK;
+    }
     CUresult r = encode(m, op->dtype == TCA_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                         3, const_cast<void *>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

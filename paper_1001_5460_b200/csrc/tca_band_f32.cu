@@ -8,6 +8,8 @@ template tca_status launch_dispatch<float>(const tca_operator *, const Params<fl
                                          const CUtensorMap *);
 template int t3_for<float>(int);
 template int boxw_for<float>(int);
+template int pp_for<float>(int);
+template int onebox_for<float>(int);
 template int minb_for<float>(int);
 }  // namespace band
 }  // namespace tca

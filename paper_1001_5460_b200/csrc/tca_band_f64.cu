@@ -8,6 +8,8 @@ template tca_status launch_dispatch<double>(const tca_operator *, const Params<d
                                          const CUtensorMap *);
 template int t3_for<double>(int);
 template int boxw_for<double>(int);
+template int pp_for<double>(int);
+template int onebox_for<double>(int);
 template int minb_for<double>(int);
 }  // namespace band
 }  // namespace tca

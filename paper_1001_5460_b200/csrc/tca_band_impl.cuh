@@ -67,6 +67,7 @@ struct Params {
     int xoff, nin;            // input slab j lives at slab j + xoff of an input of nin slabs (ghosts)
     int off3, off2, off1;     // record offsets (rows) of the mode-3/2/1 tables; mode 4 at 0
     int dbg;                  // phase switches for bisecting (TCA_BAND_DEBUG; 0 in production)
+    int onebox;               // 1: a slab is ONE 4-D TMA box (Cfg::ONEBOX and n3 n4 % UNIT == 0)
     short2 s_tile[MAXG];   // CTA b starts at tile (x = mode-2 tile, y = mode-3 tile) ...
     int s_o0[MAXG];        // ... at output slab s_o0 ...
     int s_cnt[MAXG];       // ... and processes s_cnt (tile, slab) units
@@ -94,7 +95,11 @@ struct Cfg {
     // distinct banks (the TMA rows themselves must stay 128-B aligned)
     static constexpr bool SHIFTED = sizeof(T) == 4 && (N4 > 16 ? 512 : 256) == 256;
     static constexpr int SHMAX = SHIFTED ? 24 : 0;
-    static constexpr int NEED = W + VEC - 1 + SHMAX;
+    // ONEBOX: the input map is 4-D (UNIT, n3 n4 / UNIT, n2, n1) and a whole staged
+    // slab (PR rows of PP elements) is one TMA box: 128-B chunks, start aligned to
+    // UNIT elements (host picks it when n3 n4 % UNIT == 0; otherwise NB boxes per row)
+    static constexpr bool ONEBOX = !SHIFTED;
+    static constexpr int NEED = W + (ONEBOX ? UNIT : VEC) - 1 + SHMAX;
     static constexpr int boxw_for_nb(int nb) { return ((NEED + nb - 1) / nb + UNIT - 1) / UNIT * UNIT; }
     static constexpr int pick_nb()
     {
@@ -170,6 +175,16 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
             smem_u32(dst)),
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2,
+                                            int c3)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
 }
 
@@ -427,7 +442,11 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         const int a3 = __shfl_sync(0xffffffffu, t3i * T3, 0);
         const int b2 = __shfl_sync(0xffffffffu, a.off2 + t2i * T2, 0);   // uniform mode-2 table row base
         const int ca = (a3 - 3) * N4;                              // flat column of staged column 0
-        const int delta = ((ca % C::VEC) + C::VEC) % C::VEC;       // boxes start 16-B aligned
+        // boxes start 16-B aligned (per-row boxes) or UNIT-aligned (one box per slab)
+        const bool onebox = C::ONEBOX && a.onebox;
+        const int cal = onebox ? C::UNIT : C::VEC;
+        const int delta = ((ca % cal) + cal) % cal;
+        const int cchunk = (ca - delta) / C::UNIT;                 // onebox: first 128-B chunk
         const int j0 = o0 - 3, j1 = o1 + 3;
         const int jb = j0 > -a.xoff ? j0 : -a.xoff, je = j1 < a.nin - a.xoff ? j1 : a.nin - a.xoff;
 #pragma unroll
@@ -442,6 +461,14 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             if (a.dbg & 256) { ++gi; return; }   // compute-only timing: no loads
             const unsigned st = gi % C::NSTAGE;
             T *dst = Pst + st * C::stage_elems;
+            if (onebox) {
+                if (tid == 0) {
+                    mbar_arrive_expect_tx(bar + st, (unsigned)(PR * PP * sizeof(T)));
+                    tma_load_4d(dst, xmp, bar + st, 0, cchunk, a2 - 3, js + a.xoff);
+                }
+                ++gi;
+                return;
+            }
             if (tid == 0) mbar_arrive_expect_tx(bar + st, (unsigned)(C::NB * PR * C::BOXW * sizeof(T)));
             if (lane == 0) {
 #pragma unroll
@@ -597,6 +624,30 @@ int t3_for(int n4)
     switch (n4) {
 #define TCA_CASE(n) \
     case n: return Cfg<T, n>::T3;
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return 0;
+}
+
+template <typename T>
+int pp_for(int n4)
+{
+    switch (n4) {
+#define TCA_CASE(n) \
+    case n: return Cfg<T, n>::PP;
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return 0;
+}
+
+template <typename T>
+int onebox_for(int n4)
+{
+    switch (n4) {
+#define TCA_CASE(n) \
+    case n: return Cfg<T, n>::ONEBOX ? 1 : 0;
         TCA_BAND_N4_LIST(TCA_CASE)
 #undef TCA_CASE
     }

@@ -146,9 +146,16 @@ struct tca_operator {
     int band_grid = 0;                   // persistent grid of the fused banded apply
     int apply_path = 0;                  // 0 = generic multi-pass, 1 = fused banded
     // CUDA-graph replay of CG chunks
+    // (two instances when timing: each carries its own captured event pairs, so
+    // one can be harvested while the other runs)
     cudaStream_t gstream = nullptr;
-    cudaGraphExec_t gexec = nullptr;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     const void *gx = nullptr;
+    int gtimed = 0;                      // the instances were captured with timing events
+    int64_t gkernels[2] = {0, 0};        // kernel launches captured in instance g (added per replay)
+    bool gpend[2] = {false, false};      // instance g has launched and its events are unharvested
+    std::vector<cudaEvent_t> gev[2];     // captured (external) event pairs of instance g
+    std::vector<cudaEvent_t> *cap_ev = nullptr;   // event list being captured into
     cudaEvent_t gfork = nullptr, gjoin = nullptr;
     // timing instrumentation
     int timing = 0;
