@@ -421,9 +421,9 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
         launch_dot_partials<T>(p, q, op->N, op->part, done, s);      // P+*Q
         TCA_TRY(cg_reduce(op, 1, op->part, kRedBlocks, s));          // alpha
     }
-    launch_cg_update_xr<T>(x, r, p, q, op->N, op->sc, op->part, s);  // C, R, R+*R
+    launch_cg_update_r<T>(r, q, op->N, op->sc, op->part, s);         // R := R - alpha*Q, R+*R
     TCA_TRY(cg_reduce(op, 2, op->part, kRedBlocks, s));              // rho1, stop, beta
-    launch_cg_update_p<T>(p, r, op->N, op->sc, s);                   // P := R + beta*P
+    launch_cg_update_xp<T>(x, p, r, op->N, op->sc, s);               // C := C + alpha*P*D, P := R + beta*P
     return halo_p(op, s);                                             // ghost slabs of P
 }
 

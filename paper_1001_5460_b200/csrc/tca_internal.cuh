@@ -61,7 +61,7 @@ struct CgScalars {
     int32_t done;    // 1: later kernels of the solve are no-ops
     int32_t status;  // tca_status
     int32_t converged;
-    int32_t pad;
+    int32_t xupd;    // 1: this iteration's alpha is valid (x := x + alpha p pending)
     double red[3];   // reduced dot products (stage sum -> all-reduce -> stage apply)
 };
 
@@ -191,11 +191,9 @@ template <typename T>
 void launch_dot_partials(const T *a, const T *b, int64_t N, double *part,
                          const int32_t *done, cudaStream_t s);
 template <typename T>
-void launch_cg_update_xr(T *x, T *r, const T *p, const T *q, int64_t N,
-                         const CgScalars *sc, double *part, cudaStream_t s);
+void launch_cg_update_r(T *r, const T *q, int64_t N, const CgScalars *sc, double *part, cudaStream_t s);
 template <typename T>
-void launch_cg_update_p(T *p, const T *r, int64_t N, const CgScalars *sc,
-                        cudaStream_t s);
+void launch_cg_update_xp(T *x, T *p, const T *r, int64_t N, const CgScalars *sc, cudaStream_t s);
 
 // finalisers (one block): 0 = init rho, 1 = pq -> alpha, 2 = rr -> beta/stop
 // stage: 0 = sum the partials and apply (single GPU), 1 = sum into sc->red[which]

@@ -290,10 +290,14 @@ dot_partials_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t N,
     if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// The CG updates in two streaming passes, 8 words per unknown (Fig. 2 as
+// written: 9):  R := R - alpha Q with the R+*R partials (read r, q; write r),
+// then, once beta is known,  C := C + alpha P  and  P := R + beta P  in one pass
+// over p (read x, p, r; write x, p).  x_{k+1} = x_k + alpha_k p_k uses the p_k
+// the apply read, so the iterates are exactly Fig. 2's.
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads)
-cg_update_xr_kernel(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ p,
-                    const T *__restrict__ q, int64_t N, const CgScalars *sc, double *part)
+cg_update_r_kernel(T *__restrict__ r, const T *__restrict__ q, int64_t N, const CgScalars *sc, double *part)
 {
     if (sc->done) return;
     using V = typename Vec<T>::V;
@@ -302,21 +306,17 @@ cg_update_xr_kernel(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ 
     double acc = 0.0;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
     int64_t nv = 0;
-    if (aligned16(x) && aligned16(r) && aligned16(p) && aligned16(q)) {
+    if (aligned16(r) && aligned16(q)) {
         nv = N / VW;
-        V *xv = reinterpret_cast<V *>(x), *rv = reinterpret_cast<V *>(r);
-        const V *pv = reinterpret_cast<const V *>(p), *qv = reinterpret_cast<const V *>(q);
+        V *rv = reinterpret_cast<V *>(r);
+        const V *qv = reinterpret_cast<const V *>(q);
         for (int64_t i = tid; i < nv; i += nth) {
-            const V pi = __ldcs(pv + i), qi = __ldcs(qv + i);
-            const V xi = __ldcs(xv + i), ri = __ldcs(rv + i);
-            __stcs(xv + i, vaxpy(xi, alpha, pi));        // C := C + alpha*P*D
-            const V rn = vaxpy(ri, -alpha, qi);          // R := R - alpha*Q
+            const V rn = vaxpy(__ldcs(rv + i), -alpha, __ldcs(qv + i));   // R := R - alpha*Q
             __stcs(rv + i, rn);
-            acc += vdot(rn, rn);                         // rho1 := R+*R (partials)
+            acc += vdot(rn, rn);                                           // rho1 := R+*R (partials)
         }
     }
     for (int64_t i = nv * VW + tid; i < N; i += nth) {
-        x[i] = x[i] + alpha * p[i];
         const T rv = r[i] - alpha * q[i];
         r[i] = rv;
         acc += (double)rv * (double)rv;
@@ -325,23 +325,39 @@ cg_update_xr_kernel(T *__restrict__ x, T *__restrict__ r, const T *__restrict__ 
     if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// C := C + alpha*P*D when this iteration's alpha is valid (sc->xupd), then
+// P := R + beta*P unless the solve stopped at this iteration.
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads)
-cg_update_p_kernel(T *__restrict__ p, const T *__restrict__ r, int64_t N, const CgScalars *sc)
+cg_update_xp_kernel(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ r, int64_t N, const CgScalars *sc)
 {
-    if (sc->done) return;
+    if (!sc->xupd) return;
     using V = typename Vec<T>::V;
     constexpr int VW = Vec<T>::W;
+    const T alpha = (T)sc->alpha;
     const T beta = (T)sc->beta;
+    const bool upd_p = !sc->done;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
     int64_t nv = 0;
-    if (aligned16(p) && aligned16(r)) {
+    if (aligned16(x) && aligned16(p) && aligned16(r)) {
         nv = N / VW;
-        V *pv = reinterpret_cast<V *>(p);
+        V *xv = reinterpret_cast<V *>(x), *pv = reinterpret_cast<V *>(p);
         const V *rv = reinterpret_cast<const V *>(r);
-        for (int64_t i = tid; i < nv; i += nth) __stcs(pv + i, vaxpy(__ldcs(rv + i), beta, __ldcs(pv + i)));   // P := R + beta*P
+        if (upd_p) {
+            for (int64_t i = tid; i < nv; i += nth) {
+                const V pi = __ldcs(pv + i), xi = __ldcs(xv + i), ri = __ldcs(rv + i);
+                __stcs(xv + i, vaxpy(xi, alpha, pi));   // C := C + alpha*P*D
+                __stcs(pv + i, vaxpy(ri, beta, pi));    // P := R + beta*P
+            }
+        } else {
+            for (int64_t i = tid; i < nv; i += nth) __stcs(xv + i, vaxpy(__ldcs(xv + i), alpha, __ldcs(pv + i)));
+        }
     }
-    for (int64_t i = nv * VW + tid; i < N; i += nth) p[i] = r[i] + beta * p[i];
+    for (int64_t i = nv * VW + tid; i < N; i += nth) {
+        const T pi = p[i];
+        x[i] = x[i] + alpha * pi;
+        if (upd_p) p[i] = r[i] + beta * pi;
+    }
 }
 
 template <typename T>
@@ -360,18 +376,17 @@ void launch_dot_partials(const T *a, const T *b, int64_t N, double *part,
 }
 
 template <typename T>
-void launch_cg_update_xr(T *x, T *r, const T *p, const T *q, int64_t N,
-                         const CgScalars *sc, double *part, cudaStream_t s)
+void launch_cg_update_r(T *r, const T *q, int64_t N, const CgScalars *sc, double *part, cudaStream_t s)
 {
     count_launch();
-    cg_update_xr_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, q, N, sc, part);
+    cg_update_r_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, q, N, sc, part);
 }
 
 template <typename T>
-void launch_cg_update_p(T *p, const T *r, int64_t N, const CgScalars *sc, cudaStream_t s)
+void launch_cg_update_xp(T *x, T *p, const T *r, int64_t N, const CgScalars *sc, cudaStream_t s)
 {
     count_launch();
-    cg_update_p_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(p, r, N, sc);
+    cg_update_xp_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(x, p, r, N, sc);
 }
 
 // ---------------------------------------------------------------- finalisers
@@ -379,7 +394,11 @@ void launch_cg_update_p(T *p, const T *r, int64_t N, const CgScalars *sc, cudaSt
 __global__ void __launch_bounds__(kRedThreads)
 cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgScalars *sc, double *hist, int stage)
 {
-    if (which != 0 && sc->done) return;
+    if (which != 0 && sc->done) {
+        // stopped in an earlier iteration: this iteration's x update is void
+        if (which == 1 && stage != 1 && threadIdx.x == 0) sc->xupd = 0;
+        return;
+    }
     double s = 0.0;
     if (stage != 2) {
         double acc = 0.0;
@@ -401,15 +420,17 @@ cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgSca
         sc->converged = 0;
         sc->status = TCA_OK;
         sc->done = 0;
+        sc->xupd = 0;
         if (hist) hist[0] = s;
         if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; }
         else if (s == 0.0) { sc->converged = 1; sc->done = 1; }
         else if (sc->max_iters <= 0) { sc->done = 1; if (sc->rtol2 > 0.0) sc->status = TCA_NOT_CONVERGED; }
     } else if (which == 1) {               // alpha := rho / (P+*Q)
         sc->pq = s;
+        sc->xupd = 0;
         if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; }
         else if (!(s > 0.0)) { sc->status = TCA_ERR_BREAKDOWN; sc->done = 1; }
-        else sc->alpha = sc->rho / s;
+        else { sc->alpha = sc->rho / s; sc->xupd = 1; }
     } else {                               // rho1 := R+*R; stop test; beta
         const int k = sc->iters + 1;
         sc->iters = k;
@@ -447,10 +468,10 @@ void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc
                                     cudaStream_t);                                        \
     template void launch_dot_partials<T>(const T *, const T *, int64_t, double *,         \
                                          const int32_t *, cudaStream_t);                  \
-    template void launch_cg_update_xr<T>(T *, T *, const T *, const T *, int64_t,         \
-                                         const CgScalars *, double *, cudaStream_t);      \
-    template void launch_cg_update_p<T>(T *, const T *, int64_t, const CgScalars *,       \
-                                        cudaStream_t);
+    template void launch_cg_update_r<T>(T *, const T *, int64_t, const CgScalars *,       \
+                                        double *, cudaStream_t);                          \
+    template void launch_cg_update_xp<T>(T *, T *, const T *, int64_t, const CgScalars *, \
+                                         cudaStream_t);
 
 TCA_INST(double)
 TCA_INST(float)
