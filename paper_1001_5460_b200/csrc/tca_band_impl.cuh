@@ -233,6 +233,9 @@ __device__ __forceinline__ void ring_step(T (&acc)[6][E], const T (&s)[E], const
     // s: in-slice Kronecker part (goes through G1), q: in-slice regulariser
     // part (identity in mode 1: added to output j only), pc: p itself (R1).
     constexpr int SE = (ROT + 3) % 6;   // slot of j-3 == slot of j+3
+    T pd[E];                            // p_j where it enters <p, Mp>, else 0 (one select per element)
+#pragma unroll
+    for (int e = 0; e < E; ++e) pd[e] = dot ? pc[e] : T(0);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         ov[e] = fma(g1[0], s[e], acc[SE][e]);   // o = -3: finishes output j-3
@@ -243,7 +246,7 @@ __device__ __forceinline__ void ring_step(T (&acc)[6][E], const T (&s)[E], const
 #pragma unroll
         for (int e = 0; e < E; ++e) {
             T v = acc[(ROT + o + 6) % 6][e];
-            if (o == 0 && dot) pq = fma((double)pc[e], (double)v, pq);   // <p_j, old> (see below)
+            if (o == 0) pq = fma((double)pd[e], (double)v, pq);   // <p_j, old> (see below)
             v = fma(g1[o + 3], s[e], v);
             v = fma(r1[o + 2], pc[e], v);
             if (o == 0) {
@@ -252,7 +255,7 @@ __device__ __forceinline__ void ring_step(T (&acc)[6][E], const T (&s)[E], const
                 // so <p, Mp> = sum_j <p_j, M_jj p_j + 2 sum_{j'<j} M_jj' p_j'> and the
                 // slot of output j holds exactly sum_{j'<j} M_jj' p_j' before slab j
                 // is added:  contribution = <p_j, old> + <p_j, new>
-                if (dot) pq = fma((double)pc[e], (double)v, pq);
+                pq = fma((double)pd[e], (double)v, pq);
             }
             acc[(ROT + o + 6) % 6][e] = v;
         }
