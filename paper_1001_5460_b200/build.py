@@ -42,7 +42,8 @@ def up_to_date() -> bool:
 
 def _compile(src: str, objdir: str, verbose: bool) -> str:
     obj = os.path.join(objdir, os.path.basename(src) + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    extra = os.environ.get("TCA_NVCC_EXTRA", "").split()   # experiments only (e.g. -DTCA_BAND_DBG=0)
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -39,6 +39,10 @@
 
 #include "tca_internal.cuh"
 
+#ifndef TCA_BAND_DBG
+#define TCA_BAND_DBG 1   // TCA_BAND_DEBUG phase switches compiled in
+#endif
+
 namespace tca {
 namespace band {
 
@@ -407,8 +411,9 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
 {
     using C = Cfg<T, N4>;
     constexpr int W = C::W, WI = C::WI, PP = C::PP, T3 = C::T3, E = C::E, NTHR = C::NTHR;
+    const int dbg = TCA_BAND_DBG ? a.dbg : 0;   // phase switches (measurement builds only)
     if (a.done && *a.done) return;
-    if (a.dbg & 16) return;
+    if (dbg & 16) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
     T *Pst = reinterpret_cast<T *>(smem_raw + 128);
@@ -426,7 +431,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    if (a.dbg & 32) return;
+    if (dbg & 32) return;
 
     const int seg = tid / (NTHR / C::NSEG);   // warp-uniform
     const int pos = tid % (NTHR / C::NSEG);   // (i2, i3) of the ring owner
@@ -461,7 +466,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         // stage slab js: NB boxes per staged row, issued round-robin by lane 0 of
         // every warp (one warp issuing all of them serialises ~30 UTMALDG)
         auto issue = [&](int js) {
-            if (a.dbg & 256) { ++gi; return; }   // compute-only timing: no loads
+            if (dbg & 256) { ++gi; return; }   // compute-only timing: no loads
             const unsigned st = gi % C::NSTAGE;
             T *dst = Pst + st * C::stage_elems;
             if (onebox) {
@@ -487,19 +492,19 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             }
             ++gi;
         };
-        if (!(a.dbg & 8))
+        if (!(dbg & 8))
             for (int js = jb; js < je && js < jb + C::NSTAGE - 1; ++js) issue(js);
         int next = jb + C::NSTAGE - 1;   // next slab to stage
         int rot = 0;
         int pending = -1;                // output slab whose staging buffer awaits its TMA store
 #pragma unroll 1
         for (int j = j0; j < j1; ++j) {
-            const bool live = j >= jb && j < je && !(a.dbg & 8);
+            const bool live = j >= jb && j < je && !(dbg & 8);
             const T *P = Pst + (gc % C::NSTAGE) * C::stage_elems + delta;
-            if (live && !(a.dbg & (128 | 256))) mbar_wait(bar + gc % C::NSTAGE, (gc / C::NSTAGE) & 1);
+            if (live && !(dbg & (128 | 256))) mbar_wait(bar + gc % C::NSTAGE, (gc / C::NSTAGE) & 1);
 
             // ---- pass A: G2 (all halo-extended columns), lambda R2 (interior columns)
-            if (live && !(a.dbg & 4)) {
+            if (live && !(dbg & 4)) {
 #pragma unroll 1
                 for (int c = tid; c < W; c += NTHR) {
                     T v[PR];
@@ -548,7 +553,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             __syncthreads();   // bar1: U2/RA complete; all threads finished slab j-1
 
             if (pending >= 0) {   // uniform: every thread tracks the same pending slab
-                if (tid == 0 && !(a.dbg & (1 | 256))) {
+                if (tid == 0 && !(dbg & (1 | 256))) {
                     // staging buffer of output slab `pending` (written in pass C of slab pending+3)
                     tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                     bulk_commit();
@@ -556,19 +561,19 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                 }
                 pending = -1;
             }
-            if (live && next < je && !(a.dbg & 64)) {   // stage slab `next` into the stage last read in slab j-1
+            if (live && next < je && !(dbg & 64)) {   // stage slab `next` into the stage last read in slab j-1
                 issue(next);
                 ++next;
             }
 
             // ---- pass B: G3 on U2, lambda R3 on p (8 outputs along i3 per item; item = warp)
-            if (live && !(a.dbg & 4)) pass_b<T, N4, 0>(a, U2, RA, P, U3, RB, a3, warp, lane);
+            if (live && !(dbg & 4)) pass_b<T, N4, 0>(a, U2, RA, P, U3, RB, a3, warp, lane);
             __syncthreads();   // bar2: U3/RB complete
 
             // ---- pass C + mode-1 ring + emission of output slab j-3
             const bool emit = (j - 3 >= o0) && (j - 3 < o1);
             T *OUT = OUTB + (j & 1) * C::OUTE;
-            if (!(a.dbg & 2)) pass_c_dispatch<T, N4, 0>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
+            if (!(dbg & 2)) pass_c_dispatch<T, N4, 0>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
             if (emit) {
                 fence_proxy_async();
                 pending = j - 3;
@@ -578,7 +583,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         }
         __syncthreads();
         if (pending >= 0) {
-            if (tid == 0 && !(a.dbg & (1 | 256))) {
+            if (tid == 0 && !(dbg & (1 | 256))) {
                 tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                 bulk_commit();
             }
