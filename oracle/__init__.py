@@ -65,6 +65,18 @@ def lib():
                                  ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
             L.orc_cg.restype = ctypes.c_int
             L.orc_num_threads.restype = ctypes.c_int
+            L.orc_cholesky.argtypes = [ctypes.c_int64, _dp, _dp]
+            L.orc_cholesky.restype = ctypes.c_int
+            L.orc_geomean_eig.argtypes = [ctypes.c_int64, _dp]
+            L.orc_geomean_eig.restype = ctypes.c_double
+            L.orc_precond_factors.argtypes = [ctypes.c_int, _i64p, ctypes.POINTER(_dp), ctypes.POINTER(_dp),
+                                              ctypes.c_double, ctypes.POINTER(_dp), _dp]
+            L.orc_precond_factors.restype = ctypes.c_int
+            L.orc_precond_apply.argtypes = [ctypes.c_int, _i64p, ctypes.POINTER(_dp), _dp, _dp]
+            L.orc_pcg.argtypes = [ctypes.c_int, _i64p, ctypes.POINTER(_dp), ctypes.POINTER(_dp),
+                                  ctypes.c_double, _dp, _dp, ctypes.c_double, ctypes.c_int, _dp,
+                                  ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+            L.orc_pcg.restype = ctypes.c_int
             _lib = L
     return _lib
 
@@ -179,6 +191,53 @@ class Operator:
         st = lib().orc_cg(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(x),
                           float(rtol), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
         return x, it.value, st, hist[: it.value + 1]
+
+    # ---- Kronecker-factor preconditioner (reading Z22)
+    def precond_factors(self):
+        """(F_d list, eps_d list): F_d = G_d + eps_d R_d, eps_d = lam / prod_{e!=d} gbar_e."""
+        F = [np.empty((k, k)) for k in self.n]
+        eps = np.empty(self.D)
+        st = lib().orc_precond_factors(self.D, self._np, self._G, self._R, self.lam,
+                                       _ptr_array(F), _p(eps))
+        if st != 0:
+            raise ValueError("G_d not positive definite")
+        return F, list(eps)
+
+    def precond_apply(self, r) -> np.ndarray:
+        """z = P^-1 r = (F_1^-1 (x) ... (x) F_D^-1) r by per-mode Cholesky solves."""
+        F, _ = self.precond_factors()
+        C = [cholesky(f) for f in F]
+        r = _f64(r).reshape(self.n)
+        z = np.empty(self.n)
+        lib().orc_precond_apply(self.D, self._np, _ptr_array(C), _p(r), _p(z))
+        return z
+
+    def pcg(self, b, rtol: float, max_iters: int):
+        """Preconditioned CG from x0 = 0.  Returns (x, iters, status, rr_history)."""
+        b = _f64(b).reshape(self.n)
+        x = np.empty(self.n)
+        hist = np.zeros(max_iters + 1)
+        it = ctypes.c_int(0)
+        rf = ctypes.c_double(0.0)
+        st = lib().orc_pcg(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(x),
+                           float(rtol), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
+        return x, it.value, st, hist[: it.value + 1]
+
+
+def cholesky(F) -> np.ndarray:
+    """Lower C with F = C C^T (plain loops); raises if F is not SPD."""
+    F = _f64(F)
+    n = F.shape[0]
+    C = np.empty((n, n))
+    if lib().orc_cholesky(n, _p(F), _p(C)) != 0:
+        raise ValueError("not positive definite")
+    return C
+
+
+def geomean_eig(G) -> float:
+    """det(G)^(1/n): the geometric mean of the eigenvalues of an SPD G."""
+    G = _f64(G)
+    return lib().orc_geomean_eig(G.shape[0], _p(G))
 
 
 def dot(a, b) -> float:

@@ -361,3 +361,177 @@ int orc_cg(int D, const int64_t *n, const double *const *G,
     free(q);
     return status;
 }
+
+/* ------------------------------------------------------------------------
+ * Preconditioned CG with the separable (Kronecker-factor) preconditioner
+ * P = F_1 (x) ... (x) F_D,  F_d = G_d + eps_d R_d  (reading Z22;
+ * SURVEY.md 8(f)1).  The paper's "direct tensor solvers"
+ * applied per mode through the separable structure of Eq. 4:
+ * P^-1 = F_1^-1 (x) ... (x) F_D^-1 is D successive one-dimensional solves.
+ *   gbar_e = det(G_e)^(1/n_e)   (geometric mean of the eigenvalues of G_e;
+ *                                det from the Cholesky diagonal)
+ *   eps_d  = lam / prod_{e != d} gbar_e
+ * ---------------------------------------------------------------------- */
+
+/* Dense Cholesky F = C C^T (C lower, row-major n x n).  Returns 0, or -1 when
+ * F is not positive definite. */
+int orc_cholesky(int64_t n, const double *F, double *C)
+{
+    memset(C, 0, sizeof(double) * n * n);
+    for (int64_t j = 0; j < n; j++) {
+        double s = F[j * n + j];
+        for (int64_t k = 0; k < j; k++) s -= C[j * n + k] * C[j * n + k];
+        if (!(s > 0.0)) return -1;
+        double cjj = sqrt(s);
+        C[j * n + j] = cjj;
+        for (int64_t i = j + 1; i < n; i++) {
+            double t = F[i * n + j];
+            for (int64_t k = 0; k < j; k++) t -= C[i * n + k] * C[j * n + k];
+            C[i * n + j] = t / cjj;
+        }
+    }
+    return 0;
+}
+
+/* gbar = det(G)^(1/n) = exp((2/n) sum_i log C_ii).  Returns NAN if G is not SPD. */
+double orc_geomean_eig(int64_t n, const double *G)
+{
+    double *C = (double *)malloc(sizeof(double) * n * n);
+    double s = 0.0;
+    int bad = orc_cholesky(n, G, C);
+    for (int64_t i = 0; i < n && !bad; i++) s += log(C[i * n + i]);
+    free(C);
+    return bad ? NAN : exp(2.0 * s / (double)n);
+}
+
+/* The factors F_d = G_d + eps_d R_d (R may be NULL or hold NULL entries);
+ * F[d] receives n_d x n_d, eps[d] the weight.  Returns 0 or -1 (not SPD). */
+int orc_precond_factors(int D, const int64_t *n, const double *const *G,
+                        const double *const *R, double lam, double *const *F, double *eps)
+{
+    double gbar[8];
+    for (int d = 0; d < D; d++) {
+        gbar[d] = orc_geomean_eig(n[d], G[d]);
+        if (!(gbar[d] > 0.0)) return -1;
+    }
+    for (int d = 0; d < D; d++) {
+        double pr = 1.0;
+        for (int e = 0; e < D; e++)
+            if (e != d) pr *= gbar[e];
+        eps[d] = lam / pr;
+        for (int64_t i = 0; i < n[d] * n[d]; i++)
+            F[d][i] = G[d][i] + ((R && R[d]) ? eps[d] * R[d][i] : 0.0);
+    }
+    return 0;
+}
+
+/*
+ * z = P^-1 r: for d = 1..D, every mode-d fiber v (stride `inner`) is replaced
+ * by the solution of F_d w = v, by forward substitution with C_d and back
+ * substitution with C_d^T (F_d = C_d C_d^T).  C[d]: Cholesky factors.
+ */
+void orc_precond_apply(int D, const int64_t *n, const double *const *C, const double *r, double *z)
+{
+    int64_t N = prod(n, D);
+    memcpy(z, r, sizeof(double) * N);
+    for (int d = 0; d < D; d++) {
+        int64_t outer = 1, inner = 1, len = n[d];
+        for (int e = 0; e < d; e++) outer *= n[e];
+        for (int e = d + 1; e < D; e++) inner *= n[e];
+        const double *Cd = C[d];
+#pragma omp parallel for collapse(2) schedule(static)
+        for (int64_t o = 0; o < outer; o++)
+            for (int64_t t = 0; t < inner; t++) {
+                double *v = z + o * len * inner + t;
+                for (int64_t i = 0; i < len; i++) {         /* C w' = v */
+                    double s = v[i * inner];
+                    for (int64_t k = 0; k < i; k++) s -= Cd[i * len + k] * v[k * inner];
+                    v[i * inner] = s / Cd[i * len + i];
+                }
+                for (int64_t i = len - 1; i >= 0; i--) {    /* C^T w = w' */
+                    double s = v[i * inner];
+                    for (int64_t k = i + 1; k < len; k++) s -= Cd[k * len + i] * v[k * inner];
+                    v[i * inner] = s / Cd[i * len + i];
+                }
+            }
+    }
+}
+
+/*
+ * Preconditioned CG (the textbook preconditioned form of Fig. 2's iteration):
+ *   C := 0;  R := B;  Z := P^-1 R;  P := Z;  rho := R+*Z;  rr0 := R+*R
+ *   REPEAT  Q := A*P;  alpha := rho / (P+*Q)
+ *           C := C + alpha*P;  R := R - alpha*Q;  rr := R+*R
+ *           [stop test on rr exactly as orc_cg's on rho1 (Z1/Z2/Z12/Z20)]
+ *           Z := P^-1 R;  rho1 := R+*Z  (<= 0 or non-finite: breakdown)
+ *           P := Z + (rho1/rho)*P;  rho := rho1
+ * hist receives rr_0 .. rr_k; *rr_final the last rr.
+ */
+int orc_pcg(int D, const int64_t *n, const double *const *G,
+            const double *const *R, double lam, const double *b, double *x,
+            double rtol, int max_iters, double *hist, int *iters, double *rr_final)
+{
+    int64_t N = prod(n, D);
+    double *Fs[8] = {0}, *Cs[8] = {0}, eps[8];
+    int status = ORC_OK;
+    for (int d = 0; d < D; d++) {
+        Fs[d] = (double *)malloc(sizeof(double) * n[d] * n[d]);
+        Cs[d] = (double *)malloc(sizeof(double) * n[d] * n[d]);
+    }
+    int bad = orc_precond_factors(D, n, G, R, lam, Fs, eps);
+    for (int d = 0; d < D && !bad; d++) bad = orc_cholesky(n[d], Fs[d], Cs[d]);
+    double *r = (double *)malloc(sizeof(double) * N);
+    double *z = (double *)malloc(sizeof(double) * N);
+    double *p = (double *)malloc(sizeof(double) * N);
+    double *q = (double *)malloc(sizeof(double) * N);
+    memset(x, 0, sizeof(double) * N);
+    memcpy(r, b, sizeof(double) * N);
+    double rr = orc_dot(N, r, r), rr0 = rr;
+    if (hist) hist[0] = rr;
+    *iters = 0;
+    if (bad) {
+        status = ORC_BREAKDOWN;
+    } else if (!isfinite(rr)) {
+        status = ORC_NONFINITE;
+    } else if (rr > 0.0) {
+        orc_precond_apply(D, n, (const double *const *)Cs, r, z);
+        memcpy(p, z, sizeof(double) * N);
+        double rho = orc_dot(N, r, z);
+        for (int k = 0; k < max_iters; k++) {
+            orc_apply(D, n, G, R, lam, p, q);
+            double pq = orc_dot(N, p, q);
+            if (!isfinite(pq)) { status = ORC_NONFINITE; break; }
+            if (!(pq > 0.0)) { status = ORC_BREAKDOWN; break; }
+            double alpha = rho / pq;
+            for (int64_t i = 0; i < N; i++) x[i] = x[i] + alpha * p[i];
+            for (int64_t i = 0; i < N; i++) r[i] = r[i] - alpha * q[i];
+            rr = orc_dot(N, r, r);
+            *iters = k + 1;
+            if (hist) hist[k + 1] = rr;
+            if (!isfinite(rr)) { status = ORC_NONFINITE; break; }
+            if (rr == 0.0) break;
+            if (rtol > 0.0 && rr <= rtol * rtol * rr0) break;
+            if (k + 1 == max_iters) {
+                if (rtol > 0.0) status = ORC_NOT_CONVERGED;
+                break;
+            }
+            orc_precond_apply(D, n, (const double *const *)Cs, r, z);
+            double rho1 = orc_dot(N, r, z);
+            if (!isfinite(rho1)) { status = ORC_NONFINITE; break; }
+            if (!(rho1 > 0.0)) { status = ORC_BREAKDOWN; break; }
+            double beta = rho1 / rho;
+            for (int64_t i = 0; i < N; i++) p[i] = z[i] + beta * p[i];
+            rho = rho1;
+        }
+    }
+    if (rr_final) *rr_final = rr;
+    for (int d = 0; d < D; d++) {
+        free(Fs[d]);
+        free(Cs[d]);
+    }
+    free(r);
+    free(z);
+    free(p);
+    free(q);
+    return status;
+}
