@@ -171,6 +171,35 @@ tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol,
                         int32_t max_iters, tca_cg_report *rep, void *stream);
 
 /*
+ * Preconditioned CG (reading Z22) with the
+ * separable Kronecker-factor preconditioner
+ *   P = F_1 (x) ... (x) F_D,  F_d = G_d + eps_d R_d,
+ *   eps_d = lambda / prod_{e != d} gbar_e,  gbar_e = det(G_e)^(1/n_e)
+ * (the geometric mean of G_e's eigenvalues), applied as D successive
+ * one-dimensional Cholesky solves (Eq. 4's separable structure, PAPER.md:68-73,
+ * with the per-mode "direct tensor solver" of PAPER.md:116).  Iteration:
+ *   R := B, Z := P^-1 R, P := Z, rho := R+*Z; repeat Q := M P,
+ *   alpha := rho / P+*Q, C += alpha P, R -= alpha Q, [stop test on R+*R exactly
+ *   as tca_cg_solve's], Z := P^-1 R, rho1 := R+*Z, P := Z + (rho1/rho) P.
+ * Arguments, stop rule, report and stream semantics as tca_cg_solve (the
+ * report's rho values and history are R+*R).  The factors are formed on the
+ * first call (host fp64 Cholesky, n_d <= 256) and kept by the operator.
+ * TCA_ERR_INVALID_ARG on a sharded operator (nranks > 1: the mode-1 solve
+ * would cross shards); TCA_ERR_BREAKDOWN if R+*Z <= 0.
+ */
+tca_status tca_pcg_solve(tca_operator *op, const void *b, void *x, double rtol,
+                         int32_t max_iters, tca_cg_report *rep, void *stream);
+
+/* z = P^-1 r with the PCG preconditioner above (device tensors of the local
+ * shape, z may equal r).  Stream-ordered. */
+tca_status tca_precond_apply(tca_operator *op, const void *r, void *z, void *stream);
+
+/* The preconditioner's eps_d and the lower bandwidth of each Cholesky factor
+ * (order entries each; either pointer may be NULL).  Forms the factors if needed. */
+tca_status tca_precond_info(tca_operator *op, double *eps, int *lower_bandwidth,
+                            void *stream);
+
+/*
  * End-to-end solve from HOST buffers: copies ydata_host (data shape of this
  * rank) to the device, forms the rhs, runs tca_cg_solve and copies x back to
  * x_host (local unknown shape).  Synchronises `stream`.

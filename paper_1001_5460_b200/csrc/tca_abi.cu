@@ -407,6 +407,8 @@ static tca_status halo_p(tca_operator *op, cudaStream_t s)
     return op->transport->halo(0, (char *)op->p, (size_t)op->slab * op->esize, op->nloc1, s);
 }
 
+// One iteration of Fig. 2 (op->pcg_mode == 0) or of its preconditioned form
+// (op->pcg_mode == 1: Z := P^-1 R, rho := R+*Z, P := Z + beta P).
 template <typename T>
 static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
 {
@@ -422,8 +424,16 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
         TCA_TRY(cg_reduce(op, 1, op->part, kRedBlocks, s));          // alpha
     }
     launch_cg_update_r<T>(r, q, op->N, op->sc, op->part, s);         // R := R - alpha*Q, R+*R
-    TCA_TRY(cg_reduce(op, 2, op->part, kRedBlocks, s));              // rho1, stop, beta
-    launch_cg_update_xp<T>(x, p, r, op->N, op->sc, s);               // C := C + alpha*P*D, P := R + beta*P
+    TCA_TRY(cg_reduce(op, 2, op->part, kRedBlocks, s));              // rho1 (PCG: R+*R), stop, beta
+    const T *d = r;
+    if (op->pcg_mode) {
+        T *z = (T *)op->z;
+        TCA_TRY(launch_precond<T>(op, r, z, done, s));               // Z := P^-1 R
+        launch_dot_partials<T>(r, z, op->N, op->part, done, s);      // R+*Z
+        TCA_TRY(cg_reduce(op, 3, op->part, kRedBlocks, s));          // rho1, beta
+        d = z;
+    }
+    launch_cg_update_xp<T>(x, p, d, op->N, op->sc, s);               // C := C + alpha*P*D, P := R|Z + beta*P
     return halo_p(op, s);                                             // ghost slabs of P
 }
 
@@ -485,12 +495,13 @@ static tca_status cg_graph_loop(tca_operator *op, T *x, double rtol, int32_t max
     // with timing, two instances alternate: instance g's events are read while
     // the other instance is queued behind it, so the GPU never drains
     const int ng = op->timing ? 2 : 1;
-    if (!op->gexec[0] || op->gx != (const void *)x || op->gtimed != op->timing) {
+    if (!op->gexec[0] || op->gx != (const void *)x || op->gtimed != op->timing || op->gpcg != op->pcg_mode) {
         TCA_TRY(harvest_timing(op));
         destroy_graphs(op);
         for (int g = 0; g < ng; ++g) TCA_TRY(capture_chunk<T>(op, x, g));
         op->gx = x;
         op->gtimed = op->timing;
+        op->gpcg = op->pcg_mode;
     }
     TCA_CUDA_TRY(cudaEventRecord(op->gfork, s));
     TCA_CUDA_TRY(cudaStreamWaitEvent(op->gstream, op->gfork, 0));
@@ -518,16 +529,25 @@ static tca_status cg_graph_loop(tca_operator *op, T *x, double rtol, int32_t max
 
 template <typename T>
 static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t max_iters,
-                       tca_cg_report *rep, cudaStream_t s)
+                       tca_cg_report *rep, cudaStream_t s, int pcg = 0)
 {
     CgScalars h{};
     h.rtol2 = rtol > 0.0 ? rtol * rtol : 0.0;
     h.max_iters = max_iters;
+    h.pcg = pcg;
+    op->pcg_mode = pcg;
     *op->sc_host = h;
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
     TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
-    launch_cg_init<T>(b, x, (T *)op->r, (T *)op->p_own, op->N, op->part, s);
-    TCA_TRY(cg_reduce(op, 0, op->part, kRedBlocks, s));
+    launch_cg_init<T>(b, x, (T *)op->r, (T *)op->p_own, op->N, op->part, s);   // C := 0, R := B, P := R
+    TCA_TRY(cg_reduce(op, 0, op->part, kRedBlocks, s));                       // rho0 := R+*R
+    if (pcg) {   // Z := P^-1 R, P := Z, rho := R+*Z
+        T *z = (T *)op->z;
+        TCA_TRY(launch_precond<T>(op, (const T *)op->r, z, &op->sc->done, s));
+        TCA_CUDA_TRY(cudaMemcpyAsync(op->p_own, z, (size_t)op->N * op->esize, cudaMemcpyDeviceToDevice, s));
+        launch_dot_partials<T>((const T *)op->r, z, op->N, op->part, &op->sc->done, s);
+        TCA_TRY(cg_reduce(op, 4, op->part, kRedBlocks, s));
+    }
     TCA_TRY(halo_p(op, s));
     static const bool no_graph = getenv("TCA_NO_GRAPH") != nullptr;   // measurement switch
     if (!op->transport && !no_graph && max_iters > 1) {
@@ -559,7 +579,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
         rep->converged = r.converged;
         rep->status = r.status;
         rep->rho0 = r.rho0;
-        rep->rho_final = r.rho;
+        rep->rho_final = r.rr;
         rep->seconds = ms * 1e-3;
         if (rep->rho_history && rep->history_capacity > 0) {
             const int cnt = std::min(rep->history_capacity, r.iters + 1);
@@ -617,7 +637,9 @@ void tca_operator_destroy(tca_operator *op)
     if (op->gstream) cudaStreamDestroy(op->gstream);
     if (op->gfork) cudaEventDestroy(op->gfork);
     if (op->gjoin) cudaEventDestroy(op->gjoin);
-    void *bufs[] = {op->r, op->p, op->q, op->t0, op->t1, op->part, op->sc, op->hist, op->tmap_dev, op->x_ext};
+    void *bufs[] = {op->r,      op->p,    op->q,       op->t0,        op->t1,        op->part,      op->sc,
+                    op->hist,   op->tmap_dev, op->x_ext, op->z,     op->pc_tab[0], op->pc_tab[1], op->pc_tab[2],
+                    op->pc_tab[3]};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (op->sc_host) cudaFreeHost(op->sc_host);
@@ -736,6 +758,8 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
             G.assign(1, 1.0);
             Ad.assign(1, 1.0);
         }
+        op->Gh[d] = G;
+        op->Rh[d] = R;
         op->hbG[d] = half_bandwidth(G, nd);
         const bool banded = op->hbG[d] <= kHG && (!op->has_reg[d] || op->hbR[d] <= kHR);
         if (banded) op->banded_mask |= (1 << d);
@@ -901,8 +925,8 @@ tca_status tca_rhs(const tca_operator *op, const void *ydata, void *b, void *str
     return TCA_OK;
 }
 
-tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
-                        tca_cg_report *rep, void *stream)
+static tca_status solve_common(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
+                               tca_cg_report *rep, void *stream, int pcg)
 {
     TCA_TRY(check_op(op));
     if (!b || !x) return fail(TCA_ERR_INVALID_ARG, "b and x must be non-NULL device pointers");
@@ -917,8 +941,52 @@ tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol, i
         TCA_CUDA_TRY(cudaMalloc(&op->hist, sizeof(double) * (max_iters + 1)));
         op->hist_cap = max_iters + 1;
     }
-    if (op->dtype == TCA_F64) return cg_t<double>(op, (const double *)b, (double *)x, rtol, max_iters, rep, s);
-    return cg_t<float>(op, (const float *)b, (float *)x, rtol, max_iters, rep, s);
+    if (pcg) {
+        if (op->nranks > 1)
+            return fail(TCA_ERR_INVALID_ARG, "tca_pcg_solve: the mode-1 factor solve crosses shards (not available on a "
+                                             "sharded operator)");
+        TCA_TRY(precond_prepare(op, s));
+    }
+    if (op->dtype == TCA_F64)
+        return cg_t<double>(op, (const double *)b, (double *)x, rtol, max_iters, rep, s, pcg);
+    return cg_t<float>(op, (const float *)b, (float *)x, rtol, max_iters, rep, s, pcg);
+}
+
+tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
+                        tca_cg_report *rep, void *stream)
+{
+    return solve_common(op, b, x, rtol, max_iters, rep, stream, 0);
+}
+
+tca_status tca_pcg_solve(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
+                         tca_cg_report *rep, void *stream)
+{
+    return solve_common(op, b, x, rtol, max_iters, rep, stream, 1);
+}
+
+tca_status tca_precond_apply(tca_operator *op, const void *r, void *z, void *stream)
+{
+    TCA_TRY(check_op(op));
+    if (!r || !z) return fail(TCA_ERR_INVALID_ARG, "r and z must be non-NULL device pointers");
+    if (op->nranks > 1)
+        return fail(TCA_ERR_INVALID_ARG, "tca_precond_apply: not available on a sharded operator");
+    cudaStream_t s = (cudaStream_t)stream;
+    TCA_TRY(precond_prepare(op, s));
+    if (op->dtype == TCA_F64) return launch_precond<double>(op, (const double *)r, (double *)z, nullptr, s);
+    return launch_precond<float>(op, (const float *)r, (float *)z, nullptr, s);
+}
+
+tca_status tca_precond_info(tca_operator *op, double *eps, int *lower_bandwidth, void *stream)
+{
+    TCA_TRY(check_op(op));
+    if (op->nranks > 1)
+        return fail(TCA_ERR_INVALID_ARG, "tca_precond_info: not available on a sharded operator");
+    TCA_TRY(precond_prepare(op, (cudaStream_t)stream));
+    for (int d = 0; d < op->order; ++d) {
+        if (eps) eps[d] = op->pc_eps[d];
+        if (lower_bandwidth) lower_bandwidth[d] = op->pc_lbw[d];
+    }
+    return TCA_OK;
 }
 
 tca_status tca_solve_host(tca_operator *op, const void *ydata_host, void *x_host, double rtol,

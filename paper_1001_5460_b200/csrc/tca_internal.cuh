@@ -50,8 +50,8 @@ struct BandMat {
 
 // Device-resident CG scalars (always fp64, reading Z10).
 struct CgScalars {
-    double rho;      // <r_k, r_k>
-    double rho0;     // <r_0, r_0>
+    double rho;      // <r_k, r_k> (CG) or <r_k, z_k> (PCG)
+    double rho0;     // <r_0, r_0> = <b, b>
     double pq;       // <p_k, q_k>
     double alpha;    // rho / pq
     double beta;     // rho1 / rho
@@ -62,7 +62,10 @@ struct CgScalars {
     int32_t status;  // tca_status
     int32_t converged;
     int32_t xupd;    // 1: this iteration's alpha is valid (x := x + alpha p pending)
-    double red[3];   // reduced dot products (stage sum -> all-reduce -> stage apply)
+    double rr;       // <r_k, r_k> (the residual; == rho for plain CG)
+    int32_t pcg;     // 1: preconditioned (rho = <r, z>; beta set by finalize 3)
+    int32_t pad;
+    double red[5];   // reduced dot products (stage sum -> all-reduce -> stage apply)
 };
 
 // Exchange steps of a mode-1 sharded operator (tca_dist.cu).
@@ -114,6 +117,16 @@ struct tca_operator {
     std::vector<double> bandG[tca::kD];
     std::vector<double> bandR[tca::kD];
     std::vector<unsigned char> band_params;   // prebuilt kernel-parameter block (tap tables)
+    // dense host G_d, R_d (fp64; R_d empty without a regulariser) for the PCG factors
+    std::vector<double> Gh[tca::kD], Rh[tca::kD];
+    // Kronecker-factor preconditioner (tca_precond.cu; built on first use)
+    bool pc_ready = false;
+    double pc_eps[tca::kD] = {0, 0, 0, 0};
+    int pc_w[tca::kD] = {0, 0, 0, 0};            // sub-diagonals stored per factor row
+    int pc_lbw[tca::kD] = {0, 0, 0, 0};          // lower bandwidth of the Cholesky factor
+    bool pc_banded[tca::kD] = {false, false, false, false};
+    void *pc_tab[tca::kD] = {nullptr, nullptr, nullptr, nullptr};   // device rows [1/C_ii, C_i,i-1..]
+    void *z = nullptr;                           // PCG workspace z = P^-1 r
     // generic compressed-band forms
     tca::BandMat Gm[tca::kD], Rm[tca::kD], At[tca::kD], Af[tca::kD];
 
@@ -152,6 +165,8 @@ struct tca_operator {
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     const void *gx = nullptr;
     int gtimed = 0;                      // the instances were captured with timing events
+    int gpcg = 0;                        // ... for the preconditioned iteration
+    int pcg_mode = 0;                    // iteration being run/captured: 0 CG (Fig. 2), 1 PCG
     int64_t gkernels[2] = {0, 0};        // kernel launches captured in instance g (added per replay)
     bool gpend[2] = {false, false};      // instance g has launched and its events are unharvested
     std::vector<cudaEvent_t> gev[2];     // captured (external) event pairs of instance g
@@ -190,6 +205,9 @@ void launch_cg_init(const T *b, T *x, T *r, T *p, int64_t N, double *part,
 template <typename T>
 void launch_dot_partials(const T *a, const T *b, int64_t N, double *part,
                          const int32_t *done, cudaStream_t s);
+tca_status precond_prepare(tca_operator *op, cudaStream_t s);
+template <typename T>
+tca_status launch_precond(const tca_operator *op, const T *r, T *z, const int32_t *done, cudaStream_t s);
 template <typename T>
 void launch_cg_update_r(T *r, const T *q, int64_t N, const CgScalars *sc, double *part, cudaStream_t s);
 template <typename T>

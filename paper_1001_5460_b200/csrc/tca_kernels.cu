@@ -416,6 +416,7 @@ cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgSca
     if (which == 0) {                      // rho := R+*R
         sc->rho = s;
         sc->rho0 = s;
+        sc->rr = s;
         sc->iters = 0;
         sc->converged = 0;
         sc->status = TCA_OK;
@@ -431,21 +432,34 @@ cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgSca
         if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; }
         else if (!(s > 0.0)) { sc->status = TCA_ERR_BREAKDOWN; sc->done = 1; }
         else { sc->alpha = sc->rho / s; sc->xupd = 1; }
-    } else {                               // rho1 := R+*R; stop test; beta
+    } else if (which == 2) {               // rho1 := R+*R (PCG: rr); stop test; CG: beta
         const int k = sc->iters + 1;
         sc->iters = k;
+        sc->rr = s;
         if (hist) hist[k] = s;
-        if (!isfinite(s)) { sc->rho = s; sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
-        if (s == 0.0) { sc->rho = s; sc->converged = 1; sc->done = 1; return; }   // Z12
-        if (sc->rtol2 > 0.0 && s <= sc->rtol2 * sc->rho0) {                      // Z1, Z2
-            sc->rho = s; sc->converged = 1; sc->done = 1; return;
+        if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; if (!sc->pcg) sc->rho = s; return; }
+        if (s == 0.0) { sc->converged = 1; sc->done = 1; if (!sc->pcg) sc->rho = s; return; }   // Z12
+        if (sc->rtol2 > 0.0 && s <= sc->rtol2 * sc->rho0) {                                   // Z1, Z2
+            sc->converged = 1; sc->done = 1; if (!sc->pcg) sc->rho = s; return;
         }
         if (k >= sc->max_iters) {
-            sc->rho = s; sc->done = 1;
+            sc->done = 1;
+            if (!sc->pcg) sc->rho = s;
             if (sc->rtol2 > 0.0) sc->status = TCA_NOT_CONVERGED;
             return;
         }
+        if (!sc->pcg) {
+            sc->beta = s / sc->rho;
+            sc->rho = s;
+        }
+    } else if (which == 3) {               // PCG: rho1 := R+*Z; beta
+        if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
+        if (!(s > 0.0)) { sc->status = TCA_ERR_BREAKDOWN; sc->done = 1; return; }
         sc->beta = s / sc->rho;
+        sc->rho = s;
+    } else {                               // 4, PCG start: rho := R+*Z (R = B, Z = P^-1 B)
+        if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
+        if (!(s > 0.0)) { sc->status = TCA_ERR_BREAKDOWN; sc->done = 1; return; }
         sc->rho = s;
     }
 }

@@ -31,7 +31,7 @@ EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
             "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches",
             "tca_operator_apply_path", "tca_shard_layout", "tca_nccl_get_unique_id",
             "tca_nccl_comm_create", "tca_nccl_comm_destroy", "tca_local_group_create",
-            "tca_local_group_destroy"]
+            "tca_local_group_destroy", "tca_pcg_solve", "tca_precond_apply", "tca_precond_info"]
 
 _vp = ctypes.c_void_p
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -92,6 +92,9 @@ _lib.tca_local_group_create.restype = ctypes.c_int
 _lib.tca_local_group_destroy.argtypes = [_vp]
 _lib.tca_local_group_destroy.restype = None
 _lib.tca_operator_apply_path.argtypes = [_vp]
+_lib.tca_pcg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
+_lib.tca_precond_apply.argtypes = [_vp, _vp, _vp, _vp]
+_lib.tca_precond_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), _vp]
 _lib.tca_operator_apply_path.restype = ctypes.c_int
 for _name in ("tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
               "tca_cg_solve", "tca_solve_host", "tca_generate_normal", "tca_forward_model",
@@ -262,6 +265,14 @@ class Operator:
     def cg_solve(self, b, x=None, rtol=0.0, max_iters=100, history=False, stream=None,
                  raise_on=("breakdown", "nonfinite")):
         """Fig. 2 CG from x0 = 0.  Returns (x, report dict)."""
+        return self._solve(_lib.tca_cg_solve, "tca_cg_solve", b, x, rtol, max_iters, history, stream, raise_on)
+
+    def pcg_solve(self, b, x=None, rtol=0.0, max_iters=100, history=False, stream=None,
+                  raise_on=("breakdown", "nonfinite")):
+        """CG preconditioned with the Kronecker-factor P (tca_pcg_solve).  Returns (x, report dict)."""
+        return self._solve(_lib.tca_pcg_solve, "tca_pcg_solve", b, x, rtol, max_iters, history, stream, raise_on)
+
+    def _solve(self, fn, name, b, x, rtol, max_iters, history, stream, raise_on):
         if x is None:
             x = self.empty()
         rep = CgReport()
@@ -270,20 +281,36 @@ class Operator:
             hist = np.zeros(max_iters + 1)
             rep.rho_history = hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
             rep.history_capacity = max_iters + 1
-        st = _lib.tca_cg_solve(self._h, _dev_ptr(b, self.N, self.torch_dtype, "b"),
-                               _dev_ptr(x, self.N, self.torch_dtype, "x"), float(rtol),
-                               int(max_iters), ctypes.byref(rep), _vp(_stream_ptr(stream)))
+        st = fn(self._h, _dev_ptr(b, self.N, self.torch_dtype, "b"),
+                _dev_ptr(x, self.N, self.torch_dtype, "x"), float(rtol),
+                int(max_iters), ctypes.byref(rep), _vp(_stream_ptr(stream)))
         allow = [NOT_CONVERGED]
         if "breakdown" not in raise_on:
             allow.append(ERR_BREAKDOWN)
         if "nonfinite" not in raise_on:
             allow.append(ERR_NONFINITE)
-        _check(st, "tca_cg_solve", allow=allow)
+        _check(st, name, allow=allow)
         out = dict(iterations=rep.iterations, converged=bool(rep.converged), status=rep.status,
                    rho0=rep.rho0, rho_final=rep.rho_final, seconds=rep.seconds)
         if hist is not None:
             out["rho_history"] = hist[: rep.iterations + 1]
         return x, out
+
+    def precond_apply(self, r, z=None, stream=None):
+        """z = P^-1 r with the PCG preconditioner (device tensors of the local shape)."""
+        if z is None:
+            z = self.empty()
+        _check(_lib.tca_precond_apply(self._h, _dev_ptr(r, self.N, self.torch_dtype, "r"),
+                                      _dev_ptr(z, self.N, self.torch_dtype, "z"),
+                                      _vp(_stream_ptr(stream))), "tca_precond_apply")
+        return z
+
+    def precond_info(self):
+        """(eps_d list, lower bandwidth of each Cholesky factor)."""
+        eps = (ctypes.c_double * self.order)()
+        bw = (ctypes.c_int * self.order)()
+        _check(_lib.tca_precond_info(self._h, eps, bw, _vp(0)), "tca_precond_info")
+        return list(eps), list(bw)
 
     def solve_host(self, ydata_host, x_host, rtol=0.0, max_iters=100, stream=None):
         """End-to-end solve from host buffers (torch CPU tensors, pinned recommended)."""
