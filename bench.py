@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--solver", default="cg", choices=["cg", "pcg"],
+                    help="pcg: CG with the Kronecker-factor preconditioner (tca_pcg_solve)")
+    ap.add_argument("--rtol", type=float, default=None, help="override the config's stop rule")
     return ap.parse_args()
 
 
@@ -58,10 +61,12 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def workload_name(cfg, dtype, iters):
+def workload_name(cfg, dtype, iters, rtol=None, solver="cg"):
     n = "x".join(map(str, cfg.n))
     m = "x".join(map(str, cfg.m))
-    stop = f"{iters} CG iterations" if cfg.rtol <= 0 else f"CG to rel. residual {cfg.rtol:g}"
+    rtol = cfg.rtol if rtol is None else rtol
+    name = solver.upper()
+    stop = f"{iters} {name} iterations" if rtol <= 0 else f"{name} to rel. residual {rtol:g}"
     return f"config {cfg.index}: {n} unknowns {dtype}, data {m}, lambda {cfg.lam:g}, {stop}"
 
 
@@ -186,6 +191,8 @@ def run_tca(args):
     dev_index = torch.cuda.current_device()
     cfg = synth.CONFIGS[args.config]
     iters = args.iters or cfg.max_iters
+    rtol = cfg.rtol if args.rtol is None else args.rtol
+    pcg = args.solver == "pcg"
     dtype = args.dtype
     tdt = torch.float64 if dtype == "f64" else torch.float32
     esize = 8 if dtype == "f64" else 4
@@ -232,7 +239,8 @@ def run_tca(args):
         if timing:
             op.set_timing(True)
         b = op.rhs(ydata)                                               # a2
-        x, rep = op.cg_solve(b, rtol=cfg.rtol, max_iters=iters)         # a3-a7
+        solve = op.pcg_solve if pcg else op.cg_solve
+        x, rep = solve(b, rtol=rtol, max_iters=iters)                   # a3-a7
         if timing:
             ms, cnt = op.get_timing()
             state["apply_ms"] = state.get("apply_ms", 0.0) + ms
@@ -301,7 +309,7 @@ def run_tca(args):
     e0.record(stream)
     b = op.rhs(ydata)
     e1.record(stream)
-    x, rep = op.cg_solve(b, rtol=cfg.rtol, max_iters=iters)
+    x, rep = (op.pcg_solve if pcg else op.cg_solve)(b, rtol=rtol, max_iters=iters)
     torch.cuda.synchronize()
     rhs_ms = e0.elapsed_time(e1)
     # standalone apply (operator-apply GB/s, the metric's second half)
@@ -326,12 +334,12 @@ def run_tca(args):
               "apply_us_in_cg": apply_us}
 
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not pcg:   # (tca_solve_host runs plain CG)
         yh = torch.empty(local_m, dtype=tdt, pin_memory=True)
         yh.copy_(ydata.cpu())
         xh = torch.empty(local_n, dtype=tdt, pin_memory=True)
         op = tca.Operator(A, L, cfg.lam, dtype=dtype, dist=dist_arg)
-        op.solve_host(yh, xh, rtol=cfg.rtol, max_iters=iters)   # warm-up
+        op.solve_host(yh, xh, rtol=rtol, max_iters=iters)   # warm-up
         op.close()
         e_steps = max(1, min(args.steps, 3))
         it_sum = 0
@@ -340,7 +348,7 @@ def run_tca(args):
         e0.record(stream)
         for _ in range(e_steps):
             op = tca.Operator(A, L, cfg.lam, dtype=dtype, dist=dist_arg)
-            rep_e = op.solve_host(yh, xh, rtol=cfg.rtol, max_iters=iters)
+            rep_e = op.solve_host(yh, xh, rtol=rtol, max_iters=iters)
             it_sum += rep_e["iterations"]
             retired.append(op)
         e1.record(stream)
@@ -372,7 +380,7 @@ def run_tca(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": dtype, "data": "synthetic (seeded counter RNG on device; cubic B-spline A_d)",
-        "config": {"workload": workload_name(cfg, dtype, iters), "config_index": cfg.index,
+        "config": {"workload": workload_name(cfg, dtype, iters, rtol, args.solver), "solver": args.solver, "config_index": cfg.index,
                    "unknowns": cfg.N, "data_points": cfg.Mdata, "cg_iters_per_step": iters,
                    "step": "tca_operator_create + tca_rhs + tca_cg_solve (operators destroyed after the timed region)",
                    "l2": "inputs larger than L2 (each vector %d MB, y %d MB)" % (

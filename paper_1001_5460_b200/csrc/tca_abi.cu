@@ -144,6 +144,11 @@ static tca_status make_band(tca_dtype dt, const std::vector<double> &M, int rows
     return upload_dtype(dt, taps, &out->taps, bytes);
 }
 
+tca_status make_dense_mat(tca_dtype dt, const std::vector<double> &M, int n, BandMat *out, size_t *bytes)
+{
+    return make_band(dt, M, n, n, -1, out, bytes);
+}
+
 static void free_band(BandMat &b)
 {
     if (b.start) cudaFree(b.start);
@@ -409,6 +414,29 @@ static tca_status halo_p(tca_operator *op, cudaStream_t s)
 
 // One iteration of Fig. 2 (op->pcg_mode == 0) or of its preconditioned form
 // (op->pcg_mode == 1: Z := P^-1 R, rho := R+*Z, P := Z + beta P).
+// z = P^-1 r (PCG): banded factors by the in-place sweep kernel, dense factors
+// (F_d^-1 formed at setup) by the dense mode product on the FP64 tensor cores.
+template <typename T>
+static tca_status apply_precond(tca_operator *op, const T *r, T *z, const int32_t *done, cudaStream_t s)
+{
+    const T *cur = r;
+    for (int d = 0; d < op->order; ++d) {
+        int64_t outer = 1, inner = 1;
+        for (int e = 0; e < d; ++e) outer *= op->n[e];
+        for (int e = d + 1; e < kD; ++e) inner *= op->n[e];
+        if (op->pc_banded[d]) {
+            TCA_TRY(launch_precond_sweep<T>(op, d, cur, z, outer, inner, done, s));
+            cur = z;
+        } else {   // out of place: ping-pong between z and the preconditioner scratch
+            T *dst = (cur == z) ? (T *)op->pc_tmp : z;
+            mode_product<T>(cur, dst, outer, op->pc_inv[d], inner, 1.0, false, done, s);
+            cur = dst;
+        }
+    }
+    if (cur != z) TCA_CUDA_TRY(cudaMemcpyAsync(z, cur, (size_t)op->N * op->esize, cudaMemcpyDeviceToDevice, s));
+    return TCA_OK;
+}
+
 template <typename T>
 static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
 {
@@ -428,7 +456,7 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
     const T *d = r;
     if (op->pcg_mode) {
         T *z = (T *)op->z;
-        TCA_TRY(launch_precond<T>(op, r, z, done, s));               // Z := P^-1 R
+        TCA_TRY(apply_precond<T>(op, r, z, done, s));                // Z := P^-1 R
         launch_dot_partials<T>(r, z, op->N, op->part, done, s);      // R+*Z
         TCA_TRY(cg_reduce(op, 3, op->part, kRedBlocks, s));          // rho1, beta
         d = z;
@@ -543,7 +571,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     TCA_TRY(cg_reduce(op, 0, op->part, kRedBlocks, s));                       // rho0 := R+*R
     if (pcg) {   // Z := P^-1 R, P := Z, rho := R+*Z
         T *z = (T *)op->z;
-        TCA_TRY(launch_precond<T>(op, (const T *)op->r, z, &op->sc->done, s));
+        TCA_TRY(apply_precond<T>(op, (const T *)op->r, z, &op->sc->done, s));
         TCA_CUDA_TRY(cudaMemcpyAsync(op->p_own, z, (size_t)op->N * op->esize, cudaMemcpyDeviceToDevice, s));
         launch_dot_partials<T>((const T *)op->r, z, op->N, op->part, &op->sc->done, s);
         TCA_TRY(cg_reduce(op, 4, op->part, kRedBlocks, s));
@@ -631,6 +659,7 @@ void tca_operator_destroy(tca_operator *op)
         free_band(op->Rm[d]);
         free_band(op->At[d]);
         free_band(op->Af[d]);
+        free_band(op->pc_inv[d]);
     }
     delete op->transport;
     destroy_graphs(op);
@@ -639,7 +668,7 @@ void tca_operator_destroy(tca_operator *op)
     if (op->gjoin) cudaEventDestroy(op->gjoin);
     void *bufs[] = {op->r,      op->p,    op->q,       op->t0,        op->t1,        op->part,      op->sc,
                     op->hist,   op->tmap_dev, op->x_ext, op->z,     op->pc_tab[0], op->pc_tab[1], op->pc_tab[2],
-                    op->pc_tab[3]};
+                    op->pc_tab[3], op->pc_tmp};
     for (void *b : bufs)
         if (b) cudaFree(b);
     if (op->sc_host) cudaFreeHost(op->sc_host);
@@ -972,8 +1001,8 @@ tca_status tca_precond_apply(tca_operator *op, const void *r, void *z, void *str
         return fail(TCA_ERR_INVALID_ARG, "tca_precond_apply: not available on a sharded operator");
     cudaStream_t s = (cudaStream_t)stream;
     TCA_TRY(precond_prepare(op, s));
-    if (op->dtype == TCA_F64) return launch_precond<double>(op, (const double *)r, (double *)z, nullptr, s);
-    return launch_precond<float>(op, (const float *)r, (float *)z, nullptr, s);
+    if (op->dtype == TCA_F64) return apply_precond<double>(op, (const double *)r, (double *)z, nullptr, s);
+    return apply_precond<float>(op, (const float *)r, (float *)z, nullptr, s);
 }
 
 tca_status tca_precond_info(tca_operator *op, double *eps, int *lower_bandwidth, void *stream)

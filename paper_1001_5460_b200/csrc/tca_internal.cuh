@@ -126,7 +126,9 @@ struct tca_operator {
     int pc_lbw[tca::kD] = {0, 0, 0, 0};          // lower bandwidth of the Cholesky factor
     bool pc_banded[tca::kD] = {false, false, false, false};
     void *pc_tab[tca::kD] = {nullptr, nullptr, nullptr, nullptr};   // device rows [1/C_ii, C_i,i-1..]
+    tca::BandMat pc_inv[tca::kD];                // dense factors: F_d^-1 (dense mode product)
     void *z = nullptr;                           // PCG workspace z = P^-1 r
+    void *pc_tmp = nullptr;                      // scratch of the dense-factor mode products
     // generic compressed-band forms
     tca::BandMat Gm[tca::kD], Rm[tca::kD], At[tca::kD], Af[tca::kD];
 
@@ -206,8 +208,12 @@ template <typename T>
 void launch_dot_partials(const T *a, const T *b, int64_t N, double *part,
                          const int32_t *done, cudaStream_t s);
 tca_status precond_prepare(tca_operator *op, cudaStream_t s);
+// banded PCG factor solve along mode d (tca_precond.cu); src may equal dst
 template <typename T>
-tca_status launch_precond(const tca_operator *op, const T *r, T *z, const int32_t *done, cudaStream_t s);
+tca_status launch_precond_sweep(const tca_operator *op, int d, const T *src, T *dst, int64_t outer, int64_t inner,
+                                const int32_t *done, cudaStream_t s);
+// dense n x n matrix in the operator's dtype (tca_abi.cu)
+tca_status make_dense_mat(tca_dtype dt, const std::vector<double> &M, int n, BandMat *out, size_t *bytes);
 template <typename T>
 void launch_cg_update_r(T *r, const T *q, int64_t N, const CgScalars *sc, double *part, cudaStream_t s);
 template <typename T>

@@ -9,13 +9,15 @@
 // tensor solvers", used per mode): every mode-d fibre is solved
 // with the Cholesky factor F_d = C_d C_d^T by a forward and a back sweep.
 //
-// Host: factors in fp64 (dense Cholesky of n_d x n_d, n_d <= 256), stored per
-// mode as rows [1/C_ii, C_i,i-1, ..., C_i,i-W] where W is the factor's lower
-// bandwidth (3 for the B-spline modes: a banded SPD matrix has a banded
-// Cholesky factor; n_d - 1 for dense modes).
-// Device: one thread per fibre, fibres ordered with the mode's inner index
-// fastest so a warp's accesses at each step are contiguous.  W = 3 keeps the
-// last three solved values in registers; the dense form re-reads them (L1).
+// Host: factors in fp64 (dense Cholesky of n_d x n_d, n_d <= 256).  A banded
+// factor (lower bandwidth <= 3: the B-spline modes; a banded SPD matrix has a
+// banded Cholesky factor) is stored as rows [1/C_ii, C_i,i-1, C_i,i-2, C_i,i-3]
+// and solved by the sweep kernel below; a dense factor (Gaussian modes) is
+// replaced by the explicit F_d^-1 and applied as a dense mode product on the
+// FP64 tensor cores (tca_abi.cu apply_precond).
+// Sweep kernel: one thread per fibre, fibres ordered with the mode's inner
+// index fastest so a warp's accesses at each step are contiguous; the last
+// three solved values stay in registers.
 #include <cmath>
 #include <cstring>
 
@@ -29,8 +31,8 @@ namespace {
 // (element i at v[i * inner]); src may equal dst.
 template <typename T, int W>
 __global__ void __launch_bounds__(256)
-precond_sweep_kernel(const T *__restrict__ src, T *dst, int64_t outer, int len, int64_t inner,
-                     const T *__restrict__ tab, int wrt, const int32_t *done)
+precond_sweep_kernel(const T *src, T *dst, int64_t outer, int len, int64_t inner,
+                     const T *__restrict__ tab, const int32_t *done)
 {
     if (done && *done) return;
     const int64_t line = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -39,7 +41,8 @@ precond_sweep_kernel(const T *__restrict__ src, T *dst, int64_t outer, int len, 
     const int64_t base = o * (int64_t)len * inner + t;
     const T *x = src + base;
     T *z = dst + base;
-    if constexpr (W > 0) {
+    static_assert(W >= 1 && W <= 3, "banded factor rows");
+    {
         constexpr int R = W + 1;
         T w1 = T(0), w2 = T(0), w3 = T(0);   // z[i-1], z[i-2], z[i-3]
         for (int i = 0; i < len; ++i) {
@@ -61,21 +64,6 @@ precond_sweep_kernel(const T *__restrict__ src, T *dst, int64_t outer, int len, 
             s *= tab[(int64_t)i * R];
             z[(int64_t)i * inner] = s;
             u3 = u2; u2 = u1; u1 = s;
-        }
-    } else {   // dense factor: row i holds [1/C_ii, C_i,i-1 .. C_i,i-wrt]
-        const int R = wrt + 1;
-        for (int i = 0; i < len; ++i) {
-            const T *c = tab + (int64_t)i * R;
-            T s = x[(int64_t)i * inner];
-            const int kmax = i < wrt ? i : wrt;
-            for (int k = 1; k <= kmax; ++k) s -= c[k] * z[(int64_t)(i - k) * inner];
-            z[(int64_t)i * inner] = s * c[0];
-        }
-        for (int i = len - 1; i >= 0; --i) {
-            T s = z[(int64_t)i * inner];
-            const int kmax = (len - 1 - i) < wrt ? (len - 1 - i) : wrt;
-            for (int k = 1; k <= kmax; ++k) s -= tab[(int64_t)(i + k) * R + k] * z[(int64_t)(i + k) * inner];
-            z[(int64_t)i * inner] = s * tab[(int64_t)i * R];
         }
     }
 }
@@ -131,10 +119,28 @@ tca_status precond_prepare(tca_operator *op, cudaStream_t s)
         for (int i = 0; i < n; ++i)
             for (int k = 0; k < i; ++k)
                 if (C[(size_t)i * n + k] != 0.0 && i - k > w) w = i - k;
-        const int W = w <= 3 ? 3 : w;   // banded form always carries 3 sub-diagonals
-        op->pc_w[d] = W;
         op->pc_lbw[d] = w;
         op->pc_banded[d] = w <= 3;
+        if (!op->pc_banded[d]) {   // dense factor: F_d^-1 = C^-T C^-1, column by column
+            std::vector<double> Fi((size_t)n * n), v(n);
+            for (int j = 0; j < n; ++j) {
+                for (int i = 0; i < n; ++i) {   // C v = e_j
+                    double t = i == j ? 1.0 : 0.0;
+                    for (int k = 0; k < i; ++k) t -= C[(size_t)i * n + k] * v[k];
+                    v[i] = t / C[(size_t)i * n + i];
+                }
+                for (int i = n - 1; i >= 0; --i) {   // C^T u = v
+                    double t = v[i];
+                    for (int k = i + 1; k < n; ++k) t -= C[(size_t)k * n + i] * v[k];
+                    v[i] = t / C[(size_t)i * n + i];
+                }
+                for (int i = 0; i < n; ++i) Fi[(size_t)i * n + j] = v[i];
+            }
+            TCA_TRY(make_dense_mat(op->dtype, Fi, n, &op->pc_inv[d], &bytes));
+            continue;
+        }
+        const int W = 3;   // banded rows: [1/C_ii, C_i,i-1, C_i,i-2, C_i,i-3]
+        op->pc_w[d] = W;
         std::vector<double> tab((size_t)n * (W + 1), 0.0);
         for (int i = 0; i < n; ++i) {
             tab[(size_t)i * (W + 1)] = 1.0 / C[(size_t)i * n + i];
@@ -150,38 +156,34 @@ tca_status precond_prepare(tca_operator *op, cudaStream_t s)
         bytes += raw.size();
     }
     TCA_CUDA_TRY(cudaMalloc(&op->z, (size_t)op->N * op->esize));
-    op->device_bytes += bytes + (size_t)op->N * op->esize;
+    bytes += (size_t)op->N * op->esize;
+    bool any_dense = false;
+    for (int d = 0; d < op->order; ++d) any_dense |= !op->pc_banded[d];
+    if (any_dense) {
+        TCA_CUDA_TRY(cudaMalloc(&op->pc_tmp, (size_t)op->N * op->esize));
+        bytes += (size_t)op->N * op->esize;
+    }
+    op->device_bytes += bytes;
     op->pc_ready = true;
     return TCA_OK;
 }
 
 template <typename T>
-tca_status launch_precond(const tca_operator *op, const T *r, T *z, const int32_t *done, cudaStream_t s)
+tca_status launch_precond_sweep(const tca_operator *op, int d, const T *src, T *dst, int64_t outer, int64_t inner,
+                                const int32_t *done, cudaStream_t s)
 {
-    const T *src = r;
-    for (int d = 0; d < op->order; ++d) {   // mode order 1..D (Eq. 5: any order is the same P^-1)
-        const int len = (int)op->n[d];
-        int64_t outer = 1, inner = 1;
-        for (int e = 0; e < d; ++e) outer *= op->n[e];
-        for (int e = d + 1; e < kD; ++e) inner *= op->n[e];
-        const int64_t lines = outer * inner;
-        const unsigned blocks = (unsigned)((lines + 255) / 256);
-        count_launch();
-        if (op->pc_banded[d])
-            precond_sweep_kernel<T, 3><<<blocks, 256, 0, s>>>(src, z, outer, len, inner, (const T *)op->pc_tab[d], 3,
-                                                               done);
-        else
-            precond_sweep_kernel<T, 0><<<blocks, 256, 0, s>>>(src, z, outer, len, inner, (const T *)op->pc_tab[d],
-                                                               op->pc_w[d], done);
-        TCA_CUDA_TRY(cudaGetLastError());
-        src = z;   // later modes in place
-    }
+    const int len = (int)op->n[d];
+    const int64_t lines = outer * inner;
+    const unsigned blocks = (unsigned)((lines + 255) / 256);
+    count_launch();
+    precond_sweep_kernel<T, 3><<<blocks, 256, 0, s>>>(src, dst, outer, len, inner, (const T *)op->pc_tab[d], done);
+    TCA_CUDA_TRY(cudaGetLastError());
     return TCA_OK;
 }
 
-template tca_status launch_precond<double>(const tca_operator *, const double *, double *, const int32_t *,
-                                           cudaStream_t);
-template tca_status launch_precond<float>(const tca_operator *, const float *, float *, const int32_t *,
-                                          cudaStream_t);
+template tca_status launch_precond_sweep<double>(const tca_operator *, int, const double *, double *, int64_t,
+                                                 int64_t, const int32_t *, cudaStream_t);
+template tca_status launch_precond_sweep<float>(const tca_operator *, int, const float *, float *, int64_t, int64_t,
+                                                const int32_t *, cudaStream_t);
 
 }  // namespace tca
