@@ -3,8 +3,8 @@
 
 A step is one pass of the whole hot path over the
 config's synthetic input resident in HBM: operator setup (tca_operator_create),
-rhs b = (kron A_d^T) y, and the config's CG solve (500 iterations for config 3),
-then destroy.  `value` = CG iterations/s of the whole job.
+rhs b = (kron A_d^T) y, the config's CG solve (500 iterations for config 3) and
+tca_operator_destroy.  `value` = CG iterations/s of the whole job.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--dtype f64]
     python bench.py --impl reference ...     # the CPU oracle, bounded sample
@@ -15,6 +15,7 @@ on the device by the library's seeded generator before the timed region.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -232,15 +233,23 @@ def run_tca(args):
     torch.cuda.synchronize()
 
     state = {}
-    retired = []   # operators are destroyed after the timed region (teardown is not a step of the method)
+    retired = []
 
     def step(timing=False):
+        h0 = time.perf_counter()
         op = tca.Operator(A, L, cfg.lam, dtype=dtype, dist=dist_arg)  # a1
         if timing:
             op.set_timing(True)
+        h1 = time.perf_counter()
         b = op.rhs(ydata)                                               # a2
+        h2 = time.perf_counter()
         solve = op.pcg_solve if pcg else op.cg_solve
         x, rep = solve(b, rtol=rtol, max_iters=iters)                   # a3-a7
+        h3 = time.perf_counter()
+        if timing:   # host-side wall split of each timed step (diagnostics)
+            state.setdefault("host_ms", []).append(
+                [round(1e3 * (h1 - h0), 2), round(1e3 * (h2 - h1), 2), round(1e3 * (h3 - h2), 2),
+                 round(rep["seconds"] * 1e3, 2)])
         if timing:
             ms, cnt = op.get_timing()
             state["apply_ms"] = state.get("apply_ms", 0.0) + ms
@@ -249,7 +258,9 @@ def run_tca(args):
         state["cg_s"] = state.get("cg_s", 0.0) + rep["seconds"]
         state["last_rep"] = rep
         state["path"] = op.apply_path
-        retired.append(op)
+        op.close()   # tca_operator_destroy: its workspaces return to the stream-ordered pool
+        if timing:
+            state["host_ms"][-1].append(round(1e3 * (time.perf_counter() - h3), 2))
         return x
 
     for _ in range(args.warmup):
@@ -264,9 +275,11 @@ def run_tca(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     barrier()
     ev0.record(stream)
+    gc.disable()   # no collector pauses inside the timed steps
     for _ in range(args.steps):
         step(timing=True)
     ev1.record(stream)
+    gc.enable()
     barrier()
     launches = tca.kernel_launches() - launches0
     clk = clocks.stop()
@@ -350,7 +363,7 @@ def run_tca(args):
             op = tca.Operator(A, L, cfg.lam, dtype=dtype, dist=dist_arg)
             rep_e = op.solve_host(yh, xh, rtol=rtol, max_iters=iters)
             it_sum += rep_e["iterations"]
-            retired.append(op)
+            op.close()
         e1.record(stream)
         barrier()
         for o_ in retired:
@@ -382,7 +395,7 @@ def run_tca(args):
         "dtype": dtype, "data": "synthetic (seeded counter RNG on device; cubic B-spline A_d)",
         "config": {"workload": workload_name(cfg, dtype, iters, rtol, args.solver), "solver": args.solver, "config_index": cfg.index,
                    "unknowns": cfg.N, "data_points": cfg.Mdata, "cg_iters_per_step": iters,
-                   "step": "tca_operator_create + tca_rhs + tca_cg_solve (operators destroyed after the timed region)",
+                   "step": "tca_operator_create + tca_rhs + tca_cg_solve (or tca_pcg_solve) + tca_operator_destroy",
                    "l2": "inputs larger than L2 (each vector %d MB, y %d MB)" % (
                        cfg.N * esize >> 20, cfg.Mdata * esize >> 20),
                    "parallelism": "single GPU" if world == 1 else
@@ -398,6 +411,7 @@ def run_tca(args):
                       "rho_final": rep["rho_final"], "status": rep["status"]},
         "apply_path": state["path"],
         "phases": phases,
+        "step_host_ms": state.get("host_ms"),   # [create, rhs enqueue, solve (synchronous), solve device, destroy] per timed step
     }
     print(json.dumps(line), flush=True)
     if tdist is not None:

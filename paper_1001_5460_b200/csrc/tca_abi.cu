@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "tca_fused.cuh"
@@ -42,6 +43,63 @@ static bool all_finite(const double *a, size_t k)
 // nonzeros of each row of M contribute (B-spline rows have <= 4): O(r nnz^2)
 // instead of O(r c^2); skipped products are exact zeros, so the sums are the
 // same as the dense loop's.
+// Small pinned host buffers (CG scalar mirror, tensor-map staging) come from a
+// process-wide free list: cudaMallocHost costs milliseconds and varies, and an
+// operator is created per solve.
+static std::mutex g_pinned_mu;
+static std::vector<std::pair<size_t, void *>> g_pinned_free;
+
+void *pinned_get(size_t bytes)
+{
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        for (size_t i = 0; i < g_pinned_free.size(); ++i)
+            if (g_pinned_free[i].first == bytes) {
+                void *p = g_pinned_free[i].second;
+                g_pinned_free.erase(g_pinned_free.begin() + (long)i);
+                return p;
+            }
+    }
+    void *p = nullptr;
+    return cudaMallocHost(&p, bytes) == cudaSuccess ? p : nullptr;
+}
+
+void pinned_put(void *p, size_t bytes)
+{
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.emplace_back(bytes, p);
+}
+
+// Small device buffers (tap tables, reduction partials, scalars, histories,
+// tensor maps) are recycled through a process-wide size-keyed free list:
+// cudaFree synchronises the device and, measured on B200, occasionally stalls
+// for hundreds of milliseconds; an operator is created and destroyed per solve.
+// (Tensor-sized workspaces use the stream-ordered pool instead.)
+static std::mutex g_dev_mu;
+static std::vector<std::pair<size_t, void *>> g_dev_free;
+
+cudaError_t dev_get(void **p, size_t bytes)
+{
+    {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        for (size_t i = 0; i < g_dev_free.size(); ++i)
+            if (g_dev_free[i].first == bytes) {
+                *p = g_dev_free[i].second;
+                g_dev_free.erase(g_dev_free.begin() + (long)i);
+                return cudaSuccess;
+            }
+    }
+    return cudaMalloc(p, bytes);
+}
+
+void dev_put(void *p, size_t bytes)
+{
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    g_dev_free.emplace_back(bytes, p);
+}
+
 static std::vector<double> gram(const double *M, int64_t r, int64_t c)
 {
     std::vector<double> G((size_t)(c * c), 0.0);
@@ -93,7 +151,7 @@ static tca_status upload(const std::vector<double> &h, void **dptr, size_t *byte
     std::vector<T> c(h.size());
     for (size_t i = 0; i < h.size(); ++i) c[i] = (T)h[i];
     size_t nb = std::max<size_t>(c.size(), 1) * sizeof(T);
-    TCA_CUDA_TRY(cudaMalloc(dptr, nb));
+    TCA_CUDA_TRY(dev_get(dptr, nb));
     *bytes += nb;
     if (!c.empty()) TCA_CUDA_TRY(cudaMemcpy(*dptr, c.data(), c.size() * sizeof(T), cudaMemcpyHostToDevice));
     return TCA_OK;
@@ -138,9 +196,10 @@ static tca_status make_band(tca_dtype dt, const std::vector<double> &M, int rows
     out->dense = (W == cols);
     for (int r = 0; r < rows && out->dense; ++r)
         if (start[r] != 0) out->dense = false;
-    TCA_CUDA_TRY(cudaMalloc(&out->start, sizeof(int) * std::max(rows, 1)));
+    TCA_CUDA_TRY(dev_get((void **)&out->start, sizeof(int) * std::max(rows, 1)));
     *bytes += sizeof(int) * std::max(rows, 1);
     TCA_CUDA_TRY(cudaMemcpy(out->start, start.data(), sizeof(int) * rows, cudaMemcpyHostToDevice));
+    out->tap_bytes = std::max<size_t>(taps.size(), 1) * (dt == TCA_F64 ? sizeof(double) : sizeof(float));
     return upload_dtype(dt, taps, &out->taps, bytes);
 }
 
@@ -151,8 +210,8 @@ tca_status make_dense_mat(tca_dtype dt, const std::vector<double> &M, int n, Ban
 
 static void free_band(BandMat &b)
 {
-    if (b.start) cudaFree(b.start);
-    if (b.taps) cudaFree(b.taps);
+    dev_put(b.start, sizeof(int) * std::max(b.rows, 1));
+    dev_put(b.taps, b.tap_bytes);
     b.start = nullptr;
     b.taps = nullptr;
 }
@@ -220,8 +279,8 @@ tca_status apply_multipass(const tca_operator *op_c, const void *x, void *y,
     tca_operator *op = const_cast<tca_operator *>(op_c);
     if (!op->t0) {   // lazily: only operators whose apply cannot take the fused path use it
         const size_t vb = (size_t)op->N * op->esize;
-        TCA_CUDA_TRY(cudaMalloc(&op->t0, vb));
-        TCA_CUDA_TRY(cudaMalloc(&op->t1, vb));
+        TCA_CUDA_TRY(cudaMallocAsync(&op->t0, vb, s));
+        TCA_CUDA_TRY(cudaMallocAsync(&op->t1, vb, s));
         op->device_bytes += 2 * vb;
     }
     if (op->dtype == TCA_F64)
@@ -666,13 +725,18 @@ void tca_operator_destroy(tca_operator *op)
     if (op->gstream) cudaStreamDestroy(op->gstream);
     if (op->gfork) cudaEventDestroy(op->gfork);
     if (op->gjoin) cudaEventDestroy(op->gjoin);
-    void *bufs[] = {op->r,      op->p,    op->q,       op->t0,        op->t1,        op->part,      op->sc,
-                    op->hist,   op->tmap_dev, op->x_ext, op->z,     op->pc_tab[0], op->pc_tab[1], op->pc_tab[2],
-                    op->pc_tab[3], op->pc_tmp};
-    for (void *b : bufs)
-        if (b) cudaFree(b);
-    if (op->sc_host) cudaFreeHost(op->sc_host);
-    if (op->tmap_host) cudaFreeHost(op->tmap_host);
+    // every stream that used the operator is done before its memory goes back
+    cudaDeviceSynchronize();
+    void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp};   // stream-ordered pool
+    for (void *b : pooled)
+        if (b) cudaFreeAsync(b, 0);
+    dev_put(op->part, sizeof(double) * kRedBlocks * 2);
+    dev_put(op->sc, sizeof(CgScalars));
+    dev_put(op->hist, sizeof(double) * op->hist_cap);
+    dev_put(op->tmap_dev, sizeof(TmapSlot::map) * kTmapSlots);
+    for (int d = 0; d < kD; ++d) dev_put(op->pc_tab[d], op->pc_tab_bytes[d]);
+    pinned_put(op->sc_host, sizeof(CgScalars));
+    pinned_put(op->tmap_host, sizeof(TmapSlot::map) * kTmapSlots);
     for (cudaEvent_t e : op->tmap_ev)
         if (e) cudaEventDestroy(e);
     if (op->ev0) cudaEventDestroy(op->ev0);
@@ -854,14 +918,20 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
     const size_t vb = (size_t)op->N * op->esize;
     const size_t pb = (size_t)(op->nloc1 + 2 * op->ghost) * op->slab * op->esize;   // ghosted p
     cudaError_t e = cudaSuccess;
-    e = cudaMalloc(&op->r, vb);
-    if (e == cudaSuccess) e = cudaMalloc(&op->p, pb);
+    // the vector workspaces come from the device's stream-ordered pool (kept at
+    // a maximal release threshold above): an operator created after another was
+    // destroyed reuses its memory without new mappings
+    e = cudaMallocAsync(&op->r, vb, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&op->p, pb, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(op->p, 0, pb, s);   // ghosts beyond the domain stay 0
     if (e == cudaSuccess) op->p_own = (char *)op->p + (size_t)op->ghost * op->slab * op->esize;
-    if (e == cudaSuccess) e = cudaMalloc(&op->q, vb);
-    if (e == cudaSuccess) e = cudaMalloc(&op->part, sizeof(double) * kRedBlocks * 2);
-    if (e == cudaSuccess) e = cudaMalloc(&op->sc, sizeof(CgScalars));
-    if (e == cudaSuccess) e = cudaMallocHost(&op->sc_host, sizeof(CgScalars));
+    if (e == cudaSuccess) e = cudaMallocAsync(&op->q, vb, s);
+    if (e == cudaSuccess) e = dev_get((void **)&op->part, sizeof(double) * kRedBlocks * 2);
+    if (e == cudaSuccess) e = dev_get((void **)&op->sc, sizeof(CgScalars));
+    if (e == cudaSuccess) {
+        op->sc_host = (CgScalars *)pinned_get(sizeof(CgScalars));
+        if (!op->sc_host) e = cudaErrorMemoryAllocation;
+    }
     if (e == cudaSuccess) e = cudaEventCreate(&op->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&op->ev1);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -905,7 +975,7 @@ tca_status tca_apply(const tca_operator *op, const void *x, void *y, void *strea
         const size_t sb = (size_t)o->slab * o->esize;
         const size_t xb = (size_t)(o->nloc1 + 2 * o->ghost) * sb;
         if (!o->x_ext) {
-            TCA_CUDA_TRY(cudaMalloc(&o->x_ext, xb));
+            TCA_CUDA_TRY(cudaMallocAsync(&o->x_ext, xb, s));
             TCA_CUDA_TRY(cudaMemsetAsync(o->x_ext, 0, xb, s));
             o->device_bytes += xb;
         }
@@ -964,10 +1034,12 @@ static tca_status solve_common(tca_operator *op, const void *b, void *x, double 
     if (!isfinite(rtol)) return fail(TCA_ERR_INVALID_ARG, "rtol must be finite");
     cudaStream_t s = (cudaStream_t)stream;
     if (op->hist_cap < max_iters + 1) {
-        if (op->hist) cudaFree(op->hist);
+        destroy_graphs(op);   // captured iterations reference the old history buffer
+        TCA_CUDA_TRY(cudaStreamSynchronize(s));
+        dev_put(op->hist, sizeof(double) * op->hist_cap);
         op->hist = nullptr;
         op->hist_cap = 0;
-        TCA_CUDA_TRY(cudaMalloc(&op->hist, sizeof(double) * (max_iters + 1)));
+        TCA_CUDA_TRY(dev_get((void **)&op->hist, sizeof(double) * (max_iters + 1)));
         op->hist_cap = max_iters + 1;
     }
     if (pcg) {

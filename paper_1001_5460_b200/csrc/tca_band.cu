@@ -200,8 +200,11 @@ const CUtensorMap *cached_tmap(const tca_operator *op_c, const void *ptr, int ki
             return reinterpret_cast<const CUtensorMap *>(op->tmap_dev) + e.slot;
         }
     if (!op->tmap_dev) {
-        cudaError_t e = cudaMalloc(&op->tmap_dev, sizeof(CUtensorMap) * kTmapSlots);
-        if (e == cudaSuccess) e = cudaMallocHost(&op->tmap_host, sizeof(CUtensorMap) * kTmapSlots);
+        cudaError_t e = dev_get(&op->tmap_dev, sizeof(TmapSlot::map) * kTmapSlots);
+        if (e == cudaSuccess) {
+            op->tmap_host = (uint64_t *)pinned_get(sizeof(TmapSlot::map) * kTmapSlots);
+            if (!op->tmap_host) e = cudaErrorMemoryAllocation;
+        }
         for (int i = 0; i < kTmapSlots && e == cudaSuccess; ++i)
             e = cudaEventCreateWithFlags(&op->tmap_ev[i], cudaEventDisableTiming);
         if (e != cudaSuccess) { *st = cuda_fail(e, "tensor-map buffer"); return nullptr; }

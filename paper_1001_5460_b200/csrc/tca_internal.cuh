@@ -45,6 +45,7 @@ struct BandMat {
     int rows = 0, cols = 0, W = 0;
     int *start = nullptr;  // device, rows
     void *taps = nullptr;  // device, rows*W of the operator dtype
+    size_t tap_bytes = 0;
     bool dense = false;    // W == cols and start == 0: taps is the dense row-major matrix
 };
 
@@ -125,7 +126,8 @@ struct tca_operator {
     int pc_w[tca::kD] = {0, 0, 0, 0};            // sub-diagonals stored per factor row
     int pc_lbw[tca::kD] = {0, 0, 0, 0};          // lower bandwidth of the Cholesky factor
     bool pc_banded[tca::kD] = {false, false, false, false};
-    void *pc_tab[tca::kD] = {nullptr, nullptr, nullptr, nullptr};   // device rows [1/C_ii, C_i,i-1..]
+    void *pc_tab[tca::kD] = {nullptr, nullptr, nullptr, nullptr};   // device factor rows (tca_precond.cu)
+    size_t pc_tab_bytes[tca::kD] = {0, 0, 0, 0};
     tca::BandMat pc_inv[tca::kD];                // dense factors: F_d^-1 (dense mode product)
     void *z = nullptr;                           // PCG workspace z = P^-1 r
     void *pc_tmp = nullptr;                      // scratch of the dense-factor mode products
@@ -208,6 +210,12 @@ template <typename T>
 void launch_dot_partials(const T *a, const T *b, int64_t N, double *part,
                          const int32_t *done, cudaStream_t s);
 tca_status precond_prepare(tca_operator *op, cudaStream_t s);
+// process-wide free list of small pinned host buffers (tca_abi.cu)
+void *pinned_get(size_t bytes);
+// process-wide free list of small device buffers (tca_abi.cu)
+cudaError_t dev_get(void **p, size_t bytes);
+void dev_put(void *p, size_t bytes);
+void pinned_put(void *p, size_t bytes);
 // banded PCG factor solve along mode d (tca_precond.cu); src may equal dst
 template <typename T>
 tca_status launch_precond_sweep(const tca_operator *op, int d, const T *src, T *dst, int64_t outer, int64_t inner,

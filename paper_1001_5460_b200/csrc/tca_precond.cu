@@ -254,17 +254,18 @@ tca_status precond_prepare(tca_operator *op, cudaStream_t s)
         if (op->dtype == TCA_F64) std::memcpy(raw.data(), tab.data(), raw.size());
         else
             for (size_t i = 0; i < tab.size(); ++i) reinterpret_cast<float *>(raw.data())[i] = (float)tab[i];
-        TCA_CUDA_TRY(cudaMalloc(&op->pc_tab[d], raw.size()));
+        TCA_CUDA_TRY(dev_get(&op->pc_tab[d], raw.size()));
+        op->pc_tab_bytes[d] = raw.size();
         TCA_CUDA_TRY(cudaMemcpyAsync(op->pc_tab[d], raw.data(), raw.size(), cudaMemcpyHostToDevice, s));
         TCA_CUDA_TRY(cudaStreamSynchronize(s));
         bytes += raw.size();
     }
-    TCA_CUDA_TRY(cudaMalloc(&op->z, (size_t)op->N * op->esize));
+    TCA_CUDA_TRY(cudaMallocAsync(&op->z, (size_t)op->N * op->esize, s));
     bytes += (size_t)op->N * op->esize;
     bool any_dense = false;
     for (int d = 0; d < op->order; ++d) any_dense |= !op->pc_banded[d];
     if (any_dense) {
-        TCA_CUDA_TRY(cudaMalloc(&op->pc_tmp, (size_t)op->N * op->esize));
+        TCA_CUDA_TRY(cudaMallocAsync(&op->pc_tmp, (size_t)op->N * op->esize, s));
         bytes += (size_t)op->N * op->esize;
     }
     op->device_bytes += bytes;
