@@ -87,6 +87,7 @@ struct Cfg {
     // two 256-thread CTAs per SM
     static constexpr int NTHR = (N4 > 16 || sizeof(T) == 8) ? 512 : 256;
     static constexpr int MINB = NTHR == 512 ? 1 : 2;  // CTAs per SM
+    static constexpr bool RING_SHIFT = sizeof(T) == 4;   // mode-1 ring form (see ring_step)
     static constexpr int T3 = NTHR / (T2 * NSEG);    // mode-3 columns per tile
     static_assert(NTHR % (T2 * NSEG) == 0, "unsupported n4");
     static constexpr int W = (T3 + 6) * N4;          // halo-extended flat columns
@@ -227,11 +228,52 @@ __device__ __forceinline__ T tapR(const Params<T> &a, int off, int r, int k)
     return k >= 0 ? a.taps[(off + r + PADR) * REC + 4 + k] : a.taps[(off + r + k + PADR) * REC + 4 - k];
 }
 
-// ---------------------------------------------------------------- pass C + ring (per segment, per rotation)
-// 6-slot ring: output slab o lives in slot (o - j0) mod 6; at slab j the slot
-// of j-3 is emitted and reused for j+3.
-template <typename T, int E, int ROT>
+// ---------------------------------------------------------------- pass C + ring (per segment)
+// Shift-register form (fp32): 6-slot ring: before slab j, acc[k] holds the partial sum of
+// output slab j-3+k (k = 0..5).  Slab j finishes output j-3 (emitted), adds its
+// contributions to outputs j-2..j+2 while shifting them down one slot (each
+// DFMA writes the slot its input vacates: no register moves, no rotation
+// copies of the code) and starts output j+3 in slot 5.
+template <typename T, int E>
 __device__ __forceinline__ void ring_step(T (&acc)[6][E], const T (&s)[E], const T (&q)[E], const T (&pc)[E],
+                                          const T (&g1)[7], const T (&r1)[5], T (&ov)[E], bool dot, double &pq)
+{
+    // s: in-slice Kronecker part (goes through G1), q: in-slice regulariser
+    // part (identity in mode 1: added to output j only), pc: p itself (R1).
+    T pd[E];                            // p_j where it enters <p, Mp>, else 0 (one select per element)
+#pragma unroll
+    for (int e = 0; e < E; ++e) pd[e] = dot ? pc[e] : T(0);
+#pragma unroll
+    for (int e = 0; e < E; ++e) ov[e] = fma(g1[0], s[e], acc[0][e]);   // o = -3: finishes output j-3
+#pragma unroll
+    for (int o = -2; o <= 2; ++o) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            T v = acc[o + 3][e];
+            if (o == 0) pq = fma((double)pd[e], (double)v, pq);   // <p_j, old> (see below)
+            v = fma(g1[o + 3], s[e], v);
+            v = fma(r1[o + 2], pc[e], v);
+            if (o == 0) {
+                v += q[e];
+                // <p, Mp> without a p history: M is block-symmetric along mode 1,
+                // so <p, Mp> = sum_j <p_j, M_jj p_j + 2 sum_{j'<j} M_jj' p_j'> and the
+                // slot of output j holds exactly sum_{j'<j} M_jj' p_j' before slab j
+                // is added:  contribution = <p_j, old> + <p_j, new>
+                pq = fma((double)pd[e], (double)v, pq);
+            }
+            acc[o + 2][e] = v;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[5][e] = g1[6] * s[e];               // o = +3: first term of output j+3
+}
+
+// Rotating form (fp64): output slab o lives in slot (o - j0) mod 6; at slab j
+// the slot of j-3 is emitted and reused for j+3; the rotation is a compile-time
+// parameter (6 copies of the code).  Measured on B200 (config 3): fp64 320 us
+// rotating vs 327 us shift-register; fp32 296 us rotating vs 266 us shift.
+template <typename T, int E, int ROT>
+__device__ __forceinline__ void ring_step_rot(T (&acc)[6][E], const T (&s)[E], const T (&q)[E], const T (&pc)[E],
                                           const T (&g1)[7], const T (&r1)[5], T (&ov)[E], bool dot, double &pq)
 {
     // s: in-slice Kronecker part (goes through G1), q: in-slice regulariser
@@ -321,13 +363,17 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
     T *out = OUT + (pos / C::T3) * C::WI + (pos % C::T3) * N4 + e0;
     T ov[E];
     const bool dot = a.pq_part != nullptr && j >= o0 && j < o1;   // input slab j is one of this CTA's
-    switch (rot) {
-#define TCA_ROT(R)                                                  \
-    case R:                                                         \
-        ring_step<T, E, R>(acc, s, q, pc, g1, r1, ov, dot, pq);     \
+    if constexpr (C::RING_SHIFT) {
+        ring_step<T, E>(acc, s, q, pc, g1, r1, ov, dot, pq);
+    } else {
+        switch (rot) {
+#define TCA_ROT(R)                                                      \
+    case R:                                                             \
+        ring_step_rot<T, E, R>(acc, s, q, pc, g1, r1, ov, dot, pq);     \
         break;
-        TCA_ROT(0) TCA_ROT(1) TCA_ROT(2) TCA_ROT(3) TCA_ROT(4) default: ring_step<T, E, 5>(acc, s, q, pc, g1, r1, ov, dot, pq);
+            TCA_ROT(0) TCA_ROT(1) TCA_ROT(2) TCA_ROT(3) TCA_ROT(4) default: ring_step_rot<T, E, 5>(acc, s, q, pc, g1, r1, ov, dot, pq);
 #undef TCA_ROT
+        }
     }
     if (emit) {
 #pragma unroll
@@ -495,7 +541,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         if (!(dbg & 8))
             for (int js = jb; js < je && js < jb + C::NSTAGE - 1; ++js) issue(js);
         int next = jb + C::NSTAGE - 1;   // next slab to stage
-        int rot = 0;
+        int rot = 0;                     // ring rotation (rotating form only)
         int pending = -1;                // output slab whose staging buffer awaits its TMA store
 #pragma unroll 1
         for (int j = j0; j < j1; ++j) {
