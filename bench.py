@@ -73,7 +73,7 @@ def workload_name(cfg, dtype, iters, rtol=None, solver="cg"):
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -91,7 +91,9 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
-    def stop(self):
+    def stop(self, window=None):
+        """Median SM clock and throttle reasons of the samples inside `window`
+        (host wall-clock [t0, t1]; all samples if none fall inside)."""
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -102,8 +104,21 @@ class ClockSampler:
             out, _ = self.proc.communicate()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            parts = [p.strip() for p in line.split(",")]
+        lines = out.strip().splitlines()
+        if window is not None:
+            import datetime
+            inside = []
+            for line in lines:
+                try:
+                    ts = datetime.datetime.strptime(line.split(",")[0].strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                if window[0] <= ts <= window[1]:
+                    inside.append(line)
+            if inside:
+                lines = inside
+        for line in lines:
+            parts = [p.strip() for p in line.split(",")][1:]
             if len(parts) < 7:
                 continue
             try:
@@ -263,13 +278,13 @@ def run_tca(args):
             state["host_ms"][-1].append(round(1e3 * (time.perf_counter() - h3), 2))
         return x
 
+    clocks = ClockSampler(dev_index)   # sampling from before the warm-up: no idle gap before timing
+    clocks.start()
     for _ in range(args.warmup):
         step()
     state.clear()
     barrier()
-    clocks = ClockSampler(dev_index)
-    clocks.start()
-    time.sleep(0.3)
+    t_wall0 = time.time()
     launches0 = tca.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -282,7 +297,7 @@ def run_tca(args):
     gc.enable()
     barrier()
     launches = tca.kernel_launches() - launches0
-    clk = clocks.stop()
+    clk = clocks.stop(window=(t_wall0, time.time()))
     total_ms = max_over_ranks(ev0.elapsed_time(ev1))
     for o_ in retired:
         o_.close()

@@ -77,6 +77,36 @@ band_mode_product_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t out
     }
 }
 
+// Short planes (mode D of a wide tensor: rows x 1) would leave most of every
+// block idle in the (plane, outer) mapping: there the flat index runs over
+// outer x plane instead.
+template <typename T>
+__global__ void __launch_bounds__(256)
+band_mode_product_flat_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t total, int rows, int cols,
+                              int inner, const int *__restrict__ start, const T *__restrict__ taps, int W, T alpha,
+                              int accumulate, const int32_t *done)
+{
+    if (done && *done) return;
+    const int64_t plane = (int64_t)rows * inner;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o = idx / plane;
+        const int64_t rem = idx - o * plane;
+        const int r = (int)(rem / inner), t = (int)(rem - (int64_t)r * inner);
+        const int s0 = __ldg(start + r);
+        const T *xp = X + o * (int64_t)cols * inner + t;
+        const T *tp = taps + (int64_t)r * W;
+        T acc = T(0);
+        for (int w = 0; w < W; ++w) {
+            const int c = s0 + w;
+            if (c >= 0 && c < cols) acc = fma(__ldg(tp + w), __ldg(xp + (int64_t)c * inner), acc);
+        }
+        acc *= alpha;
+        if (accumulate) acc += Y[idx];
+        Y[idx] = acc;
+    }
+}
+
 template <typename T>
 void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
                               int64_t inner, double alpha, bool accumulate,
@@ -84,14 +114,22 @@ void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
 {
     const int64_t plane = (int64_t)M.rows * inner;
     if (plane == 0 || outer == 0) return;
+    const int64_t target = 148 * 16;   // enough CTAs to fill the GPU
+    count_launch();
+    if (plane < 64 * 256 && outer > 1) {
+        const int64_t total = plane * outer;
+        const int64_t bx = std::min<int64_t>((total + 255) / 256, 8 * target);
+        band_mode_product_flat_kernel<T><<<(unsigned)bx, 256, 0, s>>>(
+            X, Y, total, M.rows, M.cols, (int)inner, M.start, (const T *)M.taps, M.W, (T)alpha, accumulate ? 1 : 0,
+            done);
+        return;
+    }
     // plane < 2^32 is guaranteed by the extent limits checked at create
     int64_t bx = (plane + 255) / 256;
     int64_t by = outer;
-    const int64_t target = 148 * 16;   // enough CTAs to fill the GPU
     if (bx > target) bx = target;
     if (by > 65535) by = 65535;
     if (bx * by > 8 * target) by = std::max<int64_t>(1, 8 * target / bx);
-    count_launch();
     band_mode_product_kernel<T><<<dim3((unsigned)bx, (unsigned)by), 256, 0, s>>>(
         X, Y, outer, M.rows, M.cols, (int)inner, M.start, (const T *)M.taps, M.W, (T)alpha,
         accumulate ? 1 : 0, done);
