@@ -77,6 +77,61 @@ band_mode_product_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t out
     }
 }
 
+// Row-blocked form for wide fibres (inner >= 256): a block owns RB consecutive
+// output rows x 256 consecutive t and stages the union of their input-row
+// windows (<= KWIN rows) in shared memory once, so each input element is read
+// from memory ~window/RB times instead of W times (config 3's rhs mode 1:
+// 22 staged rows for 8 outputs rows vs 8 taps each).  Falls back to direct
+// loads for a group whose window exceeds KWIN.
+constexpr int kRB = 8, kKWIN = 24;
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+band_mode_product_rows_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t outer, int rows, int cols,
+                              int64_t inner, const int *__restrict__ start, const T *__restrict__ taps, int W,
+                              T alpha, int accumulate, const int32_t *done)
+{
+    if (done && *done) return;
+    __shared__ T sm[kKWIN * 256];
+    const int r0 = blockIdx.y * kRB;
+    const int nr = min(kRB, rows - r0);
+    const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    int c0 = cols, c1 = 0;   // union of the group's windows, clipped to [0, cols)
+    for (int k = 0; k < nr; ++k) {
+        const int sr = __ldg(start + r0 + k);
+        c0 = min(c0, max(sr, 0));
+        c1 = max(c1, min(sr + W, cols));
+    }
+    const bool staged = c1 - c0 <= kKWIN;
+    for (int64_t o = blockIdx.z; o < outer; o += gridDim.z) {
+        const T *xo = X + o * (int64_t)cols * inner;
+        T *yo = Y + o * (int64_t)rows * inner;
+        if (staged) {
+            __syncthreads();   // previous o's reads of sm are done
+            if (t < inner)
+                for (int c = c0; c < c1; ++c) sm[(c - c0) * 256 + threadIdx.x] = xo[(int64_t)c * inner + t];
+            __syncthreads();
+        }
+        if (t >= inner) continue;
+        for (int k = 0; k < nr; ++k) {
+            const int r = r0 + k;
+            const int sr = __ldg(start + r);
+            const T *tp = taps + (int64_t)r * W;
+            T acc = T(0);
+            for (int w = 0; w < W; ++w) {
+                const int c = sr + w;
+                if (c >= 0 && c < cols)
+                    acc = fma(__ldg(tp + w), staged ? sm[(c - c0) * 256 + threadIdx.x] : __ldg(xo + (int64_t)c * inner + t),
+                              acc);
+            }
+            acc *= alpha;
+            T *yp = yo + (int64_t)r * inner + t;
+            if (accumulate) acc += *yp;
+            *yp = acc;
+        }
+    }
+}
+
 // Short planes (mode D of a wide tensor: rows x 1) would leave most of every
 // block idle in the (plane, outer) mapping: there the flat index runs over
 // outer x plane instead.
@@ -122,6 +177,13 @@ void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
         band_mode_product_flat_kernel<T><<<(unsigned)bx, 256, 0, s>>>(
             X, Y, total, M.rows, M.cols, (int)inner, M.start, (const T *)M.taps, M.W, (T)alpha, accumulate ? 1 : 0,
             done);
+        return;
+    }
+    if (inner >= 256 && M.rows >= 2) {
+        const int64_t bx = (inner + 255) / 256, by = (M.rows + kRB - 1) / kRB;
+        const int64_t bz = std::max<int64_t>(1, std::min<int64_t>(outer, std::min<int64_t>(65535, 8 * target / std::max<int64_t>(1, bx * by))));
+        band_mode_product_rows_kernel<T><<<dim3((unsigned)bx, (unsigned)by, (unsigned)bz), 256, 0, s>>>(
+            X, Y, outer, M.rows, M.cols, inner, M.start, (const T *)M.taps, M.W, (T)alpha, accumulate ? 1 : 0, done);
         return;
     }
     // plane < 2^32 is guaranteed by the extent limits checked at create
