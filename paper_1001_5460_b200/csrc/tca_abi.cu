@@ -734,6 +734,7 @@ void tca_operator_destroy(tca_operator *op)
     dev_put(op->sc, sizeof(CgScalars));
     dev_put(op->hist, sizeof(double) * op->hist_cap);
     dev_put(op->tmap_dev, sizeof(TmapSlot::map) * kTmapSlots);
+    dev_put(op->band_gtaps, op->band_gtaps_bytes);
     for (int d = 0; d < kD; ++d) dev_put(op->pc_tab[d], op->pc_tab_bytes[d]);
     pinned_put(op->sc_host, sizeof(CgScalars));
     pinned_put(op->tmap_host, sizeof(TmapSlot::map) * kTmapSlots);

@@ -15,10 +15,14 @@
 
 namespace tca {
 namespace band {
-extern template tca_status launch_dispatch<double>(const tca_operator *, const Params<double> &, cudaStream_t,
+extern template tca_status launch_dispatch<Params<double>>(const tca_operator *, const Params<double> &, cudaStream_t,
                                                    const CUtensorMap *, const CUtensorMap *);
-extern template tca_status launch_dispatch<float>(const tca_operator *, const Params<float> &, cudaStream_t,
+extern template tca_status launch_dispatch<Params<float>>(const tca_operator *, const Params<float> &, cudaStream_t,
                                                   const CUtensorMap *, const CUtensorMap *);
+extern template tca_status launch_dispatch<ParamsG<double>>(const tca_operator *, const ParamsG<double> &, cudaStream_t,
+                                                            const CUtensorMap *, const CUtensorMap *);
+extern template tca_status launch_dispatch<ParamsG<float>>(const tca_operator *, const ParamsG<float> &, cudaStream_t,
+                                                           const CUtensorMap *, const CUtensorMap *);
 extern template int t3_for<double>(int);
 extern template int t3_for<float>(int);
 extern template int boxw_for<double>(int);
@@ -89,11 +93,19 @@ TableLayout table_layout(const tca_operator *op)
     return L;
 }
 
+bool tables_fit(const tca_operator *op);
+
+// Kernel parameters: schedule and table offsets, plus the tap records either in
+// the parameter block (Params, when they fit in TAP_BYTES) or in a device
+// buffer (ParamsG, n_d ~ 256: config 4).
 template <typename T>
-void build_params(const tca_operator *op, std::vector<unsigned char> &blob)
+void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob)
 {
-    blob.assign(sizeof(band::Params<T>), 0);
-    auto *p = reinterpret_cast<band::Params<T> *>(blob.data());
+    tca_operator *op = const_cast<tca_operator *>(op_c);
+    const bool in_block = tables_fit(op);
+    op->band_gt = !in_block;
+    blob.assign(in_block ? sizeof(band::Params<T>) : sizeof(band::ParamsG<T>), 0);
+    auto *p = reinterpret_cast<band::ParamsBase<T> *>(blob.data());
     const TableLayout L = table_layout(op);
     const int t3 = t3_of(op);
     p->n1 = (int)op->nloc1;
@@ -115,12 +127,13 @@ void build_params(const tca_operator *op, std::vector<unsigned char> &blob)
         p->s_o0[b] = (int)(u0 % p->n1);
         p->s_cnt[b] = (int)(u1 - u0);
     }
-    const_cast<tca_operator *>(op)->band_grid = G;
+    op->band_grid = G;
     p->xoff = op->ghost;
     p->nin = (int)op->nloc1 + 2 * op->ghost;
     p->off1 = L.off[0];
     p->off2 = L.off[1];
     p->off3 = L.off[2];
+    std::vector<T> taps((size_t)L.total * band::REC, T(0));
     for (int d = 0; d < kD; ++d) {
         const int nd = (int)(d == 0 ? op->nloc1 : op->n[d]);
         const int row0 = d == 0 ? (int)op->own_lo : 0;   // global row of local row 0 (mode 1 of a shard)
@@ -129,10 +142,20 @@ void build_params(const tca_operator *op, std::vector<unsigned char> &blob)
         for (int r = rlo; r < rhi; ++r) {
             const int64_t g = row0 + r;
             if (g < 0 || g >= op->n[d]) continue;   // outside the domain: zero rows
-            T *rec = p->taps + (size_t)(L.off[d] + r + band::PADR) * band::REC;
+            T *rec = taps.data() + (size_t)(L.off[d] + r + band::PADR) * band::REC;
             for (int k = 0; k < 4; ++k) rec[k] = (T)op->bandG[d][(size_t)g * 4 + k];
             for (int k = 0; k < 3; ++k) rec[4 + k] = (T)op->bandR[d][(size_t)g * 3 + k];
         }
+    }
+    if (in_block) {
+        std::memcpy(reinterpret_cast<band::Params<T> *>(blob.data())->taps, taps.data(), taps.size() * sizeof(T));
+    } else {   // global tables (uploaded once; freed with the operator)
+        const size_t nb = taps.size() * sizeof(T);
+        if (dev_get(&op->band_gtaps, nb) == cudaSuccess) {
+            op->band_gtaps_bytes = nb;
+            cudaMemcpy(op->band_gtaps, taps.data(), nb, cudaMemcpyHostToDevice);
+        }
+        reinterpret_cast<band::ParamsG<T> *>(blob.data())->gtaps = (const T *)op->band_gtaps;
     }
 }
 
@@ -252,7 +275,7 @@ tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_
     const CUtensorMap *ym = cached_tmap(op, y, 1, s, &st, &ys);
     if (!ym) return st;
     // the parameter block is prebuilt at create; patch the per-call pointers
-    band::Params<T> *p = reinterpret_cast<band::Params<T> *>(const_cast<unsigned char *>(op->band_params.data()));
+    band::ParamsBase<T> *p = reinterpret_cast<band::ParamsBase<T> *>(const_cast<unsigned char *>(op->band_params.data()));
     p->x = (const T *)x;
     p->y = (T *)y;
     p->done = done;
@@ -261,7 +284,8 @@ tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_
         static const char *e = getenv("TCA_BAND_DEBUG");
         p->dbg = e ? atoi(e) : 0;
     }
-    TCA_TRY(band::launch_dispatch<T>(op, *p, s, xm, ym));
+    if (op->band_gt) TCA_TRY(band::launch_dispatch(op, *static_cast<band::ParamsG<T> *>(p), s, xm, ym));
+    else TCA_TRY(band::launch_dispatch(op, *static_cast<band::Params<T> *>(p), s, xm, ym));
     // the slots are in use until this launch completes; a launch captured into a
     // CUDA graph keeps using them for the graph's lifetime: pin them instead
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -286,8 +310,7 @@ bool fused_shape_supported(const tca_operator *op)
     (void)n4;
     if ((op->n[2] * op->n[3] * op->esize) % 16 != 0) return false;   // TMA global stride rule
     if (op->nloc1 <= 0 || op->nloc1 > (1ll << 30) || op->n[1] > (1ll << 30)) return false;
-    if (!tables_fit(op)) return false;
-    return get_encode() != nullptr;
+    return get_encode() != nullptr;   // (tables that do not fit the parameter block go to global memory)
 }
 
 tca_status fused_prepare(tca_operator *op)

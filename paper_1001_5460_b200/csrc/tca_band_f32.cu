@@ -4,7 +4,7 @@
 
 namespace tca {
 namespace band {
-template tca_status launch_dispatch<float>(const tca_operator *, const Params<float> &, cudaStream_t, const CUtensorMap *,
+template tca_status launch_dispatch<Params<float>>(const tca_operator *, const Params<float> &, cudaStream_t, const CUtensorMap *,
                                          const CUtensorMap *);
 template int t3_for<float>(int);
 template int boxw_for<float>(int);

@@ -4,7 +4,7 @@
 
 namespace tca {
 namespace band {
-template tca_status launch_dispatch<double>(const tca_operator *, const Params<double> &, cudaStream_t, const CUtensorMap *,
+template tca_status launch_dispatch<Params<double>>(const tca_operator *, const Params<double> &, cudaStream_t, const CUtensorMap *,
                                          const CUtensorMap *);
 template int t3_for<double>(int);
 template int boxw_for<double>(int);

@@ -62,7 +62,7 @@ constexpr int MAXG = 320;        // max persistent CTAs (>= 2 x SM count)
 // integer division on device): the compiler then keeps tile coordinates in
 // uniform registers and loads taps with LDCU into uniform-register operands.
 template <typename T>
-struct Params {
+struct ParamsBase {
     const T *x;
     T *y;
     const int32_t *done;
@@ -75,7 +75,19 @@ struct Params {
     short2 s_tile[MAXG];   // CTA b starts at tile (x = mode-2 tile, y = mode-3 tile) ...
     int s_o0[MAXG];        // ... at output slab s_o0 ...
     int s_cnt[MAXG];       // ... and processes s_cnt (tile, slab) units
+};
+// taps in the parameter block (constant bank: LDCU into uniform-register operands)
+template <typename T>
+struct Params : ParamsBase<T> {
+    using value_type = T;
     T taps[TAP_BYTES / sizeof(T)];
+};
+// tables too large for the parameter block (n_d ~ 256): the same records in
+// global memory, read through the read-only path (register operands)
+template <typename T>
+struct ParamsG : ParamsBase<T> {
+    using value_type = T;
+    const T *gtaps;
 };
 
 template <typename T, int N4>
@@ -227,6 +239,17 @@ __device__ __forceinline__ T tapR(const Params<T> &a, int off, int r, int k)
 {
     return k >= 0 ? a.taps[(off + r + PADR) * REC + 4 + k] : a.taps[(off + r + k + PADR) * REC + 4 - k];
 }
+template <typename T>
+__device__ __forceinline__ T tapG(const ParamsG<T> &a, int off, int r, int k)
+{
+    return k >= 0 ? __ldg(a.gtaps + (off + r + PADR) * REC + k) : __ldg(a.gtaps + (off + r + k + PADR) * REC - k);
+}
+template <typename T>
+__device__ __forceinline__ T tapR(const ParamsG<T> &a, int off, int r, int k)
+{
+    return k >= 0 ? __ldg(a.gtaps + (off + r + PADR) * REC + 4 + k)
+                  : __ldg(a.gtaps + (off + r + k + PADR) * REC + 4 - k);
+}
 
 // ---------------------------------------------------------------- pass C + ring (per segment)
 // Shift-register form (fp32): 6-slot ring: before slab j, acc[k] holds the partial sum of
@@ -308,8 +331,8 @@ __device__ __forceinline__ void ring_step_rot(T (&acc)[6][E], const T (&s)[E], c
     }
 }
 
-template <typename T, int N4, int SEG>
-__device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3, const T *RB,
+template <typename T, int N4, int SEG, typename PA>
+__device__ __forceinline__ void pass_c(const PA &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3, const T *RB,
                                        const T *P, T *OUT, int pos, int rot, int j, bool live, bool emit, int a2,
                                        int a3, int o0, int o1, double &pq)
 {
@@ -381,26 +404,26 @@ __device__ __forceinline__ void pass_c(const Params<T> &a, T (&acc)[6][Cfg<T, N4
     }
 }
 
-template <typename T, int N4, int SEG>
-__device__ __forceinline__ void pass_c_dispatch(const Params<T> &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3,
+template <typename T, int N4, int SEG, typename PA>
+__device__ __forceinline__ void pass_c_dispatch(const PA &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3,
                                                 const T *RB, const T *P, T *OUT, int seg, int pos, int rot, int j,
                                                 bool live, bool emit, int a2, int a3, int o0, int o1, double &pq)
 {
     if constexpr (SEG < Cfg<T, N4>::NSEG) {
-        if (seg == SEG) pass_c<T, N4, SEG>(a, acc, U3, RB, P, OUT, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
-        else pass_c_dispatch<T, N4, SEG + 1>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
+        if (seg == SEG) pass_c<T, N4, SEG, PA>(a, acc, U3, RB, P, OUT, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
+        else pass_c_dispatch<T, N4, SEG + 1, PA>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
     }
 }
 
 // ---------------------------------------------------------------- pass B (compile-time block B)
-template <typename T, int N4, int B>
-__device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T *RA, const T *P, T *U3, T *RB,
+template <typename T, int N4, int B, typename PA>
+__device__ __forceinline__ void pass_b(const PA &a, const T *U2, const T *RA, const T *P, T *U3, T *RB,
                                        int a3, int warp, int lane)
 {
     using C = Cfg<T, N4>;
     if constexpr (B < C::NBLK) {
         if (warp / C::WPB != B) {
-            pass_b<T, N4, B + 1>(a, U2, RA, P, U3, RB, a3, warp, lane);
+            pass_b<T, N4, B + 1, PA>(a, U2, RA, P, U3, RB, a3, warp, lane);
             return;
         }
         constexpr int h0b = B * C::BL;
@@ -450,10 +473,10 @@ __device__ __forceinline__ void pass_b(const Params<T> &a, const T *U2, const T 
 }
 
 // ---------------------------------------------------------------- kernel
-template <typename T, int N4>
+template <typename T, int N4, typename PA>
 __global__ void __launch_bounds__(Cfg<T, N4>::NTHR, Cfg<T, N4>::MINB)
 band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict__ ymp,
-                  const __grid_constant__ Params<T> a)
+                  const __grid_constant__ PA a)
 {
     using C = Cfg<T, N4>;
     constexpr int W = C::W, WI = C::WI, PP = C::PP, T3 = C::T3, E = C::E, NTHR = C::NTHR;
@@ -613,13 +636,13 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             }
 
             // ---- pass B: G3 on U2, lambda R3 on p (8 outputs along i3 per item; item = warp)
-            if (live && !(dbg & 4)) pass_b<T, N4, 0>(a, U2, RA, P, U3, RB, a3, warp, lane);
+            if (live && !(dbg & 4)) pass_b<T, N4, 0, PA>(a, U2, RA, P, U3, RB, a3, warp, lane);
             __syncthreads();   // bar2: U3/RB complete
 
             // ---- pass C + mode-1 ring + emission of output slab j-3
             const bool emit = (j - 3 >= o0) && (j - 3 < o1);
             T *OUT = OUTB + (j & 1) * C::OUTE;
-            if (!(dbg & 2)) pass_c_dispatch<T, N4, 0>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
+            if (!(dbg & 2)) pass_c_dispatch<T, N4, 0, PA>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
             if (emit) {
                 fence_proxy_async();
                 pending = j - 3;
@@ -653,19 +676,19 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
 }
 
 // ---------------------------------------------------------------- host side
-template <typename T, int N4>
-tca_status launch_n4(const tca_operator *op, const Params<T> &prm, cudaStream_t s, const CUtensorMap *xm,
+template <typename T, int N4, typename PA>
+tca_status launch_n4(const tca_operator *op, const PA &prm, cudaStream_t s, const CUtensorMap *xm,
                      const CUtensorMap *ym)
 {
     using C = Cfg<T, N4>;
     static bool attr_set = false;
     if (!attr_set) {
-        TCA_CUDA_TRY(cudaFuncSetAttribute(band_apply_kernel<T, N4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        TCA_CUDA_TRY(cudaFuncSetAttribute(band_apply_kernel<T, N4, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)C::smem_bytes));
         attr_set = true;
     }
     count_launch();
-    band_apply_kernel<T, N4><<<(unsigned)op->band_grid, C::NTHR, C::smem_bytes, s>>>(xm, ym, prm);
+    band_apply_kernel<T, N4, PA><<<(unsigned)op->band_grid, C::NTHR, C::smem_bytes, s>>>(xm, ym, prm);
     TCA_CUDA_TRY(cudaGetLastError());
     return TCA_OK;
 }
@@ -732,13 +755,14 @@ int boxw_for(int n4)
     return 0;
 }
 
-template <typename T>
-tca_status launch_dispatch(const tca_operator *op, const Params<T> &prm, cudaStream_t s, const CUtensorMap *xm,
+template <typename PA>
+tca_status launch_dispatch(const tca_operator *op, const PA &prm, cudaStream_t s, const CUtensorMap *xm,
                            const CUtensorMap *ym)
 {
+    using T = typename PA::value_type;
     switch ((int)op->n[3]) {
 #define TCA_CASE(n) \
-    case n: return launch_n4<T, n>(op, prm, s, xm, ym);
+    case n: return launch_n4<T, n, PA>(op, prm, s, xm, ym);
         TCA_BAND_N4_LIST(TCA_CASE)
 #undef TCA_CASE
     }

@@ -272,3 +272,31 @@ def test_full_size_cfg3_cg_residual_sampled(tca, cfg3_inputs):
     Mx = o.apply_points(xh, pts)
     bb = np.array([b[p] for p in pts])
     assert np.max(np.abs(Mx - bb)) <= 1e-6 * np.abs(b).max()
+
+
+# ------------------------------------------------------------------ tap tables in global memory
+# (n_d ~ 256: the records no longer fit the kernel-parameter block; config 4's shape class)
+def test_apply_global_tables_f64(tca):
+    n, m = (20, 256, 200, 4), (30, 384, 300, 6)
+    A, L = synth.mode_matrices(n, m, seed=2)
+    g = tca.Operator(A, L, 1e-3)
+    assert g.apply_path == "fused"
+    x = synth.random_tensor(n, seed=12)
+    y = to_host(g.apply(to_dev(x)))
+    assert relerr(y, oracle.Operator(A, L, 1e-3).apply(x)) <= 1e-12
+
+
+def test_apply_global_tables_f32_sampled(tca):
+    n, m = (400, 256, 256), (600, 384, 384)
+    A, L = synth.mode_matrices(n, m, seed=2)
+    g = tca.Operator(A, L, 1e-3, dtype="f32")
+    assert g.apply_path == "fused"
+    x = synth.random_tensor(n, seed=13)
+    y = to_host(g.apply(to_dev(x, torch.float32)))
+    rng = np.random.default_rng(4)
+    pts = [tuple(int(rng.integers(0, nd)) for nd in n) for _ in range(150)]
+    pts += [(0, 0, 0), (399, 255, 255), (1, 254, 2), (398, 3, 253)]
+    o = oracle.Operator(A, L, 1e-3)
+    want = o.apply_points(x, pts)
+    got = np.array([y[p] for p in pts])
+    assert relerr(got, want) <= 1e-5
