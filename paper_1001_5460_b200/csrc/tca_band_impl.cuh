@@ -46,10 +46,11 @@
 namespace tca {
 namespace band {
 
-// CTA shape per (dtype, n4) (Cfg): NTHR threads, MINB CTAs per SM.  fp32 with
-// n4 <= 16: two 256-thread CTAs per SM (each with its own barriers and TMA
-// pipeline, so one CTA's barrier/memory phases overlap the other's compute);
-// fp64 and n4 = 32: one 512-thread CTA.
+// CTA shape per n4 (Cfg): NTHR threads, MINB CTAs per SM.  n4 <= 16: two
+// 256-thread CTAs per SM (each with its own barriers and TMA pipeline, so one
+// CTA's barrier/memory phases overlap the other's compute; with the
+// shift-register ring the code fits the instruction cache); n4 = 32: one
+// 512-thread CTA.
 constexpr int T2 = 8;            // mode-2 rows per tile
 constexpr int PR = T2 + 6;       // staged rows (halo 3 + 3)
 constexpr int REC = 7;           // tap record per row: G[r,r..r+3], lambda R[r,r..r+2]
@@ -94,12 +95,9 @@ template <typename T, int N4>
 struct Cfg {
     static constexpr int NSEG = (N4 + 3) / 4;        // ring segments along i4
     static constexpr int E = (N4 + NSEG - 1) / NSEG; // elements per segment (<= 4: ring 24 doubles)
-    // fp64: one 512-thread CTA per SM (T3 = 16: pass-C lanes span 2 mode-2 rows,
-    // conflict-free on the TMA-pitched slab); fp32 (half the shared memory):
-    // two 256-thread CTAs per SM
-    static constexpr int NTHR = (N4 > 16 || sizeof(T) == 8) ? 512 : 256;
+    static constexpr int NTHR = N4 > 16 ? 512 : 256;
     static constexpr int MINB = NTHR == 512 ? 1 : 2;  // CTAs per SM
-    static constexpr bool RING_SHIFT = sizeof(T) == 4;   // mode-1 ring form (see ring_step)
+    static constexpr bool RING_SHIFT = NTHR == 256;   // mode-1 ring form (see ring_step)
     static constexpr int T3 = NTHR / (T2 * NSEG);    // mode-3 columns per tile
     static_assert(NTHR % (T2 * NSEG) == 0, "unsupported n4");
     static constexpr int W = (T3 + 6) * N4;          // halo-extended flat columns
