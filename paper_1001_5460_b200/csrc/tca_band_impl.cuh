@@ -142,7 +142,33 @@ struct Cfg {
     // consecutive banks (conflict-free)
     static constexpr int BANKS = 128 / (int)sizeof(T);
     static constexpr int WP = W + (((N4 - W) % BANKS) + BANKS) % BANKS;    // U2 pitch
-    static constexpr int WIP = WI + (((N4 - WI) % BANKS) + BANKS) % BANKS; // RA/U3/RB pitch
+    // RA/U3/RB pitch: the candidate in [WI, WI + BANKS) with the fewest shared-
+    // memory wavefronts for the two warp access patterns that read these
+    // buffers -- pass B lanes (RPW mode-2 rows x N4) and pass C lanes
+    // (32 / T3 mode-2 rows x T3 columns of stride N4) -- counted per 4-byte bank
+    static constexpr int wavefronts(int X, int pass)
+    {
+        int cnt[32] = {};   // words per 4-byte bank (the lanes' addresses are all distinct)
+        int worst = 0;
+        for (int l = 0; l < 32; ++l) {
+            if (pass == 0 && l >= RPW * N4) continue;
+            const int idx = pass == 0 ? (l / N4) * X + l % N4        // pass B
+                                      : (l / T3) * X + (l % T3) * N4;  // pass C
+            for (int h = 0; h < (int)sizeof(T) / 4; ++h) ++cnt[(idx * ((int)sizeof(T) / 4) + h) % 32];
+        }
+        for (int b = 0; b < 32; ++b) worst = cnt[b] > worst ? cnt[b] : worst;
+        return worst;
+    }
+    static constexpr int pick_wip()
+    {
+        int best = WI, bc = 1 << 30;
+        for (int X = WI; X < WI + BANKS; ++X) {
+            const int c = wavefronts(X, 0) + wavefronts(X, 1);
+            if (c < bc) { bc = c; best = X; }
+        }
+        return best;
+    }
+    static constexpr int WIP = pick_wip();
     static constexpr size_t U2E = al((size_t)T2 * WP);   // smem buffers, each 128-B aligned
     static constexpr size_t WIE = al((size_t)T2 * WIP);
     static constexpr size_t OUTE = al((size_t)T2 * WI);  // TMA store source: dense [T2][WI]
