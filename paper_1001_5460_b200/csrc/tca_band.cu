@@ -32,6 +32,10 @@ extern template int pp_for<float>(int);
 extern template int onebox_for<double>(int);
 extern template int onebox_for<float>(int);
 extern template int minb_for<double>(int);
+extern template int unit_for<double>(int);
+extern template int unit_for<float>(int);
+extern template int pitched_for<double>(int);
+extern template int pitched_for<float>(int);
 extern template int minb_for<float>(int);
 }  // namespace band
 
@@ -63,7 +67,7 @@ int t3_of(const tca_operator *op)
 bool onebox_of(const tca_operator *op)
 {
     const int n4 = (int)op->n[3];
-    const int unit = 128 / (int)op->esize;
+    const int unit = op->dtype == TCA_F64 ? band::unit_for<double>(n4) : band::unit_for<float>(n4);
     const int ob = op->dtype == TCA_F64 ? band::onebox_for<double>(n4) : band::onebox_for<float>(n4);
     const int pp = op->dtype == TCA_F64 ? band::pp_for<double>(n4) : band::pp_for<float>(n4);
     return ob && (op->n[2] * op->n[3]) % unit == 0 && pp / unit <= 256;
@@ -188,8 +192,12 @@ tca_status make_tmap(const tca_operator *op, const void *ptr, int kind, CUtensor
         box[2] = 1;
     }
     cuuint32_t es[4] = {1, 1, 1, 1};
-    if (kind == 0 && onebox_of(op)) {   // whole staged slab (PR rows x PP elements) as one box
-        const cuuint64_t unit = 128 / op->esize;
+    const bool pitched = (op->dtype == TCA_F64 ? band::pitched_for<double>(n4) : band::pitched_for<float>(n4)) != 0;
+    if (kind == 0 && (onebox_of(op) || pitched)) {   // whole staged slab (PR rows x PP elements) as one box
+        // chunk: Cfg::UNIT elements, or 16 B for a pitched fp32 slab whose n3 n4 is not a multiple of UNIT
+        const cuuint64_t unit = onebox_of(op) ? (cuuint64_t)(op->dtype == TCA_F64 ? band::unit_for<double>(n4)
+                                                                                  : band::unit_for<float>(n4))
+                                              : 16 / op->esize;
         const cuuint64_t F = (cuuint64_t)(op->n[2] * op->n[3]);
         const int pp = op->dtype == TCA_F64 ? band::pp_for<double>(n4) : band::pp_for<float>(n4);
         cuuint64_t d4[4] = {unit, F / unit, (cuuint64_t)op->n[1], (cuuint64_t)slabs};

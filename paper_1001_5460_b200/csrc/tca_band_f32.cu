@@ -11,5 +11,7 @@ template int boxw_for<float>(int);
 template int pp_for<float>(int);
 template int onebox_for<float>(int);
 template int minb_for<float>(int);
+template int unit_for<float>(int);
+template int pitched_for<float>(int);
 }  // namespace band
 }  // namespace tca

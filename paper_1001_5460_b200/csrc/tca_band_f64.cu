@@ -11,5 +11,7 @@ template int boxw_for<double>(int);
 template int pp_for<double>(int);
 template int onebox_for<double>(int);
 template int minb_for<double>(int);
+template int unit_for<double>(int);
+template int pitched_for<double>(int);
 }  // namespace band
 }  // namespace tca

@@ -103,16 +103,17 @@ struct Cfg {
     static constexpr int W = (T3 + 6) * N4;          // halo-extended flat columns
     static constexpr int WI = T3 * N4;               // interior flat columns
     static constexpr int VEC = 16 / (int)sizeof(T);  // TMA coordinate granularity (16 B)
-    static constexpr int UNIT = 128 / (int)sizeof(T);
-    // fp32 two-CTA tiles: staged row r is shifted right by SH(r) = 8 pi(r mod 4)
-    // elements (pi = 0,1,3,2) inside its 128-B-aligned TMA row, so the 4 mode-2
-    // rows one pass-C warp reads, and the 2 rows one pass-B warp reads, land on
-    // distinct banks (the TMA rows themselves must stay 128-B aligned)
-    static constexpr bool SHIFTED = sizeof(T) == 4 && (N4 > 16 ? 512 : 256) == 256;
-    static constexpr int SHMAX = SHIFTED ? 24 : 0;
+    // fp32 two-CTA tiles (PITCHED): the slab box uses 32-B chunks and a row
+    // pitch picked against the pass-B/C bank patterns (pick_pp); fp64 keeps
+    // 128-B chunks at a 128-B multiple pitch (measured faster for it)
+    static constexpr bool PITCHED = sizeof(T) == 4 && NTHR == 256;
+    static constexpr bool SHIFTED = false;
+    static constexpr int SHMAX = 0;
+    static constexpr int UNIT = PITCHED ? 8 : 128 / (int)sizeof(T);
     // ONEBOX: the input map is 4-D (UNIT, n3 n4 / UNIT, n2, n1) and a whole staged
-    // slab (PR rows of PP elements) is one TMA box: 128-B chunks, start aligned to
-    // UNIT elements (host picks it when n3 n4 % UNIT == 0; otherwise NB boxes per row)
+    // slab (PR rows of PP elements) is one TMA box, start aligned to UNIT elements
+    // (host picks it when n3 n4 % UNIT == 0; otherwise NB boxes per row for
+    // fp64, 16-B chunks for PITCHED fp32)
     static constexpr bool ONEBOX = !SHIFTED;
     static constexpr int NEED = W + (ONEBOX ? UNIT : VEC) - 1 + SHMAX;
     static constexpr int boxw_for_nb(int nb) { return ((NEED + nb - 1) / nb + UNIT - 1) / UNIT * UNIT; }
@@ -127,7 +128,7 @@ struct Cfg {
     }
     static constexpr int NB = pick_nb();
     static constexpr int BOXW = boxw_for_nb(NB);
-    static constexpr int PP = NB * BOXW;             // staged row pitch
+    static constexpr int PP_BOXES = NB * BOXW;       // staged row pitch (128-B multiple)
     static constexpr int BL = 4;                     // pass-B outputs per item
     static constexpr int NBLK = T3 / BL;
     // pass B: each warp covers whole mode-2 rows of the block (RPW rows of N4
@@ -169,18 +170,30 @@ struct Cfg {
         return best;
     }
     static constexpr int WIP = pick_wip();
+    static constexpr int pick_pp()
+    {
+        if (!PITCHED) return PP_BOXES;
+        const int p0 = (NEED + UNIT - 1) / UNIT * UNIT;
+        int best = p0, bc = 1 << 30;
+        for (int X = p0; X < p0 + BANKS; X += UNIT) {
+            const int c = wavefronts(X, 0) + wavefronts(X, 1);
+            if (c < bc) { bc = c; best = X; }
+        }
+        return best;
+    }
+    static constexpr int PP = pick_pp();             // staged row pitch
     static constexpr size_t U2E = al((size_t)T2 * WP);   // smem buffers, each 128-B aligned
     static constexpr size_t WIE = al((size_t)T2 * WIP);
     static constexpr size_t OUTE = al((size_t)T2 * WI);  // TMA store source: dense [T2][WI]
     static constexpr size_t rest_elems = U2E + 3 * WIE + 2 * OUTE;
-    static constexpr size_t stage_elems = (size_t)PR * PP;
+    static constexpr size_t stage_elems = al((size_t)PR * PP);
     static constexpr size_t SMEM_CAP = MINB == 1 ? 227 * 1024 : 113 * 1024;   // per CTA
     static constexpr int NSTAGE = ((3 * stage_elems + rest_elems) * sizeof(T) + 256 <= SMEM_CAP) ? 3 : 2;
     static constexpr size_t smem_bytes = (NSTAGE * stage_elems + rest_elems) * sizeof(T) + 128;
     static_assert(T3 % BL == 0, "T3");
     static_assert(NBLK * WPB <= NTHR / 32, "pass B: one item per warp");
     static_assert(WI <= 256, "store box");
-    static_assert((PR * PP * sizeof(T)) % 128 == 0 && (BOXW * sizeof(T)) % 128 == 0, "TMA alignment");
+    static_assert(PITCHED || ((PR * PP * sizeof(T)) % 128 == 0 && (BOXW * sizeof(T)) % 128 == 0), "TMA alignment");
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -544,10 +557,16 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         const int b2 = __shfl_sync(0xffffffffu, a.off2 + t2i * T2, 0);   // uniform mode-2 table row base
         const int ca = (a3 - 3) * N4;                              // flat column of staged column 0
         // boxes start 16-B aligned (per-row boxes) or UNIT-aligned (one box per slab)
-        const bool onebox = C::ONEBOX && a.onebox;
+        const bool onebox = C::PITCHED || (C::ONEBOX && a.onebox);
         const int cal = onebox ? C::UNIT : C::VEC;
-        const int delta = ((ca % cal) + cal) % cal;
-        const int cchunk = (ca - delta) / C::UNIT;                 // onebox: first 128-B chunk
+        int delta = ((ca % cal) + cal) % cal;
+        int cchunk = (ca - delta) / C::UNIT;                       // onebox: first chunk
+        if constexpr (C::PITCHED) {   // one box always; 16-B chunks when n3 n4 % UNIT != 0
+            if (!a.onebox) {
+                delta = ((ca % C::VEC) + C::VEC) % C::VEC;
+                cchunk = (ca - delta) / C::VEC;
+            }
+        }
         const int j0 = o0 - 3, j1 = o1 + 3;
         const int jb = j0 > -a.xoff ? j0 : -a.xoff, je = j1 < a.nin - a.xoff ? j1 : a.nin - a.xoff;
 #pragma unroll
@@ -749,6 +768,30 @@ int onebox_for(int n4)
     switch (n4) {
 #define TCA_CASE(n) \
     case n: return Cfg<T, n>::ONEBOX ? 1 : 0;
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return 0;
+}
+
+template <typename T>
+int unit_for(int n4)
+{
+    switch (n4) {
+#define TCA_CASE(n) \
+    case n: return Cfg<T, n>::UNIT;
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return 0;
+}
+
+template <typename T>
+int pitched_for(int n4)
+{
+    switch (n4) {
+#define TCA_CASE(n) \
+    case n: return Cfg<T, n>::PITCHED ? 1 : 0;
         TCA_BAND_N4_LIST(TCA_CASE)
 #undef TCA_CASE
     }
