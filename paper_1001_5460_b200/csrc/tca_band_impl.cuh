@@ -103,10 +103,11 @@ struct Cfg {
     static constexpr int W = (T3 + 6) * N4;          // halo-extended flat columns
     static constexpr int WI = T3 * N4;               // interior flat columns
     static constexpr int VEC = 16 / (int)sizeof(T);  // TMA coordinate granularity (16 B)
-    // fp32 two-CTA tiles (PITCHED): the slab box uses 32-B chunks and a row
-    // pitch picked against the pass-B/C bank patterns (pick_pp); fp64 keeps
-    // 128-B chunks at a 128-B multiple pitch (measured faster for it)
-    static constexpr bool PITCHED = sizeof(T) == 4 && NTHR == 256;
+    // two-CTA tiles (PITCHED): the slab box uses 8-element chunks (64 B fp64,
+    // 32 B fp32) and a row pitch picked against the pass-B/C bank patterns
+    // (pick_pp); measured on config 3: fp64 283 -> 276 us (128-B chunks at a
+    // 128-B pitch before), 32-B fp64 chunks 281 us; fp32 249 -> 234 us
+    static constexpr bool PITCHED = NTHR == 256;
     static constexpr bool SHIFTED = false;
     static constexpr int SHMAX = 0;
     static constexpr int UNIT = PITCHED ? 8 : 128 / (int)sizeof(T);
