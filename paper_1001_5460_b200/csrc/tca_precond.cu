@@ -134,21 +134,40 @@ precond_sweep_smem_kernel(const T *src, T *dst, int64_t outer, int len, int64_t 
     const int j = tid;
     if (j < nl) {
         T w1 = T(0), w2 = T(0), w3 = T(0);
-        // one DFMA on the recurrence's critical path per step (s_{i-1} enters last)
-#pragma unroll 4
+        // one DFMA on the recurrence's critical path per step (s_{i-1} enters last);
+        // the next step's coefficients and input are loaded before this step's
+        // store (the table and the tile share the shared-memory buffer, so the
+        // compiler would otherwise order every load after the previous store)
+        T c0 = tb[0], c1 = tb[1], c2 = tb[2], c3 = tb[3], x0 = v[j];
         for (int i = 0; i < len; ++i) {
-            const T *c = tb + 8 * i;
-            const T s = fma(-c[1], w1, fma(-c[2], w2, fma(-c[3], w3, c[0] * v[i * P + j])));
+            T n0 = T(0), n1 = T(0), n2 = T(0), n3 = T(0), xn = T(0);
+            if (i + 1 < len) {
+                const T *cn = tb + 8 * (i + 1);
+                n0 = cn[0]; n1 = cn[1]; n2 = cn[2]; n3 = cn[3];
+                xn = v[(i + 1) * P + j];
+            }
+            const T s = fma(-c1, w1, fma(-c2, w2, fma(-c3, w3, c0 * x0)));
             v[i * P + j] = s;
             w3 = w2; w2 = w1; w1 = s;
+            c0 = n0; c1 = n1; c2 = n2; c3 = n3; x0 = xn;
         }
         T u1 = T(0), u2 = T(0), u3 = T(0);
-#pragma unroll 4
+        {
+            const T *cb = tb + 8 * (len - 1) + 4;
+            c0 = cb[0]; c1 = cb[1]; c2 = cb[2]; c3 = cb[3];
+        }
+        x0 = v[(len - 1) * P + j];
         for (int i = len - 1; i >= 0; --i) {
-            const T *c = tb + 8 * i + 4;
-            const T s = fma(-c[1], u1, fma(-c[2], u2, fma(-c[3], u3, c[0] * v[i * P + j])));
+            T n0 = T(0), n1 = T(0), n2 = T(0), n3 = T(0), xn = T(0);
+            if (i > 0) {
+                const T *cn = tb + 8 * (i - 1) + 4;
+                n0 = cn[0]; n1 = cn[1]; n2 = cn[2]; n3 = cn[3];
+                xn = v[(i - 1) * P + j];
+            }
+            const T s = fma(-c1, u1, fma(-c2, u2, fma(-c3, u3, c0 * x0)));
             v[i * P + j] = s;
             u3 = u2; u2 = u1; u1 = s;
+            c0 = n0; c1 = n1; c2 = n2; c3 = n3; x0 = xn;
         }
     }
     __syncthreads();
