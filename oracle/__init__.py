@@ -77,6 +77,8 @@ def lib():
                                   ctypes.c_double, _dp, _dp, ctypes.c_double, ctypes.c_int, _dp,
                                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
             L.orc_pcg.restype = ctypes.c_int
+            L.orc_cgsr.argtypes = L.orc_cg.argtypes
+            L.orc_cgsr.restype = ctypes.c_int
             _lib = L
     return _lib
 
@@ -190,6 +192,18 @@ class Operator:
         rf = ctypes.c_double(0.0)
         st = lib().orc_cg(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(x),
                           float(rtol), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
+        return x, it.value, st, hist[: it.value + 1]
+
+    def cgsr(self, b, rtol: float, max_iters: int):
+        """Single-reduction (Chronopoulos-Gear) CG from x0 = 0 (reading Z24).
+        Returns (x, iters, status, rr_history)."""
+        b = _f64(b).reshape(self.n)
+        x = np.empty(self.n)
+        hist = np.zeros(max_iters + 1)
+        it = ctypes.c_int(0)
+        rf = ctypes.c_double(0.0)
+        st = lib().orc_cgsr(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(x),
+                            float(rtol), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
         return x, it.value, st, hist[: it.value + 1]
 
     # ---- Kronecker-factor preconditioner (DESIGN.md reading Z22)

@@ -535,3 +535,75 @@ int orc_pcg(int D, const int64_t *n, const double *const *G,
     free(q);
     return status;
 }
+
+/* ------------------------------------------------------------------------
+ * Single-reduction CG (Chronopoulos & Gear's rearrangement of Fig. 2's CG;
+ * SURVEY.md 8(f)2, reading Z24).  Same Krylov iterates as Fig. 2 in
+ * exact arithmetic; the two inner products of an iteration are taken together
+ * after the one apply, so a distributed solve needs one reduction per step:
+ *   C := 0;  R := B;  W := A*R;  gamma := R+*R;  delta := R+*W
+ *   alpha := gamma / delta;  beta := 0;  P := 0;  S := 0
+ *   REPEAT  P := R + beta*P;  S := W + beta*S        (S = A*P)
+ *           C := C + alpha*P;  R := R - alpha*S
+ *           W := A*R;  gamma1 := R+*R;  delta := R+*W
+ *           [stop test on gamma1 exactly as orc_cg's on rho1]
+ *           beta := gamma1/gamma;  alpha := gamma1 / (delta - beta*gamma1/alpha)
+ *           gamma := gamma1
+ * (alpha's denominator <= 0 or non-finite: breakdown).  hist: gamma_0..gamma_k.
+ * ---------------------------------------------------------------------- */
+int orc_cgsr(int D, const int64_t *n, const double *const *G,
+             const double *const *R, double lam, const double *b, double *x,
+             double rtol, int max_iters, double *hist, int *iters, double *rr_final)
+{
+    int64_t N = prod(n, D);
+    double *r = (double *)malloc(sizeof(double) * N);
+    double *w = (double *)malloc(sizeof(double) * N);
+    double *p = (double *)calloc(N, sizeof(double));
+    double *s = (double *)calloc(N, sizeof(double));
+    int status = ORC_OK;
+    memset(x, 0, sizeof(double) * N);
+    memcpy(r, b, sizeof(double) * N);
+    double gamma = orc_dot(N, r, r), gamma0 = gamma;
+    if (hist) hist[0] = gamma;
+    *iters = 0;
+    if (!isfinite(gamma)) {
+        status = ORC_NONFINITE;
+    } else if (gamma > 0.0 && max_iters > 0) {
+        orc_apply(D, n, G, R, lam, r, w);
+        double delta = orc_dot(N, r, w);
+        double alpha = gamma / delta, beta = 0.0;
+        if (!isfinite(delta)) status = ORC_NONFINITE;
+        else if (!(delta > 0.0)) status = ORC_BREAKDOWN;
+        for (int k = 0; k < max_iters && status == ORC_OK; k++) {
+            for (int64_t i = 0; i < N; i++) p[i] = r[i] + beta * p[i];
+            for (int64_t i = 0; i < N; i++) s[i] = w[i] + beta * s[i];
+            for (int64_t i = 0; i < N; i++) x[i] = x[i] + alpha * p[i];
+            for (int64_t i = 0; i < N; i++) r[i] = r[i] - alpha * s[i];
+            orc_apply(D, n, G, R, lam, r, w);
+            double gamma1 = orc_dot(N, r, r);
+            delta = orc_dot(N, r, w);
+            *iters = k + 1;
+            if (hist) hist[k + 1] = gamma1;
+            if (!isfinite(gamma1)) { gamma = gamma1; status = ORC_NONFINITE; break; }
+            if (gamma1 == 0.0) { gamma = gamma1; break; }
+            if (rtol > 0.0 && gamma1 <= rtol * rtol * gamma0) { gamma = gamma1; break; }
+            if (k + 1 == max_iters) {
+                gamma = gamma1;
+                if (rtol > 0.0) status = ORC_NOT_CONVERGED;
+                break;
+            }
+            beta = gamma1 / gamma;
+            double den = delta - beta * gamma1 / alpha;
+            gamma = gamma1;
+            if (!isfinite(den)) { status = ORC_NONFINITE; break; }
+            if (!(den > 0.0)) { status = ORC_BREAKDOWN; break; }
+            alpha = gamma1 / den;
+        }
+    }
+    if (rr_final) *rr_final = gamma;
+    free(r);
+    free(w);
+    free(p);
+    free(s);
+    return status;
+}

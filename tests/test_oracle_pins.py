@@ -453,3 +453,47 @@ def test_P13_pcg_fewer_iterations_than_cg_on_config0():
     assert stc == stp == oracle.OK
     assert kp < kc
     assert hist[-1] <= cfg.rtol ** 2 * hist[0]
+
+
+# ---------------------------------------------------------------- P14: single-reduction CG (reading Z24)
+@pytest.mark.parametrize("n,m", TINY_SHAPES[:2] + [((6, 5), (9, 9))])
+@pytest.mark.parametrize("basis", ["bspline", "gauss"])
+def test_P14_cgsr_equals_dense_direct_solve(n, m, basis):
+    A, L, op = tiny_problem(n, m, basis=basis)
+    K = brute_force_K(A, L, op.lam)
+    b = synth.random_tensor(n, seed=23)
+    x, k, st, hist = op.cgsr(b, rtol=1e-14, max_iters=3000)
+    ref = np.linalg.solve(K, b.ravel())
+    assert st == oracle.OK
+    tol = max(1e-10, 1e-14 * np.linalg.cond(K))
+    assert np.linalg.norm(x.ravel() - ref) <= tol * np.linalg.norm(ref)
+
+
+def test_P14_cgsr_spec_worked_example():
+    """SPEC.md:495 example through the single-reduction recurrences: exact at
+    k = 2 with gamma = 0 (the Z12 guard)."""
+    g = read_golden("spec_cg_example.txt")
+    T = np.array([[float(v) for v in row.split()] for row in g["matrix"].split(";")])
+    A1 = np.linalg.cholesky(T).T
+    ones = np.array([float(v) for v in g["b"].split()])
+    op = oracle.Operator([A1], None, 0.0)
+    b = op.rhs(np.linalg.solve(A1.T, ones))
+    x, it, st, hist = op.cgsr(b, rtol=1e-15, max_iters=int(g["max_iters"]))
+    want = np.array([float(v) for v in g["x"].split()])
+    assert st == oracle.OK and it <= int(g["max_iters"])
+    assert np.abs(x - want).max() <= 1e-12
+
+
+@pytest.mark.parametrize("cfg_index", [0, 2])
+def test_P14_cgsr_iterates_match_fig2_cg_to_rounding(cfg_index):
+    """Same Krylov iterates as Fig. 2 in exact arithmetic: at matched k the two
+    recurrences differ only by rounding on these well-conditioned systems."""
+    cfg = synth.CONFIGS[cfg_index]
+    A, L = synth.mode_matrices(cfg)
+    op = oracle.Operator(A, L, cfg.lam)
+    b = op.rhs(synth.data(A, cfg.n, cfg.m, seed=1))
+    for k in (5, 30):
+        xa, _, _, ha = op.cg(b, rtol=0.0, max_iters=k)
+        xb, _, _, hb = op.cgsr(b, rtol=0.0, max_iters=k)
+        assert np.linalg.norm(xa - xb) <= 1e-10 * np.linalg.norm(xa)
+        assert np.max(np.abs(ha - hb) / ha) <= 1e-9
