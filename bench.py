@@ -47,8 +47,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--solver", default="cg", choices=["cg", "pcg"],
-                    help="pcg: CG with the Kronecker-factor preconditioner (tca_pcg_solve)")
+    ap.add_argument("--solver", default="cg", choices=["cg", "pcg", "cgsr"],
+                    help="pcg: CG with the Kronecker-factor preconditioner (tca_pcg_solve); "
+                         "cgsr: single-reduction CG (tca_cgsr_solve)")
     ap.add_argument("--rtol", type=float, default=None, help="override the config's stop rule")
     return ap.parse_args()
 
@@ -209,6 +210,7 @@ def run_tca(args):
     iters = args.iters or cfg.max_iters
     rtol = cfg.rtol if args.rtol is None else args.rtol
     pcg = args.solver == "pcg"
+    solver_fn = {"cg": "cg_solve", "pcg": "pcg_solve", "cgsr": "cgsr_solve"}[args.solver]
     dtype = args.dtype
     tdt = torch.float64 if dtype == "f64" else torch.float32
     esize = 8 if dtype == "f64" else 4
@@ -258,8 +260,7 @@ def run_tca(args):
         h1 = time.perf_counter()
         b = op.rhs(ydata)                                               # a2
         h2 = time.perf_counter()
-        solve = op.pcg_solve if pcg else op.cg_solve
-        x, rep = solve(b, rtol=rtol, max_iters=iters)                   # a3-a7
+        x, rep = getattr(op, solver_fn)(b, rtol=rtol, max_iters=iters)  # a3-a7
         h3 = time.perf_counter()
         if timing:   # host-side wall split of each timed step (diagnostics)
             state.setdefault("host_ms", []).append(
@@ -337,7 +338,7 @@ def run_tca(args):
     e0.record(stream)
     b = op.rhs(ydata)
     e1.record(stream)
-    x, rep = (op.pcg_solve if pcg else op.cg_solve)(b, rtol=rtol, max_iters=iters)
+    x, rep = getattr(op, solver_fn)(b, rtol=rtol, max_iters=iters)
     torch.cuda.synchronize()
     rhs_ms = e0.elapsed_time(e1)
     # standalone apply (operator-apply GB/s, the metric's second half)
@@ -362,7 +363,7 @@ def run_tca(args):
               "apply_us_in_cg": apply_us}
 
     e2e = None
-    if not args.no_e2e and not pcg:   # (tca_solve_host runs plain CG)
+    if not args.no_e2e and args.solver == "cg":   # (tca_solve_host runs plain CG)
         yh = torch.empty(local_m, dtype=tdt, pin_memory=True)
         yh.copy_(ydata.cpu())
         xh = torch.empty(local_n, dtype=tdt, pin_memory=True)

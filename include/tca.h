@@ -190,6 +190,23 @@ tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol,
 tca_status tca_pcg_solve(tca_operator *op, const void *b, void *x, double rtol,
                          int32_t max_iters, tca_cg_report *rep, void *stream);
 
+/*
+ * Single-reduction CG (reading Z24): Chronopoulos
+ * and Gear's rearrangement of Fig. 2's recurrences with the
+ * same Krylov iterates in exact arithmetic:
+ *   R := B, W := M R, gamma := R+*R, delta := R+*W, alpha := gamma/delta,
+ *   beta := 0, P := S := 0; repeat P := R + beta P, S := W + beta S,
+ *   C += alpha P, R -= alpha S, W := M R, gamma1 := R+*R, delta := R+*W,
+ *   [stop test on gamma1 exactly as tca_cg_solve's], beta := gamma1/gamma,
+ *   alpha := gamma1 / (delta - beta gamma1 / alpha).
+ * Both inner products of an iteration are reduced together after the apply:
+ * one reduction point per iteration (one all-reduce of two fp64 values on a
+ * sharded operator) instead of two.  Arguments, stop rule, report (rho =
+ * R+*R) and stream semantics as tca_cg_solve; works on sharded operators.
+ */
+tca_status tca_cgsr_solve(tca_operator *op, const void *b, void *x, double rtol,
+                          int32_t max_iters, tca_cg_report *rep, void *stream);
+
 /* z = P^-1 r with the PCG preconditioner above (device tensors of the local
  * shape, z may equal r).  Stream-ordered. */
 tca_status tca_precond_apply(tca_operator *op, const void *r, void *z, void *stream);

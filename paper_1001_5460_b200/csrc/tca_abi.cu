@@ -471,8 +471,6 @@ static tca_status halo_p(tca_operator *op, cudaStream_t s)
     return op->transport->halo(0, (char *)op->p, (size_t)op->slab * op->esize, op->nloc1, s);
 }
 
-// One iteration of Fig. 2 (op->pcg_mode == 0) or of its preconditioned form
-// (op->pcg_mode == 1: Z := P^-1 R, rho := R+*Z, P := Z + beta P).
 // z = P^-1 r (PCG): banded factors by the in-place sweep kernel, dense factors
 // (F_d^-1 formed at setup) by the dense mode product on the FP64 tensor cores.
 template <typename T>
@@ -496,11 +494,49 @@ static tca_status apply_precond(tca_operator *op, const T *r, T *z, const int32_
     return TCA_OK;
 }
 
+// Single-reduction CG: W := A*R with R+*W from the apply, R+*R from the update
+// kernel, both reduced together (one all-reduce of two scalars when sharded).
+// The CGSR vectors: R in the ghosted buffer (op->p, the apply input), P in
+// op->r, S in op->sr_s, W in op->q.
+template <typename T>
+static tca_status cgsr_apply_reduce(tca_operator *op, int which, cudaStream_t s)
+{
+    T *rg = (T *)op->p, *r = (T *)op->p_own, *w = (T *)op->q;
+    const int32_t *done = &op->sc->done;
+    double *prw = op->part + kRedBlocks;
+    int nrw = kRedBlocks;
+    static const bool no_fused_dot = getenv("TCA_NO_FUSED_DOT") != nullptr;
+    if (fused_used(op, rg, w) && !no_fused_dot) {
+        TCA_TRY(timed_apply(op, rg, w, which == 7 ? nullptr : done, s, prw));   // W := A*R, R+*W
+        nrw = op->band_grid;
+    } else {
+        TCA_TRY(timed_apply(op, rg, w, which == 7 ? nullptr : done, s));
+        launch_dot_partials<T>(r, w, op->N, prw, which == 7 ? nullptr : done, s);
+    }
+    if (!op->transport) {
+        launch_cgsr_finalize(which, op->part, kRedBlocks, prw, nrw, op->sc, op->hist, s, 0);
+        return TCA_OK;
+    }
+    launch_cgsr_finalize(which, op->part, kRedBlocks, prw, nrw, op->sc, op->hist, s, 1);
+    TCA_TRY(op->transport->allreduce(&op->sc->red[3], 2, s));   // gamma and delta together
+    launch_cgsr_finalize(which, op->part, kRedBlocks, prw, nrw, op->sc, op->hist, s, 2);
+    return TCA_OK;
+}
+
+// One iteration of Fig. 2 (op->solver == 0), of its preconditioned form
+// (1: Z := P^-1 R, rho := R+*Z, P := Z + beta P) or of the single-reduction
+// rearrangement (2, reading Z24).
 template <typename T>
 static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
 {
     T *r = (T *)op->r, *pe = (T *)op->p, *p = (T *)op->p_own, *q = (T *)op->q;
     const int32_t *done = &op->sc->done;
+    if (op->solver == 2) {   // P := R + beta P, S := W + beta S, C += alpha P, R -= alpha S, R+*R
+        launch_cgsr_update<T>(x, (T *)op->r, (T *)op->sr_s, (T *)op->p_own, (const T *)op->q, op->N, op->sc,
+                              op->part, s);
+        TCA_TRY(halo_p(op, s));                                         // ghost slabs of R
+        return cgsr_apply_reduce<T>(op, 6, s);                          // W := A*R; gamma, delta, alpha, beta
+    }
     static const bool no_fused_dot = getenv("TCA_NO_FUSED_DOT") != nullptr;   // measurement switch
     if (fused_used(op, pe, q) && !no_fused_dot) {
         TCA_TRY(timed_apply(op, pe, q, done, s, op->part));           // Q := A*(P*D), P+*Q in the epilogue
@@ -513,7 +549,7 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
     launch_cg_update_r<T>(r, q, op->N, op->sc, op->part, s);         // R := R - alpha*Q, R+*R
     TCA_TRY(cg_reduce(op, 2, op->part, kRedBlocks, s));              // rho1 (PCG: R+*R), stop, beta
     const T *d = r;
-    if (op->pcg_mode) {
+    if (op->solver == 1) {
         T *z = (T *)op->z;
         TCA_TRY(apply_precond<T>(op, r, z, done, s));                // Z := P^-1 R
         launch_dot_partials<T>(r, z, op->N, op->part, done, s);      // R+*Z
@@ -582,13 +618,13 @@ static tca_status cg_graph_loop(tca_operator *op, T *x, double rtol, int32_t max
     // with timing, two instances alternate: instance g's events are read while
     // the other instance is queued behind it, so the GPU never drains
     const int ng = op->timing ? 2 : 1;
-    if (!op->gexec[0] || op->gx != (const void *)x || op->gtimed != op->timing || op->gpcg != op->pcg_mode) {
+    if (!op->gexec[0] || op->gx != (const void *)x || op->gtimed != op->timing || op->gsolver != op->solver) {
         TCA_TRY(harvest_timing(op));
         destroy_graphs(op);
         for (int g = 0; g < ng; ++g) TCA_TRY(capture_chunk<T>(op, x, g));
         op->gx = x;
         op->gtimed = op->timing;
-        op->gpcg = op->pcg_mode;
+        op->gsolver = op->solver;
     }
     TCA_CUDA_TRY(cudaEventRecord(op->gfork, s));
     TCA_CUDA_TRY(cudaStreamWaitEvent(op->gstream, op->gfork, 0));
@@ -621,14 +657,23 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     CgScalars h{};
     h.rtol2 = rtol > 0.0 ? rtol * rtol : 0.0;
     h.max_iters = max_iters;
-    h.pcg = pcg;
-    op->pcg_mode = pcg;
+    h.pcg = pcg == 1;
+    op->solver = pcg;
     *op->sc_host = h;
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
     TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
-    launch_cg_init<T>(b, x, (T *)op->r, (T *)op->p_own, op->N, op->part, s);   // C := 0, R := B, P := R
-    TCA_TRY(cg_reduce(op, 0, op->part, kRedBlocks, s));                       // rho0 := R+*R
-    if (pcg) {   // Z := P^-1 R, P := Z, rho := R+*Z
+    if (pcg == 2) {   // single-reduction CG: R := B (ghosted), C := 0, P := 0, S := 0, W := A*R
+        if (!op->sr_s) TCA_CUDA_TRY(cudaMallocAsync(&op->sr_s, (size_t)op->N * op->esize, s));
+        launch_cg_init<T>(b, x, (T *)op->p_own, (T *)op->r, op->N, op->part, s);   // gamma0 partials
+        TCA_CUDA_TRY(cudaMemsetAsync(op->r, 0, (size_t)op->N * op->esize, s));
+        TCA_CUDA_TRY(cudaMemsetAsync(op->sr_s, 0, (size_t)op->N * op->esize, s));
+        TCA_TRY(halo_p(op, s));
+        TCA_TRY(cgsr_apply_reduce<T>(op, 7, s));
+    } else {
+        launch_cg_init<T>(b, x, (T *)op->r, (T *)op->p_own, op->N, op->part, s);   // C := 0, R := B, P := R
+        TCA_TRY(cg_reduce(op, 0, op->part, kRedBlocks, s));                       // rho0 := R+*R
+    }
+    if (pcg == 1) {   // Z := P^-1 R, P := Z, rho := R+*Z
         T *z = (T *)op->z;
         TCA_TRY(apply_precond<T>(op, (const T *)op->r, z, &op->sc->done, s));
         TCA_CUDA_TRY(cudaMemcpyAsync(op->p_own, z, (size_t)op->N * op->esize, cudaMemcpyDeviceToDevice, s));
@@ -727,7 +772,7 @@ void tca_operator_destroy(tca_operator *op)
     if (op->gjoin) cudaEventDestroy(op->gjoin);
     // every stream that used the operator is done before its memory goes back
     cudaDeviceSynchronize();
-    void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp};   // stream-ordered pool
+    void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp, op->sr_s};   // stream-ordered pool
     for (void *b : pooled)
         if (b) cudaFreeAsync(b, 0);
     dev_put(op->part, sizeof(double) * kRedBlocks * 2);
@@ -1043,7 +1088,7 @@ static tca_status solve_common(tca_operator *op, const void *b, void *x, double 
         TCA_CUDA_TRY(dev_get((void **)&op->hist, sizeof(double) * (max_iters + 1)));
         op->hist_cap = max_iters + 1;
     }
-    if (pcg) {
+    if (pcg == 1) {
         if (op->nranks > 1)
             return fail(TCA_ERR_INVALID_ARG, "tca_pcg_solve: the mode-1 factor solve crosses shards (not available on a "
                                              "sharded operator)");
@@ -1064,6 +1109,12 @@ tca_status tca_pcg_solve(tca_operator *op, const void *b, void *x, double rtol, 
                          tca_cg_report *rep, void *stream)
 {
     return solve_common(op, b, x, rtol, max_iters, rep, stream, 1);
+}
+
+tca_status tca_cgsr_solve(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
+                          tca_cg_report *rep, void *stream)
+{
+    return solve_common(op, b, x, rtol, max_iters, rep, stream, 2);
 }
 
 tca_status tca_precond_apply(tca_operator *op, const void *r, void *z, void *stream)

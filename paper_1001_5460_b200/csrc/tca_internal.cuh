@@ -134,6 +134,7 @@ struct tca_operator {
     tca::BandMat pc_inv[tca::kD];                // dense factors: F_d^-1 (dense mode product)
     void *z = nullptr;                           // PCG workspace z = P^-1 r
     void *pc_tmp = nullptr;                      // scratch of the dense-factor mode products
+    void *sr_s = nullptr;                        // single-reduction CG: S = A P (lazy)
     // generic compressed-band forms
     tca::BandMat Gm[tca::kD], Rm[tca::kD], At[tca::kD], Af[tca::kD];
 
@@ -172,8 +173,8 @@ struct tca_operator {
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     const void *gx = nullptr;
     int gtimed = 0;                      // the instances were captured with timing events
-    int gpcg = 0;                        // ... for the preconditioned iteration
-    int pcg_mode = 0;                    // iteration being run/captured: 0 CG (Fig. 2), 1 PCG
+    int gsolver = 0;                     // ... for this solver's iteration
+    int solver = 0;                      // iteration being run/captured: 0 CG (Fig. 2), 1 PCG, 2 single-reduction CG
     int64_t gkernels[2] = {0, 0};        // kernel launches captured in instance g (added per replay)
     bool gpend[2] = {false, false};      // instance g has launched and its events are unharvested
     std::vector<cudaEvent_t> gev[2];     // captured (external) event pairs of instance g
@@ -219,6 +220,12 @@ void *pinned_get(size_t bytes);
 cudaError_t dev_get(void **p, size_t bytes);
 void dev_put(void *p, size_t bytes);
 void pinned_put(void *p, size_t bytes);
+// single-reduction CG (tca_kernels.cu)
+template <typename T>
+void launch_cgsr_update(T *x, T *p, T *sv, T *r, const T *w, int64_t N, const CgScalars *sc, double *part,
+                        cudaStream_t s);
+void launch_cgsr_finalize(int which, const double *prr, int nrr, const double *prw, int nrw, CgScalars *sc,
+                          double *hist, cudaStream_t s, int stage = 0);
 // banded PCG factor solve along mode d (tca_precond.cu); src may equal dst
 template <typename T>
 tca_status launch_precond_sweep(const tca_operator *op, int d, const T *src, T *dst, int64_t outer, int64_t inner,

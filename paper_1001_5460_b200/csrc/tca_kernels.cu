@@ -460,6 +460,62 @@ cg_update_xp_kernel(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ 
     }
 }
 
+// Single-reduction CG (Chronopoulos-Gear, reading Z24): one
+// streaming pass per iteration before the apply,
+//   P := R + beta*P;  S := W + beta*S;  C := C + alpha*P;  R := R - alpha*S
+// with the R+*R partials of the new R (9 words per unknown; the apply then
+// reads R and produces W = A*R and R+*W: one reduction point per iteration).
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+cgsr_update_kernel(T *__restrict__ x, T *__restrict__ p, T *__restrict__ sv, T *__restrict__ r,
+                   const T *__restrict__ w, int64_t N, const CgScalars *sc, double *part)
+{
+    if (sc->done) return;
+    using V = typename Vec<T>::V;
+    constexpr int VW = Vec<T>::W;
+    const T alpha = (T)sc->alpha, beta = (T)sc->beta;
+    double acc = 0.0;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    int64_t nv = 0;
+    if (aligned16(x) && aligned16(p) && aligned16(sv) && aligned16(r) && aligned16(w)) {
+        nv = N / VW;
+        V *xv = reinterpret_cast<V *>(x), *pv = reinterpret_cast<V *>(p), *svv = reinterpret_cast<V *>(sv),
+          *rv = reinterpret_cast<V *>(r);
+        const V *wv = reinterpret_cast<const V *>(w);
+        for (int64_t i = tid; i < nv; i += nth) {
+            const V ri = __ldcs(rv + i);
+            const V pn = vaxpy(ri, beta, __ldcs(pv + i));                // P := R + beta*P
+            const V sn = vaxpy(__ldcs(wv + i), beta, __ldcs(svv + i));   // S := W + beta*S
+            __stcs(pv + i, pn);
+            __stcs(svv + i, sn);
+            __stcs(xv + i, vaxpy(__ldcs(xv + i), alpha, pn));           // C := C + alpha*P
+            const V rn = vaxpy(ri, -alpha, sn);                          // R := R - alpha*S
+            __stcs(rv + i, rn);
+            acc += vdot(rn, rn);
+        }
+    }
+    for (int64_t i = nv * VW + tid; i < N; i += nth) {
+        const T pn = r[i] + beta * p[i];
+        const T sn = w[i] + beta * sv[i];
+        p[i] = pn;
+        sv[i] = sn;
+        x[i] = x[i] + alpha * pn;
+        const T rn = r[i] - alpha * sn;
+        r[i] = rn;
+        acc += (double)rn * (double)rn;
+    }
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+template <typename T>
+void launch_cgsr_update(T *x, T *p, T *sv, T *r, const T *w, int64_t N, const CgScalars *sc, double *part,
+                        cudaStream_t s)
+{
+    count_launch();
+    cgsr_update_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(x, p, sv, r, w, N, sc, part);
+}
+
 template <typename T>
 void launch_cg_init(const T *b, T *x, T *r, T *p, int64_t N, double *part, cudaStream_t s)
 {
@@ -494,7 +550,7 @@ void launch_cg_update_xp(T *x, T *p, const T *r, int64_t N, const CgScalars *sc,
 __global__ void __launch_bounds__(kRedThreads)
 cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgScalars *sc, double *hist, int stage)
 {
-    if (which != 0 && sc->done) {
+    if (which != 0 && which != 7 && sc->done) {
         // stopped in an earlier iteration: this iteration's x update is void
         if (which == 1 && stage != 1 && threadIdx.x == 0) sc->xupd = 0;
         return;
@@ -564,6 +620,82 @@ cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgSca
     }
 }
 
+// Single-reduction CG finaliser: gamma = R+*R (update-kernel partials) and
+// delta = R+*W (apply partials) in one step; which = 7 starts the solve (R = B,
+// W = A*B), which = 6 closes an iteration.  Stage 1 leaves the two local sums
+// in red[3], red[4] for ONE all-reduce of two fp64 values; stage 2 finishes.
+__global__ void __launch_bounds__(kRedThreads)
+cgsr_finalize_kernel(int which, const double *__restrict__ prr, int nrr, const double *__restrict__ prw, int nrw,
+                     CgScalars *sc, double *hist, int stage)
+{
+    if (which == 6 && sc->done) return;
+    double g = 0.0, dl = 0.0;
+    if (stage != 2) {
+        double a = 0.0, b = 0.0;
+        for (int i = threadIdx.x; i < nrr; i += kRedThreads) a += prr[i];
+        g = block_sum(a);
+        __syncthreads();
+        for (int i = threadIdx.x; i < nrw; i += kRedThreads) b += prw[i];
+        dl = block_sum(b);
+        if (threadIdx.x != 0) return;
+        if (stage == 1) {
+            sc->red[3] = g;
+            sc->red[4] = dl;
+            return;
+        }
+    } else {
+        if (threadIdx.x != 0) return;
+        g = sc->red[3];
+        dl = sc->red[4];
+    }
+    if (which == 7) {   // gamma0 = <b, b>, delta0 = <b, A b>
+        sc->rho = g;
+        sc->rho0 = g;
+        sc->rr = g;
+        sc->iters = 0;
+        sc->converged = 0;
+        sc->status = TCA_OK;
+        sc->done = 0;
+        sc->xupd = 0;
+        sc->beta = 0.0;
+        if (hist) hist[0] = g;
+        if (!isfinite(g)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
+        if (g == 0.0) { sc->converged = 1; sc->done = 1; return; }
+        if (sc->max_iters <= 0) { sc->done = 1; if (sc->rtol2 > 0.0) sc->status = TCA_NOT_CONVERGED; return; }
+        if (!isfinite(dl)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
+        if (!(dl > 0.0)) { sc->status = TCA_ERR_BREAKDOWN; sc->done = 1; return; }
+        sc->alpha = g / dl;
+        return;
+    }
+    const int k = sc->iters + 1;   // which == 6: gamma1, delta of the new R
+    sc->iters = k;
+    sc->rr = g;
+    if (hist) hist[k] = g;
+    if (!isfinite(g)) { sc->rho = g; sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
+    if (g == 0.0) { sc->rho = g; sc->converged = 1; sc->done = 1; return; }
+    if (sc->rtol2 > 0.0 && g <= sc->rtol2 * sc->rho0) { sc->rho = g; sc->converged = 1; sc->done = 1; return; }
+    if (k >= sc->max_iters) {
+        sc->rho = g;
+        sc->done = 1;
+        if (sc->rtol2 > 0.0) sc->status = TCA_NOT_CONVERGED;
+        return;
+    }
+    const double beta = g / sc->rho;
+    const double den = dl - beta * g / sc->alpha;
+    sc->rho = g;
+    if (!isfinite(den)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
+    if (!(den > 0.0)) { sc->status = TCA_ERR_BREAKDOWN; sc->done = 1; return; }
+    sc->beta = beta;
+    sc->alpha = g / den;
+}
+
+void launch_cgsr_finalize(int which, const double *prr, int nrr, const double *prw, int nrw, CgScalars *sc,
+                          double *hist, cudaStream_t s, int stage)
+{
+    count_launch();
+    cgsr_finalize_kernel<<<1, stage == 2 ? 32 : kRedThreads, 0, s>>>(which, prr, nrr, prw, nrw, sc, hist, stage);
+}
+
 void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc, double *hist,
                         cudaStream_t s, int stage)
 {
@@ -585,7 +717,9 @@ void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc
     template void launch_cg_update_r<T>(T *, const T *, int64_t, const CgScalars *,       \
                                         double *, cudaStream_t);                          \
     template void launch_cg_update_xp<T>(T *, T *, const T *, int64_t, const CgScalars *, \
-                                         cudaStream_t);
+                                         cudaStream_t);                                   \
+    template void launch_cgsr_update<T>(T *, T *, T *, T *, const T *, int64_t,            \
+                                        const CgScalars *, double *, cudaStream_t);
 
 TCA_INST(double)
 TCA_INST(float)

@@ -31,7 +31,8 @@ EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
             "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches",
             "tca_operator_apply_path", "tca_shard_layout", "tca_nccl_get_unique_id",
             "tca_nccl_comm_create", "tca_nccl_comm_destroy", "tca_local_group_create",
-            "tca_local_group_destroy", "tca_pcg_solve", "tca_precond_apply", "tca_precond_info"]
+            "tca_local_group_destroy", "tca_pcg_solve", "tca_precond_apply", "tca_precond_info",
+            "tca_cgsr_solve"]
 
 _vp = ctypes.c_void_p
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -94,6 +95,7 @@ _lib.tca_local_group_destroy.restype = None
 _lib.tca_operator_apply_path.argtypes = [_vp]
 _lib.tca_pcg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
 _lib.tca_precond_apply.argtypes = [_vp, _vp, _vp, _vp]
+_lib.tca_cgsr_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
 _lib.tca_precond_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), _vp]
 _lib.tca_operator_apply_path.restype = ctypes.c_int
 for _name in ("tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
@@ -271,6 +273,11 @@ class Operator:
                   raise_on=("breakdown", "nonfinite")):
         """CG preconditioned with the Kronecker-factor P (tca_pcg_solve).  Returns (x, report dict)."""
         return self._solve(_lib.tca_pcg_solve, "tca_pcg_solve", b, x, rtol, max_iters, history, stream, raise_on)
+
+    def cgsr_solve(self, b, x=None, rtol=0.0, max_iters=100, history=False, stream=None,
+                   raise_on=("breakdown", "nonfinite")):
+        """Single-reduction (Chronopoulos-Gear) CG (tca_cgsr_solve).  Returns (x, report dict)."""
+        return self._solve(_lib.tca_cgsr_solve, "tca_cgsr_solve", b, x, rtol, max_iters, history, stream, raise_on)
 
     def _solve(self, fn, name, b, x, rtol, max_iters, history, stream, raise_on):
         if x is None:
