@@ -79,6 +79,8 @@ def lib():
             L.orc_pcg.restype = ctypes.c_int
             L.orc_cgsr.argtypes = L.orc_cg.argtypes
             L.orc_cgsr.restype = ctypes.c_int
+            L.orc_jacobi.argtypes = L.orc_cg.argtypes
+            L.orc_jacobi.restype = ctypes.c_int
             _lib = L
     return _lib
 
@@ -153,6 +155,26 @@ class Operator:
         self._R = _ptr_array(self.R)
         self._A = _ptr_array(self.A)
 
+    @classmethod
+    def from_gram(cls, G, R, lam):
+        """Operator given by its factors: M = (kron_d G_d) + lam sum_d (mode-d R_d).
+        G None: no Kronecker-product term (Eq. 9's separable Poisson form); R a list
+        of n_d x n_d matrices (None entries: no term for that mode)."""
+        self = cls.__new__(cls)
+        self.D = len(R)
+        self.n = tuple(r.shape[0] for r in R)
+        self.m = self.n
+        self.lam = float(lam)
+        self.G = [_f64(g) for g in G] if G is not None else [None] * self.D
+        self.R = [None if r is None else _f64(r) for r in R]
+        self.A = [np.eye(k) for k in self.n]
+        self._na, self._np = _i64(self.n)
+        self._ma, self._mp = _i64(self.m)
+        self._G = _ptr_array(self.G)
+        self._R = _ptr_array(self.R)
+        self._A = _ptr_array(self.A)
+        return self
+
     @property
     def N(self):
         return int(np.prod(self.n))
@@ -205,6 +227,18 @@ class Operator:
         st = lib().orc_cgsr(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(x),
                             float(rtol), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
         return x, it.value, st, hist[: it.value + 1]
+
+    def jacobi(self, b, threshold: float, max_iters: int):
+        """Tensor Jacobi (Fig. 1) from U = 0, stopping when R+*R <= threshold.
+        Returns (u, iters, status, rr_history)."""
+        b = _f64(b).reshape(self.n)
+        u = np.empty(self.n)
+        hist = np.zeros(max_iters + 1)
+        it = ctypes.c_int(0)
+        rf = ctypes.c_double(0.0)
+        st = lib().orc_jacobi(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(u),
+                              float(threshold), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
+        return u, it.value, st, hist[: it.value + 1]
 
     # ---- Kronecker-factor preconditioner (DESIGN.md reading Z22)
     def precond_factors(self):

@@ -124,7 +124,8 @@ static int64_t prod(const int64_t *n, int D)
  * y = (G_1 x ... x G_D) x + lam * sum_d x x_d R_d.
  * Kronecker term: successive mode products in mode order 1..D (Eq. 4);
  * regulariser: one mode product per mode, summed in mode order (Eq. 9).
- * R may be NULL (lam ignored) or hold NULL entries (that mode has no term).
+ * R may be NULL (lam ignored) or hold NULL entries (that mode has no term);
+ * G with NULL entries means no Kronecker-product term (Eq. 9).
  */
 void orc_apply(int D, const int64_t *n, const double *const *G,
                const double *const *R, double lam, const double *x, double *y)
@@ -132,10 +133,16 @@ void orc_apply(int D, const int64_t *n, const double *const *G,
     int64_t N = prod(n, D);
     double *t0 = (double *)malloc(sizeof(double) * N);
     double *t1 = (double *)malloc(sizeof(double) * N);
-    memcpy(t0, x, sizeof(double) * N);
-    for (int d = 0; d < D; d++) {
-        orc_mode_product(D, n, t0, d, n[d], G[d], t1);
-        double *sw = t0; t0 = t1; t1 = sw;
+    int have_g = G != NULL;
+    for (int d = 0; d < D && have_g; d++) have_g = G[d] != NULL;
+    if (have_g) {
+        memcpy(t0, x, sizeof(double) * N);
+        for (int d = 0; d < D; d++) {
+            orc_mode_product(D, n, t0, d, n[d], G[d], t1);
+            double *sw = t0; t0 = t1; t1 = sw;
+        }
+    } else {   /* no Kronecker-product term (Eq. 9's separable Poisson form) */
+        memset(t0, 0, sizeof(double) * N);
     }
     /* t0 = Kronecker term */
     double *reg = (double *)calloc(N, sizeof(double));
@@ -605,5 +612,59 @@ int orc_cgsr(int D, const int64_t *n, const double *const *G,
     free(w);
     free(p);
     free(s);
+    return status;
+}
+
+/* ------------------------------------------------------------------------
+ * Tensor Jacobi (Fig. 1a/1b), step by step:
+ *   E := InvMainDiag(A);  R := A*U - B;  WHILE R+*R > threshold DO
+ *   U := U - R*E;  R := A*U - B;  END
+ * with U = 0 initially (reading Z26) and at most max_iters updates.  The main
+ * diagonal of A = (G_1 x .. x G_D) + lam sum_d (mode-d R_d) is
+ *   diag[i] = prod_d G_d[i_d, i_d] + lam sum_d R_d[i_d, i_d]
+ * (G may hold NULL entries: no Kronecker-product term, Eq. 9's Poisson form).
+ * hist (>= max_iters + 1): R+*R at every evaluation.  Returns ORC_OK when
+ * R+*R <= threshold, ORC_NOT_CONVERGED after max_iters updates.
+ * ---------------------------------------------------------------------- */
+int orc_jacobi(int D, const int64_t *n, const double *const *G, const double *const *R, double lam,
+               const double *b, double *u, double threshold, int max_iters, double *hist, int *iters,
+               double *rr_final)
+{
+    int64_t N = prod(n, D);
+    double *e = (double *)malloc(sizeof(double) * N);
+    double *r = (double *)malloc(sizeof(double) * N);
+    int status = ORC_OK;
+    int have_g = 1;
+    for (int d = 0; d < D; d++) have_g = have_g && G && G[d];
+    for (int64_t i = 0; i < N; i++) {          /* E := InvMainDiag(A) */
+        int64_t rem = i, idx[8];
+        for (int d = D - 1; d >= 0; d--) { idx[d] = rem % n[d]; rem /= n[d]; }
+        double pk = have_g ? 1.0 : 0.0, sm = 0.0;
+        for (int d = 0; d < D; d++) {
+            if (have_g) pk *= G[d][idx[d] * n[d] + idx[d]];
+            if (R && R[d]) sm += R[d][idx[d] * n[d] + idx[d]];
+        }
+        e[i] = 1.0 / (pk + lam * sm);
+    }
+    memset(u, 0, sizeof(double) * N);
+    orc_apply(D, n, G, R, lam, u, r);           /* R := A*U - B */
+    for (int64_t i = 0; i < N; i++) r[i] -= b[i];
+    double rho = orc_dot(N, r, r);
+    if (hist) hist[0] = rho;
+    int k = 0;
+    while (rho > threshold) {                   /* WHILE R+*R > threshold */
+        if (!isfinite(rho)) { status = ORC_NONFINITE; break; }
+        if (k == max_iters) { status = ORC_NOT_CONVERGED; break; }
+        for (int64_t i = 0; i < N; i++) u[i] -= r[i] * e[i];   /* U := U - R*E */
+        orc_apply(D, n, G, R, lam, u, r);                        /* R := A*U - B */
+        for (int64_t i = 0; i < N; i++) r[i] -= b[i];
+        rho = orc_dot(N, r, r);
+        k++;
+        if (hist) hist[k] = rho;
+    }
+    *iters = k;
+    if (rr_final) *rr_final = rho;
+    free(e);
+    free(r);
     return status;
 }

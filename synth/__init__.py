@@ -140,6 +140,21 @@ def second_difference(n: int) -> np.ndarray:
     return L
 
 
+def laplacian_1d(n: int) -> np.ndarray:
+    """One-dimensional second-order finite-difference factor of the separable
+    Poisson operator (Eq. 9; reading Z25): tridiag(-1, 2, -1)
+    with homogeneous Dirichlet ends (the truncated band, Z15), grid step 1."""
+    T = 2.0 * np.eye(n)
+    i = np.arange(n - 1)
+    T[i, i + 1] = -1.0
+    T[i + 1, i] = -1.0
+    return T
+
+
+# Fig. 1c's Poisson workload shape (PAPER.md:153-156): X 128, Y 129, Z 130
+POISSON_SHAPE = (128, 129, 130)
+
+
 # --------------------------------------------------------------------------
 # BASELINE.json configs
 # --------------------------------------------------------------------------

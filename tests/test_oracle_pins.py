@@ -497,3 +497,59 @@ def test_P14_cgsr_iterates_match_fig2_cg_to_rounding(cfg_index):
         xb, _, _, hb = op.cgsr(b, rtol=0.0, max_iters=k)
         assert np.linalg.norm(xa - xb) <= 1e-10 * np.linalg.norm(xa)
         assert np.max(np.abs(ha - hb) / ha) <= 1e-9
+
+
+# ---------------------------------------------------------------- P15: separable Poisson + tensor Jacobi (Z25, Z26)
+def dense_poisson(n):
+    """sum_d I..T_d..I with numpy kron (independent of the oracle)."""
+    T = [synth.laplacian_1d(k) for k in n]
+    K = 0
+    for d in range(len(n)):
+        P = np.ones((1, 1))
+        for e in range(len(n)):
+            P = np.kron(P, T[e] if e == d else np.eye(n[e]))
+        K = K + P
+    return K
+
+
+@pytest.mark.parametrize("n", [(5, 6, 7), (4, 3, 5, 2), (9,)])
+def test_P15_poisson_apply_equals_dense_kronecker_sum(n):
+    o = oracle.Operator.from_gram(None, [synth.laplacian_1d(k) for k in n], 1.0)
+    x = synth.random_tensor(n, seed=31)
+    ref = dense_poisson(n) @ x.ravel()
+    assert np.linalg.norm(o.apply(x).ravel() - ref) <= 1e-14 * np.linalg.norm(ref)
+
+
+def test_P15_poisson_textbook_spectrum():
+    """Eigen-tensors of the Dirichlet Laplacian: prod_d sin(k_d pi (i_d+1)/(n_d+1))
+    with eigenvalue sum_d (2 - 2 cos(k_d pi / (n_d+1)))."""
+    n = (7, 6, 9)
+    o = oracle.Operator.from_gram(None, [synth.laplacian_1d(k) for k in n], 1.0)
+    for ks in [(1, 1, 1), (3, 5, 2), (7, 6, 9)]:
+        vs = [np.sin(k * np.pi * (np.arange(nd) + 1) / (nd + 1)) for k, nd in zip(ks, n)]
+        lam = sum(2 - 2 * np.cos(k * np.pi / (nd + 1)) for k, nd in zip(ks, n))
+        x = np.multiply.outer(np.multiply.outer(vs[0], vs[1]), vs[2])
+        assert np.allclose(o.apply(x), lam * x, atol=1e-13 * lam)
+
+
+@pytest.mark.parametrize("n", [(5, 6, 7), (4, 3, 5, 2)])
+def test_P15_jacobi_steps_and_solution(n):
+    """Fig. 1: U_{k+1} = U_k - (K U_k - b) / diag(K) (numpy, first steps) and the
+    converged U equals the dense solve; the residual history is R+*R."""
+    K = dense_poisson(n)
+    o = oracle.Operator.from_gram(None, [synth.laplacian_1d(k) for k in n], 1.0)
+    b = synth.random_tensor(n, seed=32).ravel()
+    u = np.zeros_like(b)
+    hist = []
+    for _ in range(3):
+        r = K @ u - b
+        hist.append(r @ r)
+        u = u - r / np.diag(K)
+    uo, k, st, h = o.jacobi(b.reshape(n), threshold=0.0, max_iters=3)
+    assert st == oracle.NOT_CONVERGED and k == 3
+    assert np.linalg.norm(uo.ravel() - u) <= 1e-14 * np.linalg.norm(u)
+    assert np.allclose(h[:3], hist, rtol=1e-13)
+    uo, k, st, h = o.jacobi(b.reshape(n), threshold=1e-24, max_iters=50000)
+    ref = np.linalg.solve(K, b)
+    assert st == oracle.OK and h[-1] <= 1e-24
+    assert np.linalg.norm(uo.ravel() - ref) <= 1e-9 * np.linalg.norm(ref)
