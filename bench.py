@@ -47,10 +47,13 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--solver", default="cg", choices=["cg", "pcg", "cgsr"],
+    ap.add_argument("--solver", default="cg", choices=["cg", "pcg", "cgsr", "jacobi"],
                     help="pcg: CG with the Kronecker-factor preconditioner (tca_pcg_solve); "
                          "cgsr: single-reduction CG (tca_cgsr_solve)")
     ap.add_argument("--rtol", type=float, default=None, help="override the config's stop rule")
+    ap.add_argument("--workload", default="fit", choices=["fit", "poisson"],
+                    help="poisson: Fig. 1c's separable Poisson system 128x129x130 (Eq. 9) with tensor "
+                         "Jacobi (--solver jacobi, threshold --rtol, default 1e-4) or CG")
     return ap.parse_args()
 
 
@@ -435,10 +438,80 @@ def run_tca(args):
     return 0
 
 
+def run_poisson(args):
+    """Fig. 1c workload: the separable Poisson operator of
+    Eq. 9 on a 128x129x130 grid, tensor Jacobi to R+*R <= 1e-4 (or CG), from a
+    seeded N(0,1) right-hand side (rhs.dat is not available; reading Z25).  One
+    GPU; a step = create + solve + destroy."""
+    import torch
+    from paper_1001_5460_b200 import tca
+    n = synth.POISSON_SHAPE
+    T = [synth.laplacian_1d(k) for k in n]
+    dtype = args.dtype
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    b = torch.empty(n, dtype=tdt, device="cuda")
+    tca.generate_normal(b, seed=1, stream_id=9)
+    solver = args.solver if args.solver in ("jacobi", "cg", "cgsr") else "jacobi"
+    thr = args.rtol if args.rtol is not None else (1e-4 if solver == "jacobi" else 1e-10)
+    iters = args.iters or (200000 if solver == "jacobi" else 5000)
+    stream = torch.cuda.current_stream()
+    state = {}
+
+    def step(timing=False):
+        op = tca.Operator.from_gram(None, T, 1.0, dtype=dtype)
+        if timing:
+            op.set_timing(True)
+        fn = {"jacobi": op.jacobi_solve, "cg": op.cg_solve, "cgsr": op.cgsr_solve}[solver]
+        kw = {"threshold": thr} if solver == "jacobi" else {"rtol": thr}
+        x, rep = fn(b, max_iters=iters, **kw)
+        if timing:
+            ms, cnt = op.get_timing()
+            state["apply_ms"] = state.get("apply_ms", 0.0) + ms
+            state["apply_cnt"] = state.get("apply_cnt", 0) + cnt
+        state["iters"] = state.get("iters", 0) + rep["iterations"]
+        state["rep"] = rep
+        state["path"] = op.apply_path
+        op.close()
+
+    for _ in range(args.warmup):
+        step()
+    state.clear()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(timing=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    esize = 8 if dtype == "f64" else 4
+    N = int(np.prod(n))
+    apply_us = 1e3 * state["apply_ms"] / max(1, state["apply_cnt"])
+    hbm, src = peaks()
+    rep = state["rep"]
+    line = {"metric": f"{solver} iterations/s, Fig. 1c separable Poisson", "value": state["iters"] / (ms * 1e-3),
+            "unit": "iters/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "time_to_solution_ms": ms / args.steps, "higher_is_better": True,
+            "dtype": dtype, "data": "synthetic right-hand side N(0,1), seed 1 (rhs.dat not available)",
+            "config": {"workload": "Fig. 1c: 128x129x130 separable Poisson (Eq. 9), tridiag(-1,2,-1) factors",
+                       "solver": solver, "stop": (f"R+*R <= {thr:g}" if solver == "jacobi" else f"rtol {thr:g}"),
+                       "unknowns": N},
+            "roofline": {"bound": "hbm", "achieved": 2 * N * esize / (apply_us * 1e-6) / 1e9, "peak": hbm,
+                         "unit": "GB/s", "frac": 2 * N * esize / (apply_us * 1e-6) / 1e9 / hbm,
+                         "us_per_launch": apply_us, "peak_source": src},
+            "report": {"iterations": rep["iterations"], "converged": rep["converged"], "rho0": rep["rho0"],
+                       "rho_final": rep["rho_final"]},
+            "apply_path": state["path"]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "poisson":
+        return run_poisson(args)
     return run_tca(args)
 
 

@@ -125,6 +125,22 @@ tca_status tca_operator_create(tca_operator **op, int order, const int64_t *n,
                                void *stream);
 
 /*
+ * Create the operator from its factors instead of A_d, L_d:
+ *   M = (G_1 (x) ... (x) G_D) + lambda sum_d (mode-d R_d)
+ * G NULL: no Kronecker-product term -- Eq. 9's separable Poisson operator
+ * sum_d (mode-d R_d), e.g. R_d the 1-D finite-difference
+ * Laplacian tridiag(-1, 2, -1) and lambda = 1 (reading Z25).  G (if given) and
+ * R: D host fp64 n_d x n_d symmetric row-major matrices (R entries may be
+ * NULL: no term for that mode); copied at create.  The operator supports
+ * tca_apply and the solvers; tca_rhs / tca_forward_model return
+ * TCA_ERR_INVALID_ARG (there is no A_d).  M must be SPD for the CG solvers.
+ */
+tca_status tca_operator_create_gram(tca_operator **op, int order, const int64_t *n,
+                                    const double *const *G, const double *const *R,
+                                    double lambda, tca_dtype dtype, const tca_dist *dist,
+                                    void *stream);
+
+/*
  * Query an operator.  Any output pointer may be NULL.
  *   own_lo/own_hi     mode-1 unknown rows held by this rank ([0,n1) on 1 GPU)
  *   data_lo/data_hi   mode-1 data rows this rank's tca_rhs reads
@@ -189,6 +205,18 @@ tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol,
  */
 tca_status tca_pcg_solve(tca_operator *op, const void *b, void *x, double rtol,
                          int32_t max_iters, tca_cg_report *rep, void *stream);
+
+/*
+ * Tensor Jacobi (Fig. 1a/1b), the paper's stationary solver:
+ *   E := inverse main diagonal of M; U := 0 (reading Z26); R := M U - B;
+ *   WHILE R+*R > threshold DO U := U - R*E; R := M U - B END
+ * threshold: absolute bound on R+*R (Fig. 1c uses 1e-4), >= 0.
+ * At most max_iters updates (status TCA_NOT_CONVERGED if the bound is not
+ * reached).  x receives U.  Report as tca_cg_solve (rho values and history are
+ * R+*R).  Single GPU only (TCA_ERR_INVALID_ARG on a sharded operator).
+ */
+tca_status tca_jacobi_solve(tca_operator *op, const void *b, void *x, double threshold,
+                            int32_t max_iters, tca_cg_report *rep, void *stream);
 
 /*
  * Single-reduction CG (reading Z24): Chronopoulos

@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstring>
 #include <string>
 #include <mutex>
 #include <vector>
@@ -298,6 +299,16 @@ static bool fused_used(const tca_operator *op, const void *x, const void *y)
 static tca_status apply_dispatch(const tca_operator *op, const void *x, void *y,
                                  const int32_t *done, cudaStream_t s, double *pq_part = nullptr)
 {
+    if (op->apply_path == 2) {   // Kronecker sum only (Eq. 9): one stencil pass
+        if (op->dtype == TCA_F64)
+            launch_ksum_apply<double>((const double *)x, (double *)y, op->N, op->n, (const double *)op->ks_taps,
+                                      op->ks_off, done, s);
+        else
+            launch_ksum_apply<float>((const float *)x, (float *)y, op->N, op->n, (const float *)op->ks_taps,
+                                     op->ks_off, done, s);
+        TCA_CUDA_TRY(cudaGetLastError());
+        return TCA_OK;
+    }
     if (fused_used(op, x, y)) return launch_fused_apply(op, x, y, done, pq_part, s);
     return apply_multipass(op, x, y, done, s);
 }
@@ -531,6 +542,13 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
 {
     T *r = (T *)op->r, *pe = (T *)op->p, *p = (T *)op->p_own, *q = (T *)op->q;
     const int32_t *done = &op->sc->done;
+    if (op->solver == 3) {   // tensor Jacobi (Fig. 1): U := U - R*E; R := A*U - B; R+*R
+        launch_jacobi_update<T>(x, (const T *)op->r, (const T *)op->jac_e, op->N, op->sc, s);
+        TCA_TRY(timed_apply(op, x, q, done, s));
+        launch_jacobi_resid<T>((T *)op->r, q, (const T *)op->jac_b, op->N, op->part, done, s);
+        launch_jacobi_finalize(1, op->part, kRedBlocks, op->sc, op->hist, s);
+        return TCA_OK;
+    }
     if (op->solver == 2) {   // P := R + beta P, S := W + beta S, C += alpha P, R -= alpha S, R+*R
         launch_cgsr_update<T>(x, (T *)op->r, (T *)op->sr_s, (T *)op->p_own, (const T *)op->q, op->N, op->sc,
                               op->part, s);
@@ -618,13 +636,15 @@ static tca_status cg_graph_loop(tca_operator *op, T *x, double rtol, int32_t max
     // with timing, two instances alternate: instance g's events are read while
     // the other instance is queued behind it, so the GPU never drains
     const int ng = op->timing ? 2 : 1;
-    if (!op->gexec[0] || op->gx != (const void *)x || op->gtimed != op->timing || op->gsolver != op->solver) {
+    if (!op->gexec[0] || op->gx != (const void *)x || op->gtimed != op->timing || op->gsolver != op->solver ||
+        op->gb != op->jac_b) {
         TCA_TRY(harvest_timing(op));
         destroy_graphs(op);
         for (int g = 0; g < ng; ++g) TCA_TRY(capture_chunk<T>(op, x, g));
         op->gx = x;
         op->gtimed = op->timing;
         op->gsolver = op->solver;
+        op->gb = op->jac_b;
     }
     TCA_CUDA_TRY(cudaEventRecord(op->gfork, s));
     TCA_CUDA_TRY(cudaStreamWaitEvent(op->gstream, op->gfork, 0));
@@ -650,6 +670,38 @@ static tca_status cg_graph_loop(tca_operator *op, T *x, double rtol, int32_t max
     return TCA_OK;
 }
 
+// E := InvMainDiag(A) once per operator (tensor Jacobi)
+template <typename T>
+static tca_status jacobi_prepare(tca_operator *op, cudaStream_t s)
+{
+    if (op->jac_e) return TCA_OK;
+    int nmax = 1;
+    for (int d = 0; d < kD; ++d) nmax = std::max(nmax, (int)op->n[d]);
+    bool have_g = true;
+    std::vector<double> dg((size_t)4 * nmax, 0.0), dr((size_t)4 * nmax, 0.0);
+    for (int d = 0; d < kD; ++d) {
+        const int nd = (int)op->n[d];
+        bool nz = false;
+        for (int i = 0; i < nd; ++i) {
+            dg[(size_t)d * nmax + i] = op->Gh[d][(size_t)i * nd + i];
+            nz = nz || op->Gh[d][(size_t)i * nd + i] != 0.0;
+            if (op->has_reg[d]) dr[(size_t)d * nmax + i] = op->Rh[d][(size_t)i * nd + i];
+        }
+        // an all-zero G_d (Gram form without a product term) makes the product term vanish
+        have_g = have_g && nz;
+    }
+    double *buf = nullptr;
+    const size_t nb = sizeof(double) * 8 * nmax;
+    TCA_CUDA_TRY(dev_get((void **)&buf, nb));
+    TCA_CUDA_TRY(cudaMemcpyAsync(buf, dg.data(), nb / 2, cudaMemcpyHostToDevice, s));
+    TCA_CUDA_TRY(cudaMemcpyAsync(buf + 4 * nmax, dr.data(), nb / 2, cudaMemcpyHostToDevice, s));
+    TCA_CUDA_TRY(cudaMallocAsync(&op->jac_e, (size_t)op->N * op->esize, s));
+    launch_jacobi_diag<T>((T *)op->jac_e, op->N, op->n, buf, buf + 4 * nmax, nmax, op->lambda, have_g, s);
+    TCA_CUDA_TRY(cudaStreamSynchronize(s));
+    dev_put(buf, nb);
+    return TCA_OK;
+}
+
 template <typename T>
 static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t max_iters,
                        tca_cg_report *rep, cudaStream_t s, int pcg = 0)
@@ -662,7 +714,17 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     *op->sc_host = h;
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
     TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
-    if (pcg == 2) {   // single-reduction CG: R := B (ghosted), C := 0, P := 0, S := 0, W := A*R
+    if (pcg == 3) {   // tensor Jacobi: U := 0, E := InvMainDiag(A), R := A*U - B
+        h.thr = rtol;
+        *op->sc_host = h;
+        TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
+        TCA_TRY(jacobi_prepare<T>(op, s));
+        op->jac_b = b;
+        TCA_CUDA_TRY(cudaMemsetAsync(x, 0, (size_t)op->N * op->esize, s));
+        TCA_TRY(timed_apply(op, x, (T *)op->q, nullptr, s));
+        launch_jacobi_resid<T>((T *)op->r, (const T *)op->q, b, op->N, op->part, nullptr, s);
+        launch_jacobi_finalize(0, op->part, kRedBlocks, op->sc, op->hist, s);
+    } else if (pcg == 2) {   // single-reduction CG: R := B (ghosted), C := 0, P := 0, S := 0, W := A*R
         if (!op->sr_s) TCA_CUDA_TRY(cudaMallocAsync(&op->sr_s, (size_t)op->N * op->esize, s));
         launch_cg_init<T>(b, x, (T *)op->p_own, (T *)op->r, op->N, op->part, s);   // gamma0 partials
         TCA_CUDA_TRY(cudaMemsetAsync(op->r, 0, (size_t)op->N * op->esize, s));
@@ -682,6 +744,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     }
     TCA_TRY(halo_p(op, s));
     static const bool no_graph = getenv("TCA_NO_GRAPH") != nullptr;   // measurement switch
+    if (pcg == 3) rtol = 1.0;   // Jacobi stops on its threshold: poll the device flag per chunk
     if (!op->transport && !no_graph && max_iters > 1) {
         TCA_TRY(cg_graph_loop<T>(op, x, rtol, max_iters, s));
     } else if (rtol <= 0.0) {
@@ -772,7 +835,8 @@ void tca_operator_destroy(tca_operator *op)
     if (op->gjoin) cudaEventDestroy(op->gjoin);
     // every stream that used the operator is done before its memory goes back
     cudaDeviceSynchronize();
-    void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp, op->sr_s};   // stream-ordered pool
+    void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp, op->sr_s,
+                      op->jac_e};   // stream-ordered pool
     for (void *b : pooled)
         if (b) cudaFreeAsync(b, 0);
     dev_put(op->part, sizeof(double) * kRedBlocks * 2);
@@ -780,6 +844,7 @@ void tca_operator_destroy(tca_operator *op)
     dev_put(op->hist, sizeof(double) * op->hist_cap);
     dev_put(op->tmap_dev, sizeof(TmapSlot::map) * kTmapSlots);
     dev_put(op->band_gtaps, op->band_gtaps_bytes);
+    dev_put(op->ks_taps, op->ks_bytes);
     for (int d = 0; d < kD; ++d) dev_put(op->pc_tab[d], op->pc_tab_bytes[d]);
     pinned_put(op->sc_host, sizeof(CgScalars));
     pinned_put(op->tmap_host, sizeof(TmapSlot::map) * kTmapSlots);
@@ -791,9 +856,11 @@ void tca_operator_destroy(tca_operator *op)
     delete op;
 }
 
-tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, const int64_t *m,
-                               const double *const *A, const double *const *L, double lambda,
-                               tca_dtype dtype, const tca_dist *dist, void *stream)
+// Gram form (tca_operator_create_gram): G_d / R_d given directly, A_d = I.
+static tca_status create_impl(tca_operator **out, int order, const int64_t *n, const int64_t *m,
+                              const double *const *A, const double *const *L, double lambda, tca_dtype dtype,
+                              const tca_dist *dist, void *stream, bool gram_form, const double *const *Gin,
+                              const double *const *Rin)
 {
     if (!out) return fail(TCA_ERR_INVALID_ARG, "op (output pointer) is NULL");
     *out = nullptr;
@@ -855,6 +922,7 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
         op->xf_hi = n[0];
     }
     op->order = order;
+    op->gram_form = gram_form;
     op->dtype = dtype;
     op->esize = dtype == TCA_F64 ? 8 : 4;
     op->lambda = lambda;
@@ -881,7 +949,25 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
     for (int d = 0; d < kD && st == TCA_OK; ++d) {
         const int nd = (int)op->n[d], md = (int)op->m[d];
         std::vector<double> G, R, Ad;
-        if (d < order) {
+        if (d < order && gram_form) {   // factors given: G_d (or none: zero), R_d (Eq. 9 Kronecker sum)
+            G.assign((size_t)nd * nd, 0.0);
+            if (Gin && Gin[d]) G.assign(Gin[d], Gin[d] + (size_t)nd * nd);
+            if (Rin && Rin[d] && lambda > 0.0) {
+                R.assign(Rin[d], Rin[d] + (size_t)nd * nd);
+                op->has_reg[d] = 1;
+                op->hbR[d] = half_bandwidth(R, nd);
+            }
+            for (int i = 0; i < nd && st == TCA_OK; ++i)
+                for (int j = 0; j < i; ++j)
+                    if (G[(size_t)i * nd + j] != G[(size_t)j * nd + i] ||
+                        (!R.empty() && R[(size_t)i * nd + j] != R[(size_t)j * nd + i])) {
+                        st = fail(TCA_ERR_INVALID_ARG, "G_" + std::to_string(d + 1) + " / R_" + std::to_string(d + 1) +
+                                                           " must be symmetric");
+                        break;
+                    }
+            if (st != TCA_OK) break;
+            Ad.assign(A[d], A[d] + (size_t)md * nd);
+        } else if (d < order) {
             G = gram(A[d], md, nd);                       // G_d = A_d^T A_d
             if (!cholesky_ok(G, nd)) {
                 st = fail(TCA_ERR_NOT_SPD, "G_" + std::to_string(d + 1) + " = A^T A is not positive definite (A lacks full column rank)");
@@ -952,6 +1038,34 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
     op->N = op->nloc1 * op->slab;
     op->Mloc = (op->data_hi - op->data_lo) * op->m[1] * op->m[2] * op->m[3];
     op->apply_path = fused_shape_supported(op) ? 1 : 0;
+    if (gram_form && !Gin && !sharded) {   // Kronecker sum only, banded R_d: the stencil path
+        bool ok = true;
+        for (int d = 0; d < kD; ++d) ok = ok && (!op->has_reg[d] || op->hbR[d] <= kHR);
+        if (ok) {
+            std::vector<double> t;
+            for (int d = 0; d < kD; ++d) {
+                op->ks_off[d] = (int)(t.size() / 5);
+                const int nd = (int)op->n[d];
+                for (int r = 0; r < nd; ++r)
+                    for (int k = -2; k <= 2; ++k) {
+                        const int c = r + k;
+                        t.push_back(op->has_reg[d] && c >= 0 && c < nd ? lambda * op->Rh[d][(size_t)r * nd + c] : 0.0);
+                    }
+            }
+            std::vector<unsigned char> raw(t.size() * op->esize);
+            if (dtype == TCA_F64) std::memcpy(raw.data(), t.data(), raw.size());
+            else
+                for (size_t i = 0; i < t.size(); ++i) reinterpret_cast<float *>(raw.data())[i] = (float)t[i];
+            cudaError_t e0 = dev_get(&op->ks_taps, raw.size());
+            if (e0 == cudaSuccess) e0 = cudaMemcpy(op->ks_taps, raw.data(), raw.size(), cudaMemcpyHostToDevice);
+            if (e0 != cudaSuccess) {
+                tca_operator_destroy(op);
+                return cuda_fail(e0, "Kronecker-sum taps");
+            }
+            op->ks_bytes = raw.size();
+            op->apply_path = 2;
+        }
+    }
     if (sharded && op->apply_path != 1) {
         tca_operator_destroy(op);
         return fail(TCA_ERR_INVALID_ARG,
@@ -990,6 +1104,37 @@ tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, 
     op->device_bytes = bytes;
     *out = op;
     return TCA_OK;
+}
+
+tca_status tca_operator_create(tca_operator **out, int order, const int64_t *n, const int64_t *m,
+                               const double *const *A, const double *const *L, double lambda,
+                               tca_dtype dtype, const tca_dist *dist, void *stream)
+{
+    return create_impl(out, order, n, m, A, L, lambda, dtype, dist, stream, false, nullptr, nullptr);
+}
+
+tca_status tca_operator_create_gram(tca_operator **out, int order, const int64_t *n, const double *const *G,
+                                    const double *const *R, double lambda, tca_dtype dtype, const tca_dist *dist,
+                                    void *stream)
+{
+    if (!out) return fail(TCA_ERR_INVALID_ARG, "op (output pointer) is NULL");
+    *out = nullptr;
+    if (order < 1 || order > 4 || !n) return fail(TCA_ERR_INVALID_ARG, "order must be in 1..4 and n non-NULL");
+    if (!G && !R) return fail(TCA_ERR_INVALID_ARG, "G and R are both NULL (empty operator)");
+    std::vector<std::vector<double>> eye((size_t)order);
+    const double *Ap[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int d = 0; d < order; ++d) {
+        if (n[d] < 1 || n[d] > 4096) return fail(TCA_ERR_SHAPE, "n[" + std::to_string(d) + "] out of range");
+        if (G && !G[d]) return fail(TCA_ERR_INVALID_ARG, "G[" + std::to_string(d) + "] is NULL (give all or none)");
+        if (G && !all_finite(G[d], (size_t)(n[d] * n[d])))
+            return fail(TCA_ERR_INVALID_ARG, "G[" + std::to_string(d) + "] has non-finite entries");
+        if (R && R[d] && !all_finite(R[d], (size_t)(n[d] * n[d])))
+            return fail(TCA_ERR_INVALID_ARG, "R[" + std::to_string(d) + "] has non-finite entries");
+        eye[d].assign((size_t)(n[d] * n[d]), 0.0);
+        for (int64_t i = 0; i < n[d]; ++i) eye[d][(size_t)(i * n[d] + i)] = 1.0;
+        Ap[d] = eye[d].data();
+    }
+    return create_impl(out, order, n, n, Ap, nullptr, lambda, dtype, dist, stream, true, G, R);
 }
 
 tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo, int64_t *own_hi,
@@ -1062,6 +1207,7 @@ int64_t tca_kernel_launches(void) { return g_launches.load(); }
 tca_status tca_rhs(const tca_operator *op, const void *ydata, void *b, void *stream)
 {
     TCA_TRY(check_op(op));
+    if (op->gram_form) return fail(TCA_ERR_INVALID_ARG, "tca_rhs: operator was created from its factors (no A_d)");
     if (!ydata || !b) return fail(TCA_ERR_INVALID_ARG, "ydata and b must be non-NULL device pointers");
     cudaStream_t s = (cudaStream_t)stream;
     if (op->dtype == TCA_F64) TCA_TRY(rhs_t<double>(op, (const double *)ydata, (double *)b, s));
@@ -1088,6 +1234,9 @@ static tca_status solve_common(tca_operator *op, const void *b, void *x, double 
         TCA_CUDA_TRY(dev_get((void **)&op->hist, sizeof(double) * (max_iters + 1)));
         op->hist_cap = max_iters + 1;
     }
+    if (pcg == 3 && (op->nranks > 1 || op->transport))
+        return fail(TCA_ERR_INVALID_ARG, "tca_jacobi_solve: not available on a sharded operator");
+    if (pcg == 3 && rtol < 0.0) return fail(TCA_ERR_INVALID_ARG, "tca_jacobi_solve: threshold must be >= 0");
     if (pcg == 1) {
         if (op->nranks > 1)
             return fail(TCA_ERR_INVALID_ARG, "tca_pcg_solve: the mode-1 factor solve crosses shards (not available on a "
@@ -1109,6 +1258,12 @@ tca_status tca_pcg_solve(tca_operator *op, const void *b, void *x, double rtol, 
                          tca_cg_report *rep, void *stream)
 {
     return solve_common(op, b, x, rtol, max_iters, rep, stream, 1);
+}
+
+tca_status tca_jacobi_solve(tca_operator *op, const void *b, void *x, double threshold, int32_t max_iters,
+                            tca_cg_report *rep, void *stream)
+{
+    return solve_common(op, b, x, threshold, max_iters, rep, stream, 3);
 }
 
 tca_status tca_cgsr_solve(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
@@ -1184,6 +1339,7 @@ tca_status tca_forward_model(const tca_operator *op, const void *x, void *ydata,
                              uint64_t seed, void *stream)
 {
     TCA_TRY(check_op(op));
+    if (op->gram_form) return fail(TCA_ERR_INVALID_ARG, "tca_forward_model: operator was created from its factors");
     if (!ydata) return fail(TCA_ERR_INVALID_ARG, "ydata is NULL");
     if (op->nranks > 1 && x) return fail(TCA_ERR_INVALID_ARG, "sharded forward model takes x = NULL");
     cudaStream_t s = (cudaStream_t)stream;

@@ -65,6 +65,7 @@ struct CgScalars {
     int32_t xupd;    // 1: this iteration's alpha is valid (x := x + alpha p pending)
     double rr;       // <r_k, r_k> (the residual; == rho for plain CG)
     int32_t pcg;     // 1: preconditioned (rho = <r, z>; beta set by finalize 3)
+    double thr;      // tensor Jacobi: absolute threshold on R+*R
     int32_t pad;
     double red[5];   // reduced dot products (stage sum -> all-reduce -> stage apply)
 };
@@ -102,6 +103,10 @@ struct tca_operator {
     int tmap_next = 0;
     uint32_t tmap_pinned = 0;            // bit i: slot i is referenced by a captured CUDA graph
     int order = 0;
+    bool gram_form = false;              // created from G_d / R_d (tca_operator_create_gram): no A_d
+    void *ks_taps = nullptr;             // Kronecker-sum-only operator (apply_path 2): rows of lambda R_d, 5 taps
+    size_t ks_bytes = 0;
+    int ks_off[tca::kD] = {0, 0, 0, 0};
     int64_t n[tca::kD] = {1, 1, 1, 1};   // global unknown extents (padded)
     int64_t m[tca::kD] = {1, 1, 1, 1};   // global data extents (padded)
     tca_dtype dtype = TCA_F64;
@@ -135,6 +140,8 @@ struct tca_operator {
     void *z = nullptr;                           // PCG workspace z = P^-1 r
     void *pc_tmp = nullptr;                      // scratch of the dense-factor mode products
     void *sr_s = nullptr;                        // single-reduction CG: S = A P (lazy)
+    void *jac_e = nullptr;                       // tensor Jacobi: E = inverse main diagonal (lazy)
+    const void *jac_b = nullptr;                 // tensor Jacobi: B of the running solve
     // generic compressed-band forms
     tca::BandMat Gm[tca::kD], Rm[tca::kD], At[tca::kD], Af[tca::kD];
 
@@ -165,7 +172,7 @@ struct tca_operator {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int num_sms = 148;
     int band_grid = 0;                   // persistent grid of the fused banded apply
-    int apply_path = 0;                  // 0 = generic multi-pass, 1 = fused banded
+    int apply_path = 0;                  // 0 = generic multi-pass, 1 = fused banded, 2 = Kronecker-sum stencil
     // CUDA-graph replay of CG chunks
     // (two instances when timing: each carries its own captured event pairs, so
     // one can be harvested while the other runs)
@@ -174,6 +181,7 @@ struct tca_operator {
     const void *gx = nullptr;
     int gtimed = 0;                      // the instances were captured with timing events
     int gsolver = 0;                     // ... for this solver's iteration
+    const void *gb = nullptr;            // ... and this right-hand side (the Jacobi iteration reads B)
     int solver = 0;                      // iteration being run/captured: 0 CG (Fig. 2), 1 PCG, 2 single-reduction CG
     int64_t gkernels[2] = {0, 0};        // kernel launches captured in instance g (added per replay)
     bool gpend[2] = {false, false};      // instance g has launched and its events are unharvested
@@ -226,6 +234,19 @@ void launch_cgsr_update(T *x, T *p, T *sv, T *r, const T *w, int64_t N, const Cg
                         cudaStream_t s);
 void launch_cgsr_finalize(int which, const double *prr, int nrr, const double *prw, int nrw, CgScalars *sc,
                           double *hist, cudaStream_t s, int stage = 0);
+// Kronecker-sum apply (operators without a product term; tca_kernels.cu)
+template <typename T>
+void launch_ksum_apply(const T *x, T *y, int64_t N, const int64_t *n, const T *taps, const int *off,
+                       const int32_t *done, cudaStream_t s);
+// tensor Jacobi (tca_kernels.cu)
+template <typename T>
+void launch_jacobi_diag(T *e, int64_t N, const int64_t *n, const double *dg, const double *dr, int nmax, double lam,
+                        bool have_g, cudaStream_t s);
+template <typename T>
+void launch_jacobi_resid(T *r, const T *q, const T *b, int64_t N, double *part, const int32_t *done, cudaStream_t s);
+template <typename T>
+void launch_jacobi_update(T *u, const T *r, const T *e, int64_t N, const CgScalars *sc, cudaStream_t s);
+void launch_jacobi_finalize(int which, const double *part, int nparts, CgScalars *sc, double *hist, cudaStream_t s);
 // banded PCG factor solve along mode d (tca_precond.cu); src may equal dst
 template <typename T>
 tca_status launch_precond_sweep(const tca_operator *op, int d, const T *src, T *dst, int64_t outer, int64_t inner,

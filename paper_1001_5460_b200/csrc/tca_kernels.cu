@@ -696,6 +696,154 @@ void launch_cgsr_finalize(int which, const double *prr, int nrr, const double *p
     cgsr_finalize_kernel<<<1, stage == 2 ? 32 : kRedThreads, 0, s>>>(which, prr, nrr, prw, nrw, sc, hist, stage);
 }
 
+// ---------------------------------------------------------------- Kronecker-sum apply (Eq. 9)
+// y = sum_d (mode-d lambda R_d) x for an operator without a Kronecker-product
+// term (factor form, tca_operator_create_gram with G = NULL): one thread per
+// output, the <= 5 taps of each mode from taps[(off_d + r) * 5 + k + 2]
+// (zero outside the band and the domain); neighbour loads hit L1/L2.  One HBM
+// read and one write per element (the separable Poisson stencil).
+template <typename T>
+__global__ void __launch_bounds__(256)
+ksum_apply_kernel(const T *__restrict__ x, T *__restrict__ y, int64_t N, int n1, int n2, int n3, int n4,
+                  const T *__restrict__ taps, int o1, int o2, int o3, int o4, const int32_t *done)
+{
+    if (done && *done) return;
+    const int64_t s4 = 1, s3 = n4, s2 = (int64_t)n3 * n4, s1 = (int64_t)n2 * n3 * n4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t rem = i;
+        const int i4 = (int)(rem % n4); rem /= n4;
+        const int i3 = (int)(rem % n3); rem /= n3;
+        const int i2 = (int)(rem % n2); rem /= n2;
+        const int i1 = (int)rem;
+        T acc = T(0);
+#pragma unroll
+        for (int k = -2; k <= 2; ++k) {
+            if (i1 + k >= 0 && i1 + k < n1) acc = fma(__ldg(taps + (int64_t)(o1 + i1) * 5 + k + 2), __ldg(x + i + k * s1), acc);
+            if (i2 + k >= 0 && i2 + k < n2) acc = fma(__ldg(taps + (int64_t)(o2 + i2) * 5 + k + 2), __ldg(x + i + k * s2), acc);
+            if (i3 + k >= 0 && i3 + k < n3) acc = fma(__ldg(taps + (int64_t)(o3 + i3) * 5 + k + 2), __ldg(x + i + k * s3), acc);
+            if (i4 + k >= 0 && i4 + k < n4) acc = fma(__ldg(taps + (int64_t)(o4 + i4) * 5 + k + 2), __ldg(x + i + k * s4), acc);
+        }
+        y[i] = acc;
+    }
+}
+
+template <typename T>
+void launch_ksum_apply(const T *x, T *y, int64_t N, const int64_t *n, const T *taps, const int *off,
+                       const int32_t *done, cudaStream_t s)
+{
+    count_launch();
+    const int64_t blocks = std::min<int64_t>((N + 255) / 256, 148 * 16);
+    ksum_apply_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(x, y, N, (int)n[0], (int)n[1], (int)n[2], (int)n[3], taps,
+                                                          off[0], off[1], off[2], off[3], done);
+}
+
+// ---------------------------------------------------------------- tensor Jacobi (Fig. 1)
+// E := InvMainDiag(A): diag[i] = prod_d G_d[i_d, i_d] + lambda sum_d R_d[i_d, i_d]
+// from per-mode diagonals dg (4 x nmax, zero when there is no product term) and
+// dr (4 x nmax, zero for modes without a regulariser).
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+jacobi_diag_kernel(T *__restrict__ e, int64_t N, int n1, int n2, int n3, int n4, const double *__restrict__ dg,
+                   const double *__restrict__ dr, int nmax, double lam, int have_g)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t rem = i;
+        const int i4 = (int)(rem % n4); rem /= n4;
+        const int i3 = (int)(rem % n3); rem /= n3;
+        const int i2 = (int)(rem % n2); rem /= n2;
+        const int i1 = (int)rem;
+        const double pk = have_g ? dg[i1] * dg[nmax + i2] * dg[2 * nmax + i3] * dg[3 * nmax + i4] : 0.0;
+        const double sm = dr[i1] + dr[nmax + i2] + dr[2 * nmax + i3] + dr[3 * nmax + i4];
+        e[i] = (T)(1.0 / (pk + lam * sm));
+    }
+}
+
+// R := Q - B (Q = A*U) with the R+*R partials
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+jacobi_resid_kernel(T *__restrict__ r, const T *__restrict__ q, const T *__restrict__ b, int64_t N, double *part,
+                    const int32_t *done)
+{
+    if (done && *done) return;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const T v = q[i] - b[i];
+        r[i] = v;
+        acc += (double)v * (double)v;
+    }
+    const double sm = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = sm;
+}
+
+// U := U - R*E
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+jacobi_update_kernel(T *__restrict__ u, const T *__restrict__ r, const T *__restrict__ e, int64_t N,
+                     const CgScalars *sc)
+{
+    if (sc->done) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        u[i] = u[i] - r[i] * e[i];
+}
+
+// R+*R against the absolute threshold ("WHILE R+*R > threshold");
+// which = 0 after the initial residual, 1 after each update
+__global__ void __launch_bounds__(kRedThreads)
+jacobi_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgScalars *sc, double *hist)
+{
+    if (which == 1 && sc->done) return;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += kRedThreads) acc += part[i];
+    const double s = block_sum(acc);
+    if (threadIdx.x != 0) return;
+    int k = 0;
+    if (which == 0) {
+        sc->rho0 = s;
+        sc->iters = 0;
+        sc->status = TCA_OK;
+        sc->converged = 0;
+        sc->done = 0;
+    } else {
+        k = sc->iters + 1;
+        sc->iters = k;
+    }
+    sc->rho = s;
+    sc->rr = s;
+    if (hist) hist[k] = s;
+    if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
+    if (s <= sc->thr) { sc->converged = 1; sc->done = 1; return; }
+    if (k >= sc->max_iters) { sc->status = TCA_NOT_CONVERGED; sc->done = 1; }
+}
+
+template <typename T>
+void launch_jacobi_diag(T *e, int64_t N, const int64_t *n, const double *dg, const double *dr, int nmax, double lam,
+                        bool have_g, cudaStream_t s)
+{
+    count_launch();
+    jacobi_diag_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(e, N, (int)n[0], (int)n[1], (int)n[2], (int)n[3], dg, dr,
+                                                              nmax, lam, have_g ? 1 : 0);
+}
+
+template <typename T>
+void launch_jacobi_resid(T *r, const T *q, const T *b, int64_t N, double *part, const int32_t *done, cudaStream_t s)
+{
+    count_launch();
+    jacobi_resid_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, q, b, N, part, done);
+}
+
+template <typename T>
+void launch_jacobi_update(T *u, const T *r, const T *e, int64_t N, const CgScalars *sc, cudaStream_t s)
+{
+    count_launch();
+    jacobi_update_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(u, r, e, N, sc);
+}
+
+void launch_jacobi_finalize(int which, const double *part, int nparts, CgScalars *sc, double *hist, cudaStream_t s)
+{
+    count_launch();
+    jacobi_finalize_kernel<<<1, kRedThreads, 0, s>>>(which, part, nparts, sc, hist);
+}
+
 void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc, double *hist,
                         cudaStream_t s, int stage)
 {
@@ -719,7 +867,15 @@ void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc
     template void launch_cg_update_xp<T>(T *, T *, const T *, int64_t, const CgScalars *, \
                                          cudaStream_t);                                   \
     template void launch_cgsr_update<T>(T *, T *, T *, T *, const T *, int64_t,            \
-                                        const CgScalars *, double *, cudaStream_t);
+                                        const CgScalars *, double *, cudaStream_t);       \
+    template void launch_ksum_apply<T>(const T *, T *, int64_t, const int64_t *, const T *, \
+                                       const int *, const int32_t *, cudaStream_t);       \
+    template void launch_jacobi_diag<T>(T *, int64_t, const int64_t *, const double *,     \
+                                        const double *, int, double, bool, cudaStream_t); \
+    template void launch_jacobi_resid<T>(T *, const T *, const T *, int64_t, double *,     \
+                                         const int32_t *, cudaStream_t);                  \
+    template void launch_jacobi_update<T>(T *, const T *, const T *, int64_t,              \
+                                          const CgScalars *, cudaStream_t);
 
 TCA_INST(double)
 TCA_INST(float)

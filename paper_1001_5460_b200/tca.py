@@ -32,7 +32,7 @@ EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
             "tca_operator_apply_path", "tca_shard_layout", "tca_nccl_get_unique_id",
             "tca_nccl_comm_create", "tca_nccl_comm_destroy", "tca_local_group_create",
             "tca_local_group_destroy", "tca_pcg_solve", "tca_precond_apply", "tca_precond_info",
-            "tca_cgsr_solve"]
+            "tca_cgsr_solve", "tca_operator_create_gram", "tca_jacobi_solve"]
 
 _vp = ctypes.c_void_p
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -96,6 +96,9 @@ _lib.tca_operator_apply_path.argtypes = [_vp]
 _lib.tca_pcg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
 _lib.tca_precond_apply.argtypes = [_vp, _vp, _vp, _vp]
 _lib.tca_cgsr_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
+_lib.tca_jacobi_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
+_lib.tca_operator_create_gram.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _i64p, _dpp, _dpp, ctypes.c_double,
+                                          ctypes.c_int, _vp, _vp]
 _lib.tca_precond_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), _vp]
 _lib.tca_operator_apply_path.restype = ctypes.c_int
 for _name in ("tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
@@ -191,6 +194,36 @@ class Operator:
                                       self.lam, self.dtype_code, dist_p,
                                       _vp(_stream_ptr(stream)))
         _check(st, "tca_operator_create")
+        self._finish()
+
+    @classmethod
+    def from_gram(cls, G, R, lam=1.0, dtype="f64", stream=None, dist=None):
+        """M = (kron_d G_d) + lam * sum_d (mode-d R_d) from its factors
+        (tca_operator_create_gram).  G None: no Kronecker-product term (Eq. 9's
+        separable Poisson operator); R: list of n_d x n_d arrays (None: no term)."""
+        self = cls.__new__(cls)
+        self._h = _vp()
+        Rs = [None if r is None else np.ascontiguousarray(r, dtype=np.float64) for r in R]
+        Gs = None if G is None else [np.ascontiguousarray(g, dtype=np.float64) for g in G]
+        D = len(Rs)
+        self.order = D
+        self.n = tuple(int(r.shape[0]) if r is not None else int(Gs[d].shape[0]) for d, r in enumerate(Rs))
+        self.m = self.n
+        self.lam = float(lam)
+        self.dtype_code = _dtype_code(dtype)
+        self.dtype = "f64" if self.dtype_code == TCA_F64 else "f32"
+        dp = ctypes.POINTER(ctypes.c_double)
+        n_arr = (ctypes.c_int64 * D)(*self.n)
+        R_arr = (dp * D)(*[ctypes.cast(None, dp) if r is None else r.ctypes.data_as(dp) for r in Rs])
+        G_arr = None if Gs is None else (dp * D)(*[g.ctypes.data_as(dp) for g in Gs])
+        st = _lib.tca_operator_create_gram(ctypes.byref(self._h), D, n_arr, G_arr, R_arr, self.lam,
+                                           self.dtype_code, None if dist is None else ctypes.byref(dist),
+                                           _vp(_stream_ptr(stream)))
+        _check(st, "tca_operator_create_gram")
+        self._finish()
+        return self
+
+    def _finish(self):
         q = self.query()
         self.own_lo, self.own_hi, self.data_lo, self.data_hi = q[:4]
         self.banded_mask, self.half_bandwidth, self.device_bytes = q[4:]
@@ -216,8 +249,9 @@ class Operator:
 
     @property
     def apply_path(self):
-        """'fused' (one-pass banded kernel) or 'multipass' (generic per-mode kernels)."""
-        return "fused" if _lib.tca_operator_apply_path(self._h) == 1 else "multipass"
+        """'fused' (one-pass banded kernel), 'ksum' (Kronecker-sum stencil, factor-form
+        operators without a product term) or 'multipass' (generic per-mode kernels)."""
+        return {1: "fused", 2: "ksum"}.get(_lib.tca_operator_apply_path(self._h), "multipass")
 
     def set_timing(self, enable=True):
         _check(_lib.tca_operator_set_timing(self._h, 1 if enable else 0), "set_timing")
@@ -273,6 +307,11 @@ class Operator:
                   raise_on=("breakdown", "nonfinite")):
         """CG preconditioned with the Kronecker-factor P (tca_pcg_solve).  Returns (x, report dict)."""
         return self._solve(_lib.tca_pcg_solve, "tca_pcg_solve", b, x, rtol, max_iters, history, stream, raise_on)
+
+    def jacobi_solve(self, b, x=None, threshold=1e-4, max_iters=100000, history=False, stream=None):
+        """Tensor Jacobi (Fig. 1, tca_jacobi_solve): x <- U with R+*R <= threshold."""
+        return self._solve(_lib.tca_jacobi_solve, "tca_jacobi_solve", b, x, threshold, max_iters, history, stream,
+                           ("nonfinite",))
 
     def cgsr_solve(self, b, x=None, rtol=0.0, max_iters=100, history=False, stream=None,
                    raise_on=("breakdown", "nonfinite")):
