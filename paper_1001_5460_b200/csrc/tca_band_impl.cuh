@@ -108,15 +108,13 @@ struct Cfg {
     // (pick_pp); measured on config 3: fp64 283 -> 276 us (128-B chunks at a
     // 128-B pitch before), 32-B fp64 chunks 281 us; fp32 249 -> 234 us
     static constexpr bool PITCHED = NTHR == 256;
-    static constexpr bool SHIFTED = false;
-    static constexpr int SHMAX = 0;
     static constexpr int UNIT = PITCHED ? 8 : 128 / (int)sizeof(T);
     // ONEBOX: the input map is 4-D (UNIT, n3 n4 / UNIT, n2, n1) and a whole staged
     // slab (PR rows of PP elements) is one TMA box, start aligned to UNIT elements
     // (host picks it when n3 n4 % UNIT == 0; otherwise NB boxes per row for
     // fp64, 16-B chunks for PITCHED fp32)
-    static constexpr bool ONEBOX = !SHIFTED;
-    static constexpr int NEED = W + (ONEBOX ? UNIT : VEC) - 1 + SHMAX;
+    static constexpr bool ONEBOX = true;
+    static constexpr int NEED = W + UNIT - 1;
     static constexpr int boxw_for_nb(int nb) { return ((NEED + nb - 1) / nb + UNIT - 1) / UNIT * UNIT; }
     static constexpr int pick_nb()
     {
@@ -257,12 +255,6 @@ template <int N>
 __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-// in-row shift of staged slab row r (elements), see Cfg::SHIFTED
-template <typename T, int N4>
-__host__ __device__ constexpr int row_shift(int r)
-{
-    return Cfg<T, N4>::SHIFTED ? 8 * ((r & 3) == 2 ? 3 : (r & 3) == 3 ? 2 : (r & 3)) : 0;
-}
 
 // ---------------------------------------------------------------- taps
 // rec(r) = taps + (off + r + PADR) * REC; G(r, k) = G[r, r+k], R(r, k) = lambda R[r, r+k]
@@ -398,7 +390,7 @@ __device__ __forceinline__ void pass_c(const PA &a, T (&acc)[6][Cfg<T, N4>::E], 
     if (live) {
         const T *u3 = U3 + i2 * C::WIP + i3 * N4;
         const T *rb = RB + i2 * C::WIP + i3 * N4;
-        const T *pp = P + (i2 + 3) * C::PP + row_shift<T, N4>(i2 + 3) + (i3 + 3) * N4;
+        const T *pp = P + (i2 + 3) * C::PP + (i3 + 3) * N4;
         T uw[uhi - ulo], pw[phi - plo];
 #pragma unroll
         for (int k = ulo; k < uhi; ++k) uw[k - ulo] = u3[k];
@@ -471,7 +463,7 @@ __device__ __forceinline__ void pass_b(const PA &a, const T *U2, const T *RA, co
         if (i2 >= T2) return;
         constexpr int h0 = B * C::BL;
         const T *u2 = U2 + i2 * C::WP + h0 * N4 + i4;
-        const T *pp = P + (i2 + 3) * C::PP + row_shift<T, N4>(i2 + 3) + (h0 + 1) * N4 + i4;
+        const T *pp = P + (i2 + 3) * C::PP + (h0 + 1) * N4 + i4;
         const int ob = i2 * C::WIP + h0 * N4 + i4;
         T v[C::BL + 6], w[C::BL + 4], u[C::BL], rr[C::BL];
 #pragma unroll
@@ -598,7 +590,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     if (b < C::NB * PR) {
                         const int r = b / C::NB, h = b % C::NB;
                         tma_load_3d(dst + r * PP + h * C::BOXW, xmp, bar + st,
-                                    ca - delta - row_shift<T, N4>(r) + h * C::BOXW, a2 - 3 + r,
+                                    ca - delta + h * C::BOXW, a2 - 3 + r,
                                     js + a.xoff);
                     }
                 }
@@ -622,7 +614,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                 for (int c = tid; c < W; c += NTHR) {
                     T v[PR];
 #pragma unroll
-                    for (int s = 0; s < PR; ++s) v[s] = P[s * PP + row_shift<T, N4>(s) + c];
+                    for (int s = 0; s < PR; ++s) v[s] = P[s * PP + c];
                     T u[T2];
 #pragma unroll
                     for (int r = 0; r < T2; ++r) u[r] = T(0);
