@@ -300,3 +300,28 @@ def test_apply_global_tables_f32_sampled(tca):
     want = o.apply_points(x, pts)
     got = np.array([y[p] for p in pts])
     assert relerr(got, want) <= 1e-5
+
+
+# ------------------------------------------------------------------ full size (cfg 4, one GPU)
+def test_full_size_cfg4_apply_sampled(tca):
+    """Config 4 (256^3 x 32 = 537 M unknowns; tap tables in global memory) on one
+    GPU: sampled outputs of the fused apply against the oracle's pointwise
+    definition."""
+    c = synth.CONFIGS[4]
+    A, L = synth.mode_matrices(c)
+    g = tca.Operator(A, L, c.lam)
+    assert g.apply_path == "fused"
+    x = torch.empty(c.n, dtype=torch.float64, device="cuda")
+    tca.generate_normal(x, seed=5, stream_id=7)
+    y = g.apply(x)
+    torch.cuda.synchronize()
+    g.close()
+    o = oracle.Operator(A, L, c.lam)
+    rng = np.random.default_rng(6)
+    pts = [tuple(int(rng.integers(0, nd)) for nd in c.n) for _ in range(60)]
+    pts += [(0, 0, 0, 0), (255, 255, 255, 31), (1, 254, 2, 30), (128, 0, 255, 16)]
+    xh = x.cpu().numpy()
+    del x
+    want = o.apply_points(xh, pts)
+    got = np.array([float(y[p].item()) for p in pts])
+    assert relerr(got, want) <= 1e-12
