@@ -745,7 +745,9 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     TCA_TRY(halo_p(op, s));
     static const bool no_graph = getenv("TCA_NO_GRAPH") != nullptr;   // measurement switch
     if (pcg == 3) rtol = 1.0;   // Jacobi stops on its threshold: poll the device flag per chunk
-    if (!op->transport && !no_graph && max_iters > 1) {
+    // graphs also with an NCCL transport (its calls are stream-ordered and
+    // capture into the graph); not with the host-synchronised local transport
+    if ((!op->transport || op->transport->capturable()) && !no_graph && max_iters > 1) {
         TCA_TRY(cg_graph_loop<T>(op, x, rtol, max_iters, s));
     } else if (rtol <= 0.0) {
         for (int k = 0; k < max_iters; ++k) TCA_TRY(cg_iteration<T>(op, x, s));

@@ -113,6 +113,7 @@ tca_status nccl_fail(int r, const char *what)
 class NcclTransport final : public Transport {
   public:
     NcclTransport(void *comm, int rank, int nranks) : comm_(comm), rank_(rank), nranks_(nranks) {}
+    bool capturable() const override { return true; }   // NCCL collectives and p2p capture into graphs
     tca_status allreduce(double *dev, int count, cudaStream_t s) override
     {
         TCA_NCCL_TRY(nccl().AllReduce(dev, dev, (size_t)count, ncclFloat64, ncclSum, comm_, s));

@@ -80,6 +80,9 @@ class Transport {
     //   ext = [3 ghost | nloc own | 3 ghost] slabs of slab_bytes each
     // from the neighbours' boundary slabs; which = 0 (CG p) or 1 (apply input)
     virtual tca_status halo(int which, char *ext, size_t slab_bytes, int64_t nloc, cudaStream_t s) = 0;
+    // true when the exchanges are stream-ordered device operations that can be
+    // captured into a CUDA graph (NCCL); false for host-synchronised ones
+    virtual bool capturable() const { return false; }
 };
 Transport *make_transport(const tca_dist *d);
 tca_status shard_layout(int64_t n1, const double *A1, int64_t m1, int rank, int nranks, int64_t out[4]);

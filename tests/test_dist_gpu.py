@@ -138,9 +138,14 @@ def test_nccl_transport_single_rank_cg_matches_oracle(tca):
         assert op.apply_path == "fused"
         y = synth.data(A, n, m, seed=1)
         b = op.rhs(torch.from_numpy(y).cuda())
-        xs, rep = op.cg_solve(b, rtol=0.0, max_iters=30)
-        x_ref, k, st, _ = o.cg(o.rhs(y), rtol=0.0, max_iters=30)
+        # 70 iterations: eager first step, two captured graph chunks (NCCL calls
+        # inside the graph), eager tail
+        xs, rep = op.cg_solve(b, rtol=0.0, max_iters=70)
+        x_ref, k, st, _ = o.cg(o.rhs(y), rtol=0.0, max_iters=70)
         assert rel(xs.cpu().numpy(), x_ref) <= 1e-8
+        xs2, rep2 = op.cgsr_solve(b, rtol=0.0, max_iters=70)   # one all-reduce of two scalars per step
+        x_ref2, _, _, _ = o.cgsr(o.rhs(y), rtol=0.0, max_iters=70)
+        assert rel(xs2.cpu().numpy(), x_ref2) <= 1e-8
         xin = synth.random_tensor(n, seed=5)
         q = op.apply(torch.from_numpy(xin).cuda()).cpu().numpy()
         assert rel(q, o.apply(xin)) <= 1e-12
