@@ -119,19 +119,42 @@ void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob)
     p->tiles3 = (p->n3 + t3 - 1) / t3;
     const long long tiles2 = (p->n2 + band::T2 - 1) / band::T2;
     const long long total = tiles2 * p->tiles3 * p->n1;
-    // persistent grid: CTA b owns units [total*b/G, total*(b+1)/G) of the
-    // (tile-major, slab-minor) unit order
+    // persistent grid over the (tile-major, slab-minor) unit order.  A CTA's
+    // cost is its units plus 6 ramp slabs per tile it touches (mode-1 halo of
+    // the ring).  Two schedules, the cheaper (max over CTAs) wins:
+    //   split: CTA b owns units [total*b/G, total*(b+1)/G) (balanced units;
+    //          ranges cross tile boundaries) -- long mode 1 (one GPU);
+    //   whole: CTA b owns tile b entirely (tiles <= G) -- short mode 1 (a
+    //          mode-1 shard of 16 rows: 22 slab passes instead of up to 26).
     const int minb = op->dtype == TCA_F64 ? band::minb_for<double>((int)op->n[3]) : band::minb_for<float>((int)op->n[3]);
     const int G = (int)std::min<long long>(std::min(op->num_sms * minb, band::MAXG), total);
+    const long long tiles = tiles2 * p->tiles3;
+    long long split_cost = 0;
     for (int b = 0; b < G; ++b) {
         const long long u0 = total * b / G, u1 = total * (b + 1) / G;
-        const long long tile = u0 / p->n1;
-        p->s_tile[b].x = (short)(tile / p->tiles3);
-        p->s_tile[b].y = (short)(tile % p->tiles3);
-        p->s_o0[b] = (int)(u0 % p->n1);
-        p->s_cnt[b] = (int)(u1 - u0);
+        const long long segs = u1 > u0 ? (u1 - 1) / p->n1 - u0 / p->n1 + 1 : 0;
+        split_cost = std::max(split_cost, (u1 - u0) + 2 * band::KH1 * segs);
     }
-    op->band_grid = G;
+    const long long whole_cost = tiles <= band::MAXG ? p->n1 + 2 * band::KH1 : (1ll << 60);
+    if (whole_cost < split_cost) {
+        for (long long t = 0; t < tiles; ++t) {
+            p->s_tile[t].x = (short)(t / p->tiles3);
+            p->s_tile[t].y = (short)(t % p->tiles3);
+            p->s_o0[t] = 0;
+            p->s_cnt[t] = p->n1;
+        }
+        op->band_grid = (int)tiles;
+    } else {
+        for (int b = 0; b < G; ++b) {
+            const long long u0 = total * b / G, u1 = total * (b + 1) / G;
+            const long long tile = u0 / p->n1;
+            p->s_tile[b].x = (short)(tile / p->tiles3);
+            p->s_tile[b].y = (short)(tile % p->tiles3);
+            p->s_o0[b] = (int)(u0 % p->n1);
+            p->s_cnt[b] = (int)(u1 - u0);
+        }
+        op->band_grid = G;
+    }
     p->xoff = op->ghost;
     p->nin = (int)op->nloc1 + 2 * op->ghost;
     p->off1 = L.off[0];

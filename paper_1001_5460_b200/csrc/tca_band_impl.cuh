@@ -55,6 +55,7 @@ constexpr int T2 = 8;            // mode-2 rows per tile
 constexpr int PR = T2 + 6;       // staged rows (halo 3 + 3)
 constexpr int REC = 7;           // tap record per row: G[r,r..r+3], lambda R[r,r..r+2]
 constexpr int PADR = 6;          // zero rows below each table (row r at record off + r + PADR)
+constexpr int KH1 = 3;           // mode-1 half-bandwidth: a slab range needs 3 ramp slabs each side
 constexpr int TAP_BYTES = 27 * 1024;
 constexpr int MAXG = 320;        // max persistent CTAs (>= 2 x SM count)
 
