@@ -161,6 +161,15 @@ tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo,
  * takes the generic path for a call whose x or y is not 16-byte aligned. */
 int tca_operator_apply_path(const tca_operator *op);
 
+/* Whether CG / PCG solves on this operator run the fused step B1' (SURVEY.md
+ * 8(a) a5): ONE kernel per iteration forms P := R|Z + beta P,
+ * applies the pending C := C + alpha P and computes Q = M P with <P, Q>
+ * (reads R|Z, P, C; writes P, C, Q), instead of a separate update pass.
+ * 1 = yes, 0 = no (sharded operator, non-fused apply path, tables outside the
+ * parameter block, or the TCA_NO_B1 environment switch), -1 = not decided yet
+ * (no CG solve so far) or op NULL.  Results are the same iterates either way. */
+int tca_operator_cg_fused_step(const tca_operator *op);
+
 /* y = M x.  x, y: device tensors of the local shape (rows [own_lo, own_hi)
  * of mode 1 on a sharded operator); x and y must not alias. */
 tca_status tca_apply(const tca_operator *op, const void *x, void *y,

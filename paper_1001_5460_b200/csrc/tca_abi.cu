@@ -403,10 +403,10 @@ static tca_status forward_t(const tca_operator *op, const T *x, T *y, double sig
 // Timed apply: an event pair around the launch when instrumentation is on.
 // Inside a CUDA-graph capture the pair is recorded as external event nodes of
 // the graph (real timestamps at every replay), harvested per graph instance.
-static tca_status timed_apply(tca_operator *op, const void *x, void *y, const int32_t *done,
-                              cudaStream_t s, double *pq_part = nullptr)
+template <typename Fn>
+static tca_status timed_call(tca_operator *op, cudaStream_t s, Fn &&fn)
 {
-    if (!op->timing) return apply_dispatch(op, x, y, done, s, pq_part);
+    if (!op->timing) return fn();
     if (op->cap_ev) {
         cudaEvent_t a, b;
         TCA_CUDA_TRY(cudaEventCreate(&a));
@@ -414,7 +414,7 @@ static tca_status timed_apply(tca_operator *op, const void *x, void *y, const in
         TCA_CUDA_TRY(cudaEventCreate(&b));
         op->cap_ev->push_back(b);
         TCA_CUDA_TRY(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
-        TCA_TRY(apply_dispatch(op, x, y, done, s, pq_part));
+        TCA_TRY(fn());
         TCA_CUDA_TRY(cudaEventRecordWithFlags(b, s, cudaEventRecordExternal));
         return TCA_OK;
     }
@@ -428,9 +428,15 @@ static tca_status timed_apply(tca_operator *op, const void *x, void *y, const in
     cudaEvent_t a = op->tev[op->tev_used], b = op->tev[op->tev_used + 1];
     op->tev_used += 2;
     TCA_CUDA_TRY(cudaEventRecord(a, s));
-    TCA_TRY(apply_dispatch(op, x, y, done, s, pq_part));
+    TCA_TRY(fn());
     TCA_CUDA_TRY(cudaEventRecord(b, s));
     return TCA_OK;
+}
+
+static tca_status timed_apply(tca_operator *op, const void *x, void *y, const int32_t *done,
+                              cudaStream_t s, double *pq_part = nullptr)
+{
+    return timed_call(op, s, [&] { return apply_dispatch(op, x, y, done, s, pq_part); });
 }
 
 static tca_status harvest_pairs(tca_operator *op, const cudaEvent_t *ev, size_t n)
@@ -554,6 +560,22 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
                               op->part, s);
         TCA_TRY(halo_p(op, s));                                         // ghost slabs of R
         return cgsr_apply_reduce<T>(op, 6, s);                          // W := A*R; gamma, delta, alpha, beta
+    }
+    if (op->b1 == 1) {   // fused step B1': C += alpha P_old, P := R|Z + beta P_old, Q := A*P, P+*Q
+        T *pold = (T *)(op->pcur ? op->p2 : op->p_own), *pnew = (T *)(op->pcur ? op->p_own : op->p2);
+        const T *d = op->solver == 1 ? (const T *)op->z : r;
+        TCA_TRY(timed_call(op, s, [&] { return launch_fused_b1(op, pold, pnew, d, q, x, op->part, s); }));
+        op->pcur ^= 1;
+        TCA_TRY(cg_reduce(op, 1, op->part, op->band_grid_fu, s));     // alpha
+        launch_cg_update_r<T>(r, q, op->N, op->sc, op->part, s);       // R := R - alpha*Q, R+*R
+        TCA_TRY(cg_reduce(op, 2, op->part, kRedBlocks, s));            // rho1 (PCG: R+*R), stop, beta
+        if (op->solver == 1) {
+            T *z = (T *)op->z;
+            TCA_TRY(apply_precond<T>(op, r, z, done, s));              // Z := P^-1 R
+            launch_dot_partials<T>(r, z, op->N, op->part, done, s);    // R+*Z
+            TCA_TRY(cg_reduce(op, 3, op->part, kRedBlocks, s));        // rho1, beta
+        }
+        return TCA_OK;   // C and P are updated by the next step's B1' (or b1_finish)
     }
     static const bool no_fused_dot = getenv("TCA_NO_FUSED_DOT") != nullptr;   // measurement switch
     if (fused_used(op, pe, q) && !no_fused_dot) {
@@ -711,6 +733,23 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     h.max_iters = max_iters;
     h.pcg = pcg == 1;
     op->solver = pcg;
+    if (op->b1 < 0) {   // fused step B1' for Fig. 2 / PCG on one GPU: opt-in (TCA_B1=1), see DESIGN.md 6.5
+        const char *b1env = getenv("TCA_B1");
+        const bool want_b1 = b1env && b1env[0] == '1';
+        op->b1 = (want_b1 && fused_used(op, op->p_own, op->q) && fused_b1_supported(op)) ? 1 : 0;
+        if (op->b1 == 1) {
+            cudaError_t e = cudaMallocAsync(&op->p2, (size_t)op->N * op->esize, s);
+            if (e != cudaSuccess) { op->b1 = 0; cudaGetLastError(); }
+        }
+    }
+    const int b1_saved = op->b1;
+    if (pcg == 2 || pcg == 3) op->b1 = 0;   // single-reduction CG and Jacobi keep their own steps
+    op->pcur = 0;
+    if (op->b1 == 1) {
+        const void *ptrs[4] = {op->p_own, op->p2, pcg == 1 ? op->z : op->r, op->q};
+        const int kinds[4] = {0, 0, 0, 1};
+        TCA_TRY(fused_b1_prepare(op, ptrs, kinds, 4, s));
+    }
     *op->sc_host = h;
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
     TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
@@ -763,6 +802,9 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
             if (op->sc_host->done) break;
         }
     }
+    if (op->b1 == 1)   // the last step's pending C := C + alpha P (x only: done is set)
+        launch_cg_update_xp<T>(x, (T *)(op->pcur ? op->p2 : op->p_own), (const T *)op->r, op->N, op->sc, s);
+    op->b1 = b1_saved;
     TCA_CUDA_TRY(cudaGetLastError());
     TCA_CUDA_TRY(cudaEventRecord(op->ev1, s));
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
@@ -837,7 +879,7 @@ void tca_operator_destroy(tca_operator *op)
     if (op->gjoin) cudaEventDestroy(op->gjoin);
     // every stream that used the operator is done before its memory goes back
     cudaDeviceSynchronize();
-    void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp, op->sr_s,
+    void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp, op->sr_s, op->p2,
                       op->jac_e};   // stream-ordered pool
     for (void *b : pooled)
         if (b) cudaFreeAsync(b, 0);
@@ -1156,6 +1198,8 @@ tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo, int64_t *
 }
 
 int tca_operator_apply_path(const tca_operator *op) { return op ? op->apply_path : -1; }
+
+int tca_operator_cg_fused_step(const tca_operator *op) { return op ? op->b1 : -1; }
 
 tca_status tca_apply(const tca_operator *op, const void *x, void *y, void *stream)
 {

@@ -37,6 +37,14 @@ extern template int unit_for<float>(int);
 extern template int pitched_for<double>(int);
 extern template int pitched_for<float>(int);
 extern template int minb_for<float>(int);
+extern template tca_status launch_dispatch_fu<Params<double>>(const tca_operator *, const Params<double> &,
+                                                              cudaStream_t, const CUtensorMap *, const CUtensorMap *,
+                                                              const CUtensorMap *, const FuArgs<double> &);
+extern template tca_status launch_dispatch_fu<Params<float>>(const tca_operator *, const Params<float> &,
+                                                             cudaStream_t, const CUtensorMap *, const CUtensorMap *,
+                                                             const CUtensorMap *, const FuArgs<float> &);
+extern template int fu_ok_for<double>(int);
+extern template int fu_ok_for<float>(int);
 }  // namespace band
 
 namespace {
@@ -103,11 +111,12 @@ bool tables_fit(const tca_operator *op);
 // the parameter block (Params, when they fit in TAP_BYTES) or in a device
 // buffer (ParamsG, n_d ~ 256: config 4).
 template <typename T>
-void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob)
+void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob, int &grid, bool fu)
 {
     tca_operator *op = const_cast<tca_operator *>(op_c);
     const bool in_block = tables_fit(op);
-    op->band_gt = !in_block;
+    if (fu && !in_block) return;   // B1' takes parameter-block tables only
+    if (!fu) op->band_gt = !in_block;
     blob.assign(in_block ? sizeof(band::Params<T>) : sizeof(band::ParamsG<T>), 0);
     auto *p = reinterpret_cast<band::ParamsBase<T> *>(blob.data());
     const TableLayout L = table_layout(op);
@@ -136,14 +145,21 @@ void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob)
         split_cost = std::max(split_cost, (u1 - u0) + 2 * band::KH1 * segs);
     }
     const long long whole_cost = tiles <= band::MAXG ? p->n1 + 2 * band::KH1 : (1ll << 60);
-    if (whole_cost < split_cost) {
+    // measurement switch: TCA_BAND_SCHED=whole|split forces a schedule
+    // B1' prefers whole tile columns: all CTAs advance through mode 1 together,
+    // so the halo re-reads of D and P_old hit L2 (config 3 plain apply: DRAM
+    // reads 890 -> 273 MB per launch for 10 % more time, profiles/r01_sched_probe.txt)
+    static const char *force = getenv("TCA_BAND_SCHED");
+    const bool want_whole = fu ? tiles <= band::MAXG
+                               : (force && tiles <= band::MAXG ? force[0] == 'w' : whole_cost < split_cost);
+    if (want_whole) {
         for (long long t = 0; t < tiles; ++t) {
             p->s_tile[t].x = (short)(t / p->tiles3);
             p->s_tile[t].y = (short)(t % p->tiles3);
             p->s_o0[t] = 0;
             p->s_cnt[t] = p->n1;
         }
-        op->band_grid = (int)tiles;
+        grid = (int)tiles;
     } else {
         for (int b = 0; b < G; ++b) {
             const long long u0 = total * b / G, u1 = total * (b + 1) / G;
@@ -153,7 +169,7 @@ void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob)
             p->s_o0[b] = (int)(u0 % p->n1);
             p->s_cnt[b] = (int)(u1 - u0);
         }
-        op->band_grid = G;
+        grid = G;
     }
     p->xoff = op->ghost;
     p->nin = (int)op->nloc1 + 2 * op->ghost;
@@ -176,7 +192,7 @@ void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob)
     }
     if (in_block) {
         std::memcpy(reinterpret_cast<band::Params<T> *>(blob.data())->taps, taps.data(), taps.size() * sizeof(T));
-    } else {   // global tables (uploaded once; freed with the operator)
+    } else if (!fu) {   // global tables (uploaded once; freed with the operator)
         const size_t nb = taps.size() * sizeof(T);
         if (dev_get(&op->band_gtaps, nb) == cudaSuccess) {
             op->band_gtaps_bytes = nb;
@@ -346,9 +362,86 @@ bool fused_shape_supported(const tca_operator *op)
 
 tca_status fused_prepare(tca_operator *op)
 {
-    if (op->dtype == TCA_F64) build_params<double>(op, op->band_params);
-    else build_params<float>(op, op->band_params);
+    if (op->dtype == TCA_F64) build_params<double>(op, op->band_params, op->band_grid, false);
+    else build_params<float>(op, op->band_params, op->band_grid, false);
     return TCA_OK;
+}
+
+bool fused_b1_supported(const tca_operator *op)
+{
+    if (op->ghost != 0 || op->band_gt || op->band_params.empty()) return false;   // one GPU, block tables
+    const int n4 = (int)op->n[3];
+    const bool pitched = (op->dtype == TCA_F64 ? band::pitched_for<double>(n4) : band::pitched_for<float>(n4)) != 0;
+    if (!pitched && !onebox_of(op)) return false;   // one TMA box per staged slab
+    return (op->dtype == TCA_F64 ? band::fu_ok_for<double>(n4) : band::fu_ok_for<float>(n4)) != 0;
+}
+
+namespace {
+template <typename T>
+tca_status launch_b1_t(const tca_operator *op_c, const void *pold, void *pnew, const void *d, void *q, void *x,
+                       double *pq_part, cudaStream_t s)
+{
+    tca_operator *op = const_cast<tca_operator *>(op_c);
+    if (op->band_params_fu.empty()) return fail(TCA_ERR_INVALID_ARG, "fused CG step: not prepared");
+    tca_status st = TCA_OK;
+    int ps = 0, ds = 0;
+    const CUtensorMap *pm = cached_tmap(op, pold, 0, s, &st, &ps);
+    if (!pm) return st;
+    const CUtensorMap *dm = cached_tmap(op, d, 0, s, &st, &ds);
+    if (!dm) return st;
+    int qs = 0;
+    const CUtensorMap *qm = cached_tmap(op, q, 1, s, &st, &qs);
+    if (!qm) return st;
+    auto *p = reinterpret_cast<band::Params<T> *>(op->band_params_fu.data());
+    p->x = (const T *)pold;
+    p->y = (T *)q;
+    p->done = &op->sc->done;
+    p->pq_part = pq_part;
+    {
+        static const char *e = getenv("TCA_BAND_DEBUG");   // measurement switches (results invalid)
+        p->dbg = e ? atoi(e) : 0;
+    }
+    const band::FuArgs<T> fa{(T *)x, (T *)pnew, op->sc};
+    TCA_TRY(band::launch_dispatch_fu(op, *p, s, pm, qm, dm, fa));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TCA_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) {
+        op->tmap_pinned |= (1u << ps) | (1u << ds) | (1u << qs);
+    } else {
+        TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[ps], s));
+        TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[ds], s));
+        TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[qs], s));
+    }
+    return TCA_OK;
+}
+}  // namespace
+
+// Parameter block and tensor maps of B1' created before any graph capture: a
+// map first made inside a capture would be uploaded only when the graph runs,
+// not for eager launches after it.
+tca_status fused_b1_prepare(const tca_operator *op_c, const void *const *ptrs, const int *kinds, int n,
+                            cudaStream_t s)
+{
+    tca_operator *op = const_cast<tca_operator *>(op_c);
+    if (op->band_params_fu.empty()) {
+        if (op->dtype == TCA_F64) build_params<double>(op, op->band_params_fu, op->band_grid_fu, true);
+        else build_params<float>(op, op->band_params_fu, op->band_grid_fu, true);
+        if (op->band_params_fu.empty()) return fail(TCA_ERR_INVALID_ARG, "fused CG step: tables not in block");
+    }
+    for (int i = 0; i < n; ++i) {
+        tca_status st = TCA_OK;
+        int slot = 0;
+        if (!cached_tmap(op, ptrs[i], kinds[i], s, &st, &slot)) return st;
+        TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[slot], s));
+    }
+    return TCA_OK;
+}
+
+tca_status launch_fused_b1(const tca_operator *op, const void *pold, void *pnew, const void *d, void *q, void *x,
+                           double *pq_part, cudaStream_t s)
+{
+    if (op->dtype == TCA_F64) return launch_b1_t<double>(op, pold, pnew, d, q, x, pq_part, s);
+    return launch_b1_t<float>(op, pold, pnew, d, q, x, pq_part, s);
 }
 
 bool fused_pointers_ok(const void *x, const void *y)

@@ -92,6 +92,17 @@ struct ParamsG : ParamsBase<T> {
     const T *gtaps;
 };
 
+// Fused CG step B1': the apply kernel also
+// forms its own input, P_new = D + beta P_old (D = R, or Z in PCG), applies the
+// pending C := C + alpha P_old and writes P_new, so one HBM pass reads D, P_old
+// and C and writes P_new, C and Q (6 words per unknown; Fig. 2's order).
+template <typename T>
+struct FuArgs {
+    T *x;                 // C (own slabs)
+    T *pn;                // P_new (own slabs); P_old is the kernel input a.x
+    const CgScalars *sc;  // alpha (of the previous iteration), beta, xupd, done
+};
+
 template <typename T, int N4>
 struct Cfg {
     static constexpr int NSEG = (N4 + 3) / 4;        // ring segments along i4
@@ -190,6 +201,15 @@ struct Cfg {
     static constexpr size_t SMEM_CAP = MINB == 1 ? 227 * 1024 : 113 * 1024;   // per CTA
     static constexpr int NSTAGE = ((3 * stage_elems + rest_elems) * sizeof(T) + 256 <= SMEM_CAP) ? 3 : 2;
     static constexpr size_t smem_bytes = (NSTAGE * stage_elems + rest_elems) * sizeof(T) + 128;
+    // B1': D stages (NSTAGE_FU) + P_old stages (NSTAGE_FU - 1), RB aliases RA,
+    // Q stored from registers (no output staging)
+    // (Q stored from registers); XB: C of the next own slab, prefetched with
+    // cp.async (each thread its own 16-B vectors: no registers held across passes)
+    static constexpr size_t XBE = al((size_t)T2 * WI);
+    static constexpr size_t rest_fu = U2E + 2 * WIE + XBE;
+    static constexpr int NSTAGE_FU = ((5 * stage_elems + rest_fu) * sizeof(T) + 256 <= SMEM_CAP) ? 3 : 2;
+    static constexpr size_t smem_fu = ((2 * NSTAGE_FU - 1) * stage_elems + rest_fu) * sizeof(T) + 128;
+    static constexpr bool FU_OK = smem_fu <= SMEM_CAP;
     static_assert(T3 % BL == 0, "T3");
     static_assert(NBLK * WPB <= NTHR / 32, "pass B: one item per warp");
     static_assert(WI <= 256, "store box");
@@ -249,6 +269,12 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void 
                  : "memory");
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory"); }
@@ -362,10 +388,10 @@ __device__ __forceinline__ void ring_step_rot(T (&acc)[6][E], const T (&s)[E], c
     }
 }
 
-template <typename T, int N4, int SEG, typename PA>
+template <typename T, int N4, int SEG, typename PA, bool FU>
 __device__ __forceinline__ void pass_c(const PA &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3, const T *RB,
                                        const T *P, T *OUT, int pos, int rot, int j, bool live, bool emit, int a2,
-                                       int a3, int o0, int o1, double &pq)
+                                       int a3, int o0, int o1, double &pq, int qoff)
 {
     using C = Cfg<T, N4>;
     constexpr int E = C::E;
@@ -414,7 +440,14 @@ __device__ __forceinline__ void pass_c(const PA &a, T (&acc)[6][Cfg<T, N4>::E], 
 #pragma unroll
         for (int e = 0; e < NE; ++e) pc[e] = pw[e0 + e - plo];
     }
-    T *out = OUT + (pos / C::T3) * C::WI + (pos % C::T3) * N4 + e0;
+    T *out;
+    bool st = emit;
+    if constexpr (FU) {   // OUT: output slab j-3 in HBM; qoff: this thread's element in it (-1: clipped)
+        out = OUT + qoff + e0;
+        st = emit && qoff >= 0;
+    } else {
+        out = OUT + (pos / C::T3) * C::WI + (pos % C::T3) * N4 + e0;
+    }
     T ov[E];
     const bool dot = a.pq_part != nullptr && j >= o0 && j < o1;   // input slab j is one of this CTA's
     if constexpr (C::RING_SHIFT) {
@@ -429,20 +462,21 @@ __device__ __forceinline__ void pass_c(const PA &a, T (&acc)[6][Cfg<T, N4>::E], 
 #undef TCA_ROT
         }
     }
-    if (emit) {
+    if (st) {
 #pragma unroll
         for (int e = 0; e < NE; ++e) out[e] = ov[e];
     }
 }
 
-template <typename T, int N4, int SEG, typename PA>
+template <typename T, int N4, int SEG, typename PA, bool FU>
 __device__ __forceinline__ void pass_c_dispatch(const PA &a, T (&acc)[6][Cfg<T, N4>::E], const T *U3,
                                                 const T *RB, const T *P, T *OUT, int seg, int pos, int rot, int j,
-                                                bool live, bool emit, int a2, int a3, int o0, int o1, double &pq)
+                                                bool live, bool emit, int a2, int a3, int o0, int o1, double &pq,
+                                                int qoff)
 {
     if constexpr (SEG < Cfg<T, N4>::NSEG) {
-        if (seg == SEG) pass_c<T, N4, SEG, PA>(a, acc, U3, RB, P, OUT, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
-        else pass_c_dispatch<T, N4, SEG + 1, PA>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
+        if (seg == SEG) pass_c<T, N4, SEG, PA, FU>(a, acc, U3, RB, P, OUT, pos, rot, j, live, emit, a2, a3, o0, o1, pq, qoff);
+        else pass_c_dispatch<T, N4, SEG + 1, PA, FU>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq, qoff);
     }
 }
 
@@ -504,30 +538,71 @@ __device__ __forceinline__ void pass_b(const PA &a, const T *U2, const T *RA, co
 }
 
 // ---------------------------------------------------------------- kernel
-template <typename T, int N4, typename PA>
+template <typename T> struct V16;   // 16-byte vectors (B1' streaming parts)
+template <> struct V16<double> { using V = double2; };
+template <> struct V16<float> { using V = float4; };
+__device__ __forceinline__ double2 v_axpy(double2 y, double a, double2 x) { return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y)); }
+__device__ __forceinline__ float4 v_axpy(float4 y, float a, float4 x)
+{
+    return make_float4(fmaf(a, x.x, y.x), fmaf(a, x.y, y.y), fmaf(a, x.z, y.z), fmaf(a, x.w, y.w));
+}
+
+template <typename T, int N4, typename PA, bool FU>
 __global__ void __launch_bounds__(Cfg<T, N4>::NTHR, Cfg<T, N4>::MINB)
 band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict__ ymp,
-                  const __grid_constant__ PA a)
+                  const __grid_constant__ PA a, const CUtensorMap *__restrict__ rmp, const __grid_constant__ FuArgs<T> f)
 {
     using C = Cfg<T, N4>;
     constexpr int W = C::W, WI = C::WI, PP = C::PP, T3 = C::T3, E = C::E, NTHR = C::NTHR;
+    constexpr int NS = FU ? C::NSTAGE_FU : C::NSTAGE;   // input stages
     const int dbg = TCA_BAND_DBG ? a.dbg : 0;   // phase switches (measurement builds only)
-    if (a.done && *a.done) return;
+    if constexpr (FU) {
+        if (*a.done) {   // stopped: only the pending C := C + alpha P_old of the last iteration
+            if (f.sc->xupd) {
+                const T alpha = (T)f.sc->alpha;
+                const size_t n = (size_t)a.n1 * a.n2 * a.n3 * N4;
+                const T *po = a.x + (size_t)a.xoff * a.n2 * a.n3 * N4;
+                for (size_t i = blockIdx.x * (size_t)NTHR + threadIdx.x; i < n; i += (size_t)gridDim.x * NTHR)
+                    f.x[i] = fma(alpha, po[i], f.x[i]);
+            }
+            return;
+        }
+    } else {
+        if (a.done && *a.done) return;
+    }
     if (dbg & 16) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
     T *Pst = reinterpret_cast<T *>(smem_raw + 128);
-    T *U2 = Pst + C::NSTAGE * C::stage_elems;
+    T *POst = Pst + NS * C::stage_elems;                                   // B1': P_old stages
+    T *U2 = FU ? POst + (NS - 1) * C::stage_elems : Pst + NS * C::stage_elems;
     T *RA = U2 + C::U2E;
     T *U3 = RA + C::WIE;
-    T *RB = U3 + C::WIE;
-    T *OUTB = RB + C::WIE;   // [2][OUTE]
+    T *RB = FU ? RA : U3 + C::WIE;   // B1': pass B updates RA in place
+    T *OUTB = RB + C::WIE;   // [2][OUTE] (not used by B1')
+    T *XB = U3 + C::WIE;     // B1': C of the next own slab, [vector][VW]
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    // B1' scalars of this step: P_new = D + beta P_old, C += alpha P_old (xu)
+    T alpha = T(0), beta = T(0);
+    bool xu = false;
+    if constexpr (FU) {
+        alpha = (T)f.sc->alpha;
+        beta = (T)f.sc->beta;
+        xu = f.sc->xupd != 0;
+    }
+    using V = typename V16<T>::V;
+    constexpr int VW = 16 / (int)sizeof(T);
+    constexpr int NVR = WI / VW;                     // 16-B vectors per interior row
+    constexpr int NV = T2 * NVR;
+    constexpr int XIT = (NV + NTHR - 1) / NTHR;      // vectors per thread
+    static_assert(WI % VW == 0, "interior rows are whole vectors");
+    const int F = a.n3 * N4;                         // row stride (elements)
+    const size_t slabE = (size_t)a.n2 * F;           // slab stride (elements)
     // xmp/ymp: tensor maps in global memory (a descriptor in a >4 KB parameter
     // block is not usable by the TMA unit)
     if (tid == 0) {
-        for (int s = 0; s < C::NSTAGE; ++s) mbar_init(bar + s, 1);
+        for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -550,6 +625,29 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         const int a3 = __shfl_sync(0xffffffffu, t3i * T3, 0);
         const int b2 = __shfl_sync(0xffffffffu, a.off2 + t2i * T2, 0);   // uniform mode-2 table row base
         const int ca = (a3 - 3) * N4;                              // flat column of staged column 0
+        // B1' per-tile element offsets within a slab (-1: outside the domain):
+        // this thread's 16-B vectors of the interior, and its ring outputs
+        // B1' per-tile element offsets within a slab (-1: outside the domain):
+        // this thread's 16-B vectors of the interior, and its ring outputs
+        int voff[XIT], qoff = -1;
+        auto fetch_x = [&](int js) {   // cp.async of C's slab js (own vectors) into XB
+            const T *xg = f.x + (size_t)js * slabE;
+#pragma unroll
+            for (int it = 0; it < XIT; ++it)
+                if (voff[it] >= 0) cp_async16(XB + (tid + it * NTHR) * VW, xg + voff[it]);
+            cp_async_commit();
+        };
+        if constexpr (FU) {
+#pragma unroll
+            for (int it = 0; it < XIT; ++it) {
+                const int v = tid + it * NTHR, r = v / NVR, cv = v % NVR;
+                voff[it] = (v < NV && a2 + r < a.n2 && a3 * N4 + cv * VW < F) ? (a2 + r) * F + a3 * N4 + cv * VW : -1;
+            }
+            const int q2 = a2 + pos / C::T3, q3 = a3 + pos % C::T3;
+            qoff = (q2 < a.n2 && q3 < a.n3) ? q2 * F + q3 * N4 : -1;
+            const int jx0 = o0 > -a.xoff ? o0 : -a.xoff;   // first own slab
+            if (xu && jx0 < o1) fetch_x(jx0);
+        }
         // boxes start 16-B aligned (per-row boxes) or UNIT-aligned (one box per slab)
         const bool onebox = C::PITCHED || (C::ONEBOX && a.onebox);
         const int cal = onebox ? C::UNIT : C::VEC;
@@ -573,8 +671,18 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         // every warp (one warp issuing all of them serialises ~30 UTMALDG)
         auto issue = [&](int js) {
             if (dbg & 256) { ++gi; return; }   // compute-only timing: no loads
-            const unsigned st = gi % C::NSTAGE;
+            const unsigned st = gi % NS;
             T *dst = Pst + st * C::stage_elems;
+            if constexpr (FU) {   // D and P_old slabs, one barrier (host guarantees one box per slab)
+                if (tid == 0) {
+                    mbar_arrive_expect_tx(bar + st, (unsigned)(2 * PR * PP * sizeof(T)));
+                    tma_load_4d(dst, rmp, bar + st, 0, cchunk, a2 - 3, js + a.xoff);
+                    tma_load_4d(POst + (gi % (NS - 1)) * C::stage_elems, xmp, bar + st, 0, cchunk, a2 - 3,
+                                js + a.xoff);
+                }
+                ++gi;
+                return;
+            }
             if (onebox) {
                 if (tid == 0) {
                     mbar_arrive_expect_tx(bar + st, (unsigned)(PR * PP * sizeof(T)));
@@ -599,23 +707,33 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             ++gi;
         };
         if (!(dbg & 8))
-            for (int js = jb; js < je && js < jb + C::NSTAGE - 1; ++js) issue(js);
-        int next = jb + C::NSTAGE - 1;   // next slab to stage
+            for (int js = jb; js < je && js < jb + NS - 1; ++js) issue(js);
+        int next = jb + NS - 1;   // next slab to stage
         int rot = 0;                     // ring rotation (rotating form only)
         int pending = -1;                // output slab whose staging buffer awaits its TMA store
 #pragma unroll 1
         for (int j = j0; j < j1; ++j) {
             const bool live = j >= jb && j < je && !(dbg & 8);
-            const T *P = Pst + (gc % C::NSTAGE) * C::stage_elems + delta;
-            if (live && !(dbg & (128 | 256))) mbar_wait(bar + gc % C::NSTAGE, (gc / C::NSTAGE) & 1);
+            T *P = Pst + (gc % NS) * C::stage_elems + delta;
+            if (live && !(dbg & (128 | 256))) mbar_wait(bar + gc % NS, (gc / NS) & 1);
+            const T *PO = POst + (gc % (NS > 1 ? NS - 1 : 1)) * C::stage_elems + delta;   // B1': P_old slab j
+            const bool own = FU && live && j >= o0 && j < o1;
 
             // ---- pass A: G2 (all halo-extended columns), lambda R2 (interior columns)
             if (live && !(dbg & 4)) {
 #pragma unroll 1
                 for (int c = tid; c < W; c += NTHR) {
                     T v[PR];
+                    if (FU && !(dbg & 2048)) {   // P_new := D + beta P_old on the staged slab (halo included)
 #pragma unroll
-                    for (int s = 0; s < PR; ++s) v[s] = P[s * PP + c];
+                        for (int s = 0; s < PR; ++s) {
+                            v[s] = fma(beta, PO[s * PP + c], P[s * PP + c]);
+                            if (s >= 3 && s < 3 + T2) P[s * PP + c] = v[s];   // rows read by passes B, C
+                        }
+                    } else {
+#pragma unroll
+                        for (int s = 0; s < PR; ++s) v[s] = P[s * PP + c];
+                    }
                     T u[T2];
 #pragma unroll
                     for (int r = 0; r < T2; ++r) u[r] = T(0);
@@ -656,6 +774,20 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     }
                 }
             }
+            if (FU && own && xu && !(dbg & 512)) {   // C := C + alpha P_old (interior of slab j)
+                cp_async_wait_all();
+                T *xs = f.x + (size_t)j * slabE;
+#pragma unroll
+                for (int it = 0; it < XIT; ++it) {
+                    const int v = tid + it * NTHR;
+                    if (voff[it] >= 0) {
+                        const V xv = *reinterpret_cast<const V *>(XB + v * VW);
+                        const V po = *reinterpret_cast<const V *>(PO + (v / NVR + 3) * PP + 3 * N4 + (v % NVR) * VW);
+                        *reinterpret_cast<V *>(xs + voff[it]) = v_axpy(xv, alpha, po);
+                    }
+                }
+                if (j + 1 < o1) fetch_x(j + 1);
+            }
             __syncthreads();   // bar1: U2/RA complete; all threads finished slab j-1
 
             if (pending >= 0) {   // uniform: every thread tracks the same pending slab
@@ -671,16 +803,25 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                 issue(next);
                 ++next;
             }
-
+            if (own && !(dbg & 1024)) {   // B1': P_new of slab j (own interior) to HBM
+                T *ps = f.pn + (size_t)j * slabE;
+#pragma unroll
+                for (int it = 0; it < XIT; ++it) {
+                    const int v = tid + it * NTHR;
+                    if (voff[it] >= 0)
+                        *reinterpret_cast<V *>(ps + voff[it]) =
+                            *reinterpret_cast<const V *>(P + (v / NVR + 3) * PP + 3 * N4 + (v % NVR) * VW);
+                }
+            }
             // ---- pass B: G3 on U2, lambda R3 on p (8 outputs along i3 per item; item = warp)
             if (live && !(dbg & 4)) pass_b<T, N4, 0, PA>(a, U2, RA, P, U3, RB, a3, warp, lane);
             __syncthreads();   // bar2: U3/RB complete
 
             // ---- pass C + mode-1 ring + emission of output slab j-3
             const bool emit = (j - 3 >= o0) && (j - 3 < o1);
-            T *OUT = OUTB + (j & 1) * C::OUTE;
-            if (!(dbg & 2)) pass_c_dispatch<T, N4, 0, PA>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq);
-            if (emit) {
+            T *OUT = FU ? a.y + (ptrdiff_t)(j - 3) * (ptrdiff_t)slabE : OUTB + (j & 1) * C::OUTE;
+            if (!(dbg & 2)) pass_c_dispatch<T, N4, 0, PA, FU>(a, acc, U3, RB, P, OUT, seg, pos, rot, j, live, emit, a2, a3, o0, o1, pq, qoff);
+            if (!FU && emit) {
                 fence_proxy_async();
                 pending = j - 3;
             }
@@ -688,15 +829,17 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             rot = rot == 5 ? 0 : rot + 1;
         }
         __syncthreads();
-        if (pending >= 0) {
+        if (!FU && pending >= 0) {
             if (tid == 0 && !(dbg & (1 | 256))) {
                 tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                 bulk_commit();
             }
             pending = -1;
         }
-        if (tid == 0) bulk_wait<0>();   // the next segment rewrites the staging buffers
-        __syncthreads();
+        if (!FU) {
+            if (tid == 0) bulk_wait<0>();   // the next segment rewrites the staging buffers
+            __syncthreads();
+        }
     }
     if (a.pq_part) {   // fixed-order CTA reduction of the <x, y> partials (deterministic)
         double *red = reinterpret_cast<double *>(smem_raw + 128);   // stage memory is idle now
@@ -713,21 +856,27 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
 }
 
 // ---------------------------------------------------------------- host side
-template <typename T, int N4, typename PA>
+template <typename T, int N4, typename PA, bool FU>
 tca_status launch_n4(const tca_operator *op, const PA &prm, cudaStream_t s, const CUtensorMap *xm,
-                     const CUtensorMap *ym)
+                     const CUtensorMap *ym, const CUtensorMap *rm, const FuArgs<T> &fa)
 {
     using C = Cfg<T, N4>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        TCA_CUDA_TRY(cudaFuncSetAttribute(band_apply_kernel<T, N4, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)C::smem_bytes));
-        attr_set = true;
+    if constexpr (FU && !C::FU_OK) {
+        return fail(TCA_ERR_INVALID_ARG, "fused CG step: shape does not fit shared memory");
+    } else {
+        constexpr size_t smem = FU ? C::smem_fu : C::smem_bytes;
+        static bool attr_set = false;
+        if (!attr_set) {
+            TCA_CUDA_TRY(cudaFuncSetAttribute(band_apply_kernel<T, N4, PA, FU>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_set = true;
+        }
+        count_launch();
+        band_apply_kernel<T, N4, PA, FU>
+            <<<(unsigned)(FU ? op->band_grid_fu : op->band_grid), C::NTHR, smem, s>>>(xm, ym, prm, rm, fa);
+        TCA_CUDA_TRY(cudaGetLastError());
+        return TCA_OK;
     }
-    count_launch();
-    band_apply_kernel<T, N4, PA><<<(unsigned)op->band_grid, C::NTHR, C::smem_bytes, s>>>(xm, ym, prm);
-    TCA_CUDA_TRY(cudaGetLastError());
-    return TCA_OK;
 }
 
 #define TCA_BAND_N4_LIST(X) X(1) X(2) X(4) X(7) X(8) X(15) X(16) X(32)
@@ -816,14 +965,42 @@ int boxw_for(int n4)
     return 0;
 }
 
+template <typename T>
+int fu_ok_for(int n4)
+{
+    switch (n4) {
+#define TCA_CASE(n) \
+    case n: return Cfg<T, n>::FU_OK ? 1 : 0;
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return 0;
+}
+
 template <typename PA>
 tca_status launch_dispatch(const tca_operator *op, const PA &prm, cudaStream_t s, const CUtensorMap *xm,
                            const CUtensorMap *ym)
 {
     using T = typename PA::value_type;
+    const FuArgs<T> none{};
     switch ((int)op->n[3]) {
 #define TCA_CASE(n) \
-    case n: return launch_n4<T, n, PA>(op, prm, s, xm, ym);
+    case n: return launch_n4<T, n, PA, false>(op, prm, s, xm, ym, nullptr, none);
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return fail(TCA_ERR_INVALID_ARG, "band apply: unsupported n4");
+}
+
+// B1' (fused CG step): xm = P_old map, rm = D map, output Q = prm.y
+template <typename PA>
+tca_status launch_dispatch_fu(const tca_operator *op, const PA &prm, cudaStream_t s, const CUtensorMap *xm,
+                              const CUtensorMap *ym, const CUtensorMap *rm, const FuArgs<typename PA::value_type> &fa)
+{
+    using T = typename PA::value_type;
+    switch ((int)op->n[3]) {
+#define TCA_CASE(n) \
+    case n: return launch_n4<T, n, PA, true>(op, prm, s, xm, ym, rm, fa);
         TCA_BAND_N4_LIST(TCA_CASE)
 #undef TCA_CASE
     }

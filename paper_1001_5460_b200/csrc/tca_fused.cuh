@@ -10,4 +10,11 @@ bool fused_pointers_ok(const void *x, const void *y);      // TMA alignment of t
 // (op->band_grid entries) -- the CG <p, q> fused into the apply epilogue.
 tca_status launch_fused_apply(const tca_operator *op, const void *x, void *y,
                               const int32_t *done, double *pq_part, cudaStream_t s);
+// Fused CG step B1' (one GPU): C += alpha P_old (when sc->xupd), P_new = D +
+// beta P_old, Q = A P_new, per-CTA <P_new, Q> partials (op->band_grid_fu);
+// sc->done: only the pending C update.
+bool fused_b1_supported(const tca_operator *op);
+tca_status fused_b1_prepare(const tca_operator *op, const void *const *ptrs, const int *kinds, int n, cudaStream_t s);
+tca_status launch_fused_b1(const tca_operator *op, const void *pold, void *pnew, const void *d, void *q, void *x,
+                           double *pq_part, cudaStream_t s);
 }  // namespace tca

@@ -175,6 +175,15 @@ struct tca_operator {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int num_sms = 148;
     int band_grid = 0;                   // persistent grid of the fused banded apply
+    // fused CG step B1' (apply that also forms P_new and updates C): its own
+    // parameter block and schedule (whole tile columns: every CTA at the same
+    // mode-1 slab, so the halo re-reads hit L2), two P buffers (P_old is read
+    // by neighbouring CTAs while P_new is written)
+    std::vector<unsigned char> band_params_fu;
+    int band_grid_fu = 0;
+    int b1 = -1;                         // -1: not decided, 0: off, 1: on
+    void *p2 = nullptr;                  // second P buffer
+    int pcur = 0;                        // 0: P in p_own, 1: P in p2
     int apply_path = 0;                  // 0 = generic multi-pass, 1 = fused banded, 2 = Kronecker-sum stencil
     // CUDA-graph replay of CG chunks
     // (two instances when timing: each carries its own captured event pairs, so

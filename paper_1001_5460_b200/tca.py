@@ -29,7 +29,7 @@ EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
             "tca_cg_solve", "tca_solve_host", "tca_operator_destroy", "tca_generate_normal",
             "tca_forward_model", "tca_status_string", "tca_last_error", "tca_version",
             "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches",
-            "tca_operator_apply_path", "tca_shard_layout", "tca_nccl_get_unique_id",
+            "tca_operator_apply_path", "tca_operator_cg_fused_step", "tca_shard_layout", "tca_nccl_get_unique_id",
             "tca_nccl_comm_create", "tca_nccl_comm_destroy", "tca_local_group_create",
             "tca_local_group_destroy", "tca_pcg_solve", "tca_precond_apply", "tca_precond_info",
             "tca_cgsr_solve", "tca_operator_create_gram", "tca_jacobi_solve"]
@@ -93,6 +93,8 @@ _lib.tca_local_group_create.restype = ctypes.c_int
 _lib.tca_local_group_destroy.argtypes = [_vp]
 _lib.tca_local_group_destroy.restype = None
 _lib.tca_operator_apply_path.argtypes = [_vp]
+_lib.tca_operator_cg_fused_step.argtypes = [_vp]
+_lib.tca_operator_cg_fused_step.restype = ctypes.c_int
 _lib.tca_pcg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
 _lib.tca_precond_apply.argtypes = [_vp, _vp, _vp, _vp]
 _lib.tca_cgsr_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
@@ -252,6 +254,14 @@ class Operator:
         """'fused' (one-pass banded kernel), 'ksum' (Kronecker-sum stencil, factor-form
         operators without a product term) or 'multipass' (generic per-mode kernels)."""
         return {1: "fused", 2: "ksum"}.get(_lib.tca_operator_apply_path(self._h), "multipass")
+
+    @property
+    def cg_fused_step(self):
+        """True when CG / PCG solves run the fused step B1' (one kernel per iteration
+        forms P, updates C and applies the operator), False otherwise, None before
+        the first solve."""
+        v = _lib.tca_operator_cg_fused_step(self._h)
+        return None if v < 0 else bool(v)
 
     def set_timing(self, enable=True):
         _check(_lib.tca_operator_set_timing(self._h, 1 if enable else 0), "set_timing")
