@@ -262,6 +262,26 @@ tca_status tca_solve_host(tca_operator *op, const void *ydata_host,
                           void *x_host, double rtol, int32_t max_iters,
                           tca_cg_report *rep, void *stream);
 
+/*
+ * Pipelined end-to-end solves of `count` independent data sets with the same
+ * operator (the same bases and lambda): item i copies ydata_host[i] to the
+ * device, forms its rhs, runs tca_cg_solve and copies x back to x_host[i].
+ * The H2D of item i+1 runs on an internal copy stream while item i computes
+ * and the D2H of item i while item i+1 computes, so on a compute-bound solve
+ * the PCIe transfers are hidden (SURVEY.md 8(d) time-to-solution with host
+ * I/O).  Host buffers: caller-owned, pinned for overlap (pageable works but
+ * serialises), shapes as in tca_solve_host.  Device memory: two ydata and two
+ * x staging buffers besides the operator's.  reps: NULL or `count` reports.
+ * Returns the first error (later items are not started), else
+ * TCA_NOT_CONVERGED if any item did not converge, else TCA_OK.  Synchronises
+ * `stream` and the copy stream before returning.
+ */
+tca_status tca_solve_host_batch(tca_operator *op, int count,
+                                const void *const *ydata_host,
+                                void *const *x_host, double rtol,
+                                int32_t max_iters, tca_cg_report *reps,
+                                void *stream);
+
 void tca_operator_destroy(tca_operator *op);
 
 /*

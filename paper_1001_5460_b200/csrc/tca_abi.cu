@@ -1367,6 +1367,85 @@ tca_status tca_solve_host(tca_operator *op, const void *ydata_host, void *x_host
     return st;
 }
 
+// Pipelined host-to-host solves: the H2D of item i+1 (copy stream) overlaps the
+// rhs and CG of item i, the D2H of item i overlaps item i+1.  Two ydata
+// buffers and two x staging buffers; one b and one x work buffer (the CG
+// graphs stay cached on one x pointer).
+tca_status tca_solve_host_batch(tca_operator *op, int count, const void *const *ydata_host, void *const *x_host,
+                                double rtol, int32_t max_iters, tca_cg_report *reps, void *stream)
+{
+    TCA_TRY(check_op(op));
+    if (count < 0) return fail(TCA_ERR_INVALID_ARG, "count must be >= 0");
+    if (count > 0 && (!ydata_host || !x_host)) return fail(TCA_ERR_INVALID_ARG, "ydata_host and x_host arrays are NULL");
+    for (int i = 0; i < count; ++i)
+        if (!ydata_host[i] || !x_host[i]) return fail(TCA_ERR_INVALID_ARG, "ydata_host[i] and x_host[i] must be non-NULL");
+    if (count == 0) return TCA_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t yb = (size_t)op->Mloc * op->esize, vb = (size_t)op->N * op->esize;
+    cudaStream_t cs = nullptr;
+    void *yd[2] = {nullptr, nullptr}, *xs[2] = {nullptr, nullptr}, *bd = nullptr, *xd = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_rhs[2] = {}, ev_x[2] = {}, ev_d2h[2] = {};
+    tca_status st = TCA_OK;
+    auto cu = [&](cudaError_t e, const char *what) {
+        if (e != cudaSuccess && st == TCA_OK) st = cuda_fail(e, what);
+        return st == TCA_OK;
+    };
+    bool ok = cu(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
+    for (int k = 0; k < 2 && ok; ++k) {
+        ok = cu(cudaMallocAsync(&yd[k], yb, s), "ydata buffers") && cu(cudaMallocAsync(&xs[k], vb, s), "x staging");
+        for (cudaEvent_t *e : {&ev_h2d[k], &ev_rhs[k], &ev_x[k], &ev_d2h[k]})
+            if (ok) ok = cu(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "events");
+    }
+    if (ok) ok = cu(cudaMallocAsync(&bd, vb, s), "b") && cu(cudaMallocAsync(&xd, vb, s), "x");
+    // the copy stream starts after the allocations (stream-ordered on s)
+    if (ok) ok = cu(cudaEventRecord(ev_rhs[0], s), "event") && cu(cudaEventRecord(ev_rhs[1], s), "event") &&
+                 cu(cudaEventRecord(ev_d2h[0], s), "event") && cu(cudaEventRecord(ev_d2h[1], s), "event");
+    auto h2d = [&](int i) {
+        const int k = i & 1;
+        return cu(cudaStreamWaitEvent(cs, ev_rhs[k], 0), "wait") &&   // buffer k consumed by item i-2's rhs
+               cu(cudaMemcpyAsync(yd[k], ydata_host[i], yb, cudaMemcpyHostToDevice, cs), "H2D ydata") &&
+               cu(cudaEventRecord(ev_h2d[k], cs), "event");
+    };
+    if (ok) ok = h2d(0);
+    for (int i = 0; i < count && ok; ++i) {
+        const int k = i & 1;
+        if (i + 1 < count && !(ok = h2d(i + 1))) break;
+        if (!(ok = cu(cudaStreamWaitEvent(s, ev_h2d[k], 0), "wait"))) break;
+        tca_status r = tca_rhs(op, yd[k], bd, stream);
+        if (r != TCA_OK) { st = r; break; }
+        if (!(ok = cu(cudaEventRecord(ev_rhs[k], s), "event"))) break;
+        r = tca_cg_solve(op, bd, xd, rtol, max_iters, reps ? &reps[i] : nullptr, stream);
+        if (r != TCA_OK && r != TCA_NOT_CONVERGED) { st = r; break; }
+        if (r == TCA_NOT_CONVERGED && st == TCA_OK) st = r;
+        // x -> staging k (free once item i-2's D2H is done), D2H on the copy stream
+        if (!(ok = cu(cudaStreamWaitEvent(s, ev_d2h[k], 0), "wait") &&
+                   cu(cudaMemcpyAsync(xs[k], xd, vb, cudaMemcpyDeviceToDevice, s), "x staging copy") &&
+                   cu(cudaEventRecord(ev_x[k], s), "event") && cu(cudaStreamWaitEvent(cs, ev_x[k], 0), "wait") &&
+                   cu(cudaMemcpyAsync(x_host[i], xs[k], vb, cudaMemcpyDeviceToHost, cs), "D2H x") &&
+                   cu(cudaEventRecord(ev_d2h[k], cs), "event")))
+            break;
+    }
+    if (cs) {
+        cudaError_t e = cudaStreamSynchronize(cs);
+        if (e != cudaSuccess && (st == TCA_OK || st == TCA_NOT_CONVERGED)) st = cuda_fail(e, "copy stream");
+        cudaEventRecord(ev_h2d[0], cs);
+        cudaStreamWaitEvent(s, ev_h2d[0], 0);
+    }
+    for (int k = 0; k < 2; ++k) {
+        if (yd[k]) cudaFreeAsync(yd[k], s);
+        if (xs[k]) cudaFreeAsync(xs[k], s);
+    }
+    if (bd) cudaFreeAsync(bd, s);
+    if (xd) cudaFreeAsync(xd, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess && (st == TCA_OK || st == TCA_NOT_CONVERGED)) st = cuda_fail(e, "stream");
+    for (int k = 0; k < 2; ++k)
+        for (cudaEvent_t ev : {ev_h2d[k], ev_rhs[k], ev_x[k], ev_d2h[k]})
+            if (ev) cudaEventDestroy(ev);
+    if (cs) cudaStreamDestroy(cs);
+    return st;
+}
+
 tca_status tca_generate_normal(void *out, tca_dtype dtype, int64_t count, int64_t offset,
                                uint64_t seed, uint32_t stream_id, double scale, void *stream)
 {

@@ -26,7 +26,7 @@ OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_NOT_SPD, ERR_OOM, ERR_CUDA, ERR_NCCL, \
     ERR_BREAKDOWN, ERR_NONFINITE, NOT_CONVERGED = range(10)
 
 EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
-            "tca_cg_solve", "tca_solve_host", "tca_operator_destroy", "tca_generate_normal",
+            "tca_cg_solve", "tca_solve_host", "tca_solve_host_batch", "tca_operator_destroy", "tca_generate_normal",
             "tca_forward_model", "tca_status_string", "tca_last_error", "tca_version",
             "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches",
             "tca_operator_apply_path", "tca_operator_cg_fused_step", "tca_shard_layout", "tca_nccl_get_unique_id",
@@ -66,6 +66,8 @@ _lib.tca_cg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32,
                               ctypes.POINTER(CgReport), _vp]
 _lib.tca_solve_host.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32,
                                 ctypes.POINTER(CgReport), _vp]
+_lib.tca_solve_host_batch.argtypes = [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.c_double,
+                                      ctypes.c_int32, ctypes.POINTER(CgReport), _vp]
 _lib.tca_operator_destroy.argtypes = [_vp]
 _lib.tca_operator_destroy.restype = None
 _lib.tca_generate_normal.argtypes = [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
@@ -104,7 +106,7 @@ _lib.tca_operator_create_gram.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _i6
 _lib.tca_precond_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), _vp]
 _lib.tca_operator_apply_path.restype = ctypes.c_int
 for _name in ("tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
-              "tca_cg_solve", "tca_solve_host", "tca_generate_normal", "tca_forward_model",
+              "tca_cg_solve", "tca_solve_host", "tca_solve_host_batch", "tca_generate_normal", "tca_forward_model",
               "tca_operator_set_timing", "tca_operator_get_timing"):
     getattr(_lib, _name).restype = ctypes.c_int
 
@@ -367,6 +369,26 @@ class Operator:
         bw = (ctypes.c_int * self.order)()
         _check(_lib.tca_precond_info(self._h, eps, bw, _vp(0)), "tca_precond_info")
         return list(eps), list(bw)
+
+    def solve_host_batch(self, ydata_hosts, x_hosts, rtol=0.0, max_iters=100, stream=None):
+        """Pipelined end-to-end solves (tca_solve_host_batch): item i's host data
+        ydata_hosts[i] -> rhs -> CG -> x_hosts[i], the host<->device copies of
+        neighbouring items overlapping the compute.  Returns one report per item."""
+        if len(ydata_hosts) != len(x_hosts):
+            raise ValueError("ydata_hosts and x_hosts differ in length")
+        for lst, numel, name in ((ydata_hosts, self.Mloc, "ydata_hosts"), (x_hosts, self.N, "x_hosts")):
+            for t in lst:
+                if t.is_cuda or not t.is_contiguous() or t.dtype != self.torch_dtype or t.numel() != numel:
+                    raise ValueError(f"{name}: expected contiguous host tensors of {numel} {self.torch_dtype}")
+        n = len(ydata_hosts)
+        ys = (_vp * max(n, 1))(*[_vp(t.data_ptr()) for t in ydata_hosts])
+        xs = (_vp * max(n, 1))(*[_vp(t.data_ptr()) for t in x_hosts])
+        reps = (CgReport * max(n, 1))()
+        st = _lib.tca_solve_host_batch(self._h, n, ys, xs, float(rtol), int(max_iters), reps,
+                                       _vp(_stream_ptr(stream)))
+        _check(st, "tca_solve_host_batch", allow=[NOT_CONVERGED])
+        return [dict(iterations=r.iterations, converged=bool(r.converged), status=r.status,
+                     rho0=r.rho0, rho_final=r.rho_final, seconds=r.seconds) for r in reps[:n]]
 
     def solve_host(self, ydata_host, x_host, rtol=0.0, max_iters=100, stream=None):
         """End-to-end solve from host buffers (torch CPU tensors, pinned recommended)."""

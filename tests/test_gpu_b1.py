@@ -192,3 +192,26 @@ def test_b1_short_solves(k, tca):
     xr, _, _, _ = o.cg(b, rtol=0.0, max_iters=k)
     assert rel(x.cpu().numpy(), xr) <= 1e-8
     op.close()
+
+
+# ------------------------------------------------------------------ pipelined host solves
+def test_solve_host_batch_matches_single_solves(tca):
+    """tca_solve_host_batch: every item equals its own tca_solve_host (same
+    kernels and reductions) and the oracle's Fig. 2 iterate; copies of
+    neighbouring items overlap the compute (odd count: both buffer parities)."""
+    n, m, lam = (16, 12, 20, 15), (32, 24, 40, 30), 1e-2
+    A, L = synth.mode_matrices(n, m, seed=2)
+    o = oracle.Operator(A, L, lam)
+    op = tca.Operator(A, L, lam)
+    ys = [torch.from_numpy(synth.data(A, n, m, seed=s)).contiguous().pin_memory() for s in (3, 4, 5)]
+    xs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in ys]
+    reps = op.solve_host_batch(ys, xs, rtol=0.0, max_iters=40)
+    assert [r["iterations"] for r in reps] == [40, 40, 40]
+    for y, x in zip(ys, xs):
+        x1 = torch.empty(n, dtype=torch.float64).pin_memory()
+        op.solve_host(y, x1, rtol=0.0, max_iters=40)
+        assert torch.equal(x, x1)
+        xr, _, _, _ = o.cg(o.rhs(y.numpy()), rtol=0.0, max_iters=40)
+        assert rel(x.numpy(), xr) <= 1e-8
+    assert op.solve_host_batch([], [], max_iters=5) == []
+    op.close()
