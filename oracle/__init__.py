@@ -81,6 +81,8 @@ def lib():
             L.orc_cgsr.restype = ctypes.c_int
             L.orc_jacobi.argtypes = L.orc_cg.argtypes
             L.orc_jacobi.restype = ctypes.c_int
+            for nm in ("orc_scattered_data", "orc_scattered_rhs", "orc_scattered_forward"):
+                getattr(L, nm).argtypes = [ctypes.c_int, _i64p, ctypes.c_int64, _dp, _dp, _dp]
             _lib = L
     return _lib
 
@@ -292,3 +294,93 @@ def dot(a, b) -> float:
     a, b = _f64(a).ravel(), _f64(b).ravel()
     assert a.size == b.size
     return lib().orc_dot(a.size, _p(a), _p(b))
+
+
+def cg_fig2(apply, b, rtol: float, max_iters: int):
+    """Fig. 2 step by step for any SPD apply (numpy vectors),
+    with readings Z1-Z3, Z12 as in orc_cg; dots through orc_dot.  Returns
+    (x, iterations, status, rho history)."""
+    b = _f64(b)
+    r = b.copy()                       # R := B - A*0
+    x = np.zeros_like(b)               # C := 0
+    p = r.copy()                       # P := R
+    rho = dot(r, r)                    # rho := R+*R
+    rho0, hist, k, status = rho, [rho], 0, OK
+    if not np.isfinite(rho):
+        return x, 0, NONFINITE, np.array(hist)
+    while rho > 0.0 and k < max_iters:
+        q = apply(p)                   # Q := A*(P*D)
+        pq = dot(p, q)
+        if not np.isfinite(pq):
+            status = NONFINITE
+            break
+        if not pq > 0.0:
+            status = BREAKDOWN
+            break
+        alpha = rho / pq               # alpha := rho / (P+*Q)
+        x = x + alpha * p              # C := C + alpha*P*D
+        r = r - alpha * q              # R := R - alpha*Q
+        rho1 = dot(r, r)               # rho1 := R+*R
+        k += 1
+        hist.append(rho1)
+        if not np.isfinite(rho1):
+            status = NONFINITE
+            break
+        if rho1 == 0.0 or (rtol > 0.0 and rho1 <= rtol * rtol * rho0):   # Z12; Z1, Z2
+            break
+        if k == max_iters:
+            if rtol > 0.0:
+                status = NOT_CONVERGED
+            break
+        p = r + (rho1 / rho) * p       # P := R + (rho1/rho)*P
+        rho = rho1
+    return x, k, status, np.array(hist)
+
+
+class ScatteredOperator:
+    """Scattered-data normal operator (Sec. 4; reading Z27):
+    M x = sum_k w_k <w_k, x> + lam * sum_d (mode-d R_d) x,  w_k = (x)_d a_{k,d},
+    a_{k,d}[i] = beta3(t[k, d] - i) (the cubic B-spline of Z5), R_d = L_d^T L_d.
+    n: grid shape; t: K x D sample coordinates in grid units; L: list or None."""
+
+    def __init__(self, n, t, L=None, lam=0.0):
+        self.n = tuple(int(v) for v in n)
+        self.D = len(self.n)
+        self.t = _f64(t).reshape(-1, self.D)
+        self.K = self.t.shape[0]
+        self.lam = float(lam)
+        self._na, self._np = _i64(self.n)
+        R = [None] * self.D if L is None else [None if (l is None or l.shape[0] == 0) else gram(l) for l in L]
+        self._reg = Operator.from_gram(None, [r if r is not None else np.zeros((k, k)) for r, k in zip(R, self.n)],
+                                       self.lam)
+
+    @property
+    def N(self):
+        return int(np.prod(self.n))
+
+    def data(self, x) -> np.ndarray:
+        """sum_k w_k <w_k, x>"""
+        x = _f64(x).reshape(self.n)
+        y = np.zeros(self.n)
+        lib().orc_scattered_data(self.D, self._np, self.K, _p(self.t), _p(x), _p(y))
+        return y
+
+    def apply(self, x) -> np.ndarray:
+        return self.data(x) + self._reg.apply(x)
+
+    def rhs(self, yk) -> np.ndarray:
+        yk = _f64(yk).ravel()
+        assert yk.size == self.K
+        b = np.empty(self.n)
+        lib().orc_scattered_rhs(self.D, self._np, self.K, _p(self.t), _p(yk), _p(b))
+        return b
+
+    def forward(self, x) -> np.ndarray:
+        x = _f64(x).reshape(self.n)
+        yk = np.empty(self.K)
+        lib().orc_scattered_forward(self.D, self._np, self.K, _p(self.t), _p(x), _p(yk))
+        return yk
+
+    def cg(self, b, rtol: float, max_iters: int):
+        x, k, st, hist = cg_fig2(lambda v: self.apply(v.reshape(self.n)), _f64(b).reshape(self.n), rtol, max_iters)
+        return x, k, st, hist

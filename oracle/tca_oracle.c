@@ -668,3 +668,106 @@ int orc_jacobi(int D, const int64_t *n, const double *const *G, const double *co
     free(r);
     return status;
 }
+
+/* ------------------------------------------------------------------------
+ * Scattered-data normal operator (reading Z27).
+ * Sec. 4: spline reconstruction from scattered
+ * measurements, the system decomposed as a sum of rank-1 (CANDECOMP) terms and
+ * applied without storing the system or its decomposition:
+ *   w_k = a_{k,1} (x) ... (x) a_{k,D},   a_{k,d}[i] = beta3(t_{k,d} - i)
+ *   data term  y = sum_k w_k <w_k, x>   (= W^T W x, W the K x N sample matrix)
+ *   rhs        b = sum_k yk_k w_k       (= W^T yk)
+ *   forward    yk_k = <w_k, x>          (= W x)
+ * beta3: the centred cardinal cubic B-spline of reading Z5; t in coefficient
+ * grid units (row k of t holds sample k's D coordinates).  Every a_{k,d}[i]
+ * is evaluated for all i in [0, n_d) and zero weights are skipped.
+ * ---------------------------------------------------------------------- */
+static double orc_beta3(double u)
+{
+    u = fabs(u);
+    if (u < 1.0) return 2.0 / 3.0 - u * u + 0.5 * u * u * u;
+    if (u < 2.0) { double v = 2.0 - u; return v * v * v / 6.0; }
+    return 0.0;
+}
+
+/* nonzero entries of a_{k,d}: indices idx[0..cnt) ascending, values val */
+static int orc_sample_weights(double t, int64_t n, int64_t *idx, double *val, int cap)
+{
+    int cnt = 0;
+    for (int64_t i = 0; i < n; i++) {
+        double w = orc_beta3(t - (double)i);
+        if (w != 0.0 && cnt < cap) { idx[cnt] = i; val[cnt] = w; cnt++; }
+    }
+    return cnt;
+}
+
+#define ORC_SCAT_CAP 8
+
+/* visit every nonzero of w_k: flat index and weight, modes in order 1..D
+ * (mode D fastest), calling f(flat, weight, ctx) */
+static void orc_sample_visit(int D, const int64_t *n, const double *tk,
+                             void (*f)(int64_t, double, void *), void *ctx)
+{
+    int64_t idx[4][ORC_SCAT_CAP];
+    double val[4][ORC_SCAT_CAP];
+    int cnt[4];
+    for (int d = 0; d < D; d++) {
+        cnt[d] = orc_sample_weights(tk[d], n[d], idx[d], val[d], ORC_SCAT_CAP);
+        if (cnt[d] == 0) return;
+    }
+    int j[4] = {0, 0, 0, 0};
+    for (;;) {
+        int64_t flat = 0;
+        double w = 1.0;
+        for (int d = 0; d < D; d++) {
+            flat = flat * n[d] + idx[d][j[d]];
+            w *= val[d][j[d]];
+        }
+        f(flat, w, ctx);
+        int d = D - 1;
+        while (d >= 0 && ++j[d] == cnt[d]) { j[d] = 0; d--; }
+        if (d < 0) break;
+    }
+}
+
+struct orc_scat_ctx { const double *x; double *y; double s; };
+static void orc_scat_gather(int64_t flat, double w, void *c)
+{
+    struct orc_scat_ctx *q = (struct orc_scat_ctx *)c;
+    q->s += w * q->x[flat];
+}
+static void orc_scat_scatter(int64_t flat, double w, void *c)
+{
+    struct orc_scat_ctx *q = (struct orc_scat_ctx *)c;
+    q->y[flat] += q->s * w;
+}
+
+/* y += sum_k w_k <w_k, x> */
+void orc_scattered_data(int D, const int64_t *n, int64_t K, const double *t, const double *x, double *y)
+{
+    for (int64_t k = 0; k < K; k++) {
+        struct orc_scat_ctx c = {x, y, 0.0};
+        orc_sample_visit(D, n, t + k * D, orc_scat_gather, &c);    /* <w_k, x> */
+        orc_sample_visit(D, n, t + k * D, orc_scat_scatter, &c);   /* y += <w_k, x> w_k */
+    }
+}
+
+/* b = sum_k yk_k w_k */
+void orc_scattered_rhs(int D, const int64_t *n, int64_t K, const double *t, const double *yk, double *b)
+{
+    memset(b, 0, sizeof(double) * prod(n, D));
+    for (int64_t k = 0; k < K; k++) {
+        struct orc_scat_ctx c = {NULL, b, yk[k]};
+        orc_sample_visit(D, n, t + k * D, orc_scat_scatter, &c);
+    }
+}
+
+/* yk_k = <w_k, x> */
+void orc_scattered_forward(int D, const int64_t *n, int64_t K, const double *t, const double *x, double *yk)
+{
+    for (int64_t k = 0; k < K; k++) {
+        struct orc_scat_ctx c = {x, NULL, 0.0};
+        orc_sample_visit(D, n, t + k * D, orc_scat_gather, &c);
+        yk[k] = c.s;
+    }
+}

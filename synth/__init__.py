@@ -261,6 +261,20 @@ def data_at(A, n, m, k, seed=1, sigma=NOISE_SIGMA):
     return out
 
 
+STREAM_SCATTER = 6   # scattered sample coordinates (reading Z27)
+# the paper's scattered workload: 128^3 x 16 grid, ~9e6 samples
+SCATTER_SHAPE = (128, 128, 128, 16)
+SCATTER_K = 9_000_000
+
+
+def scattered_positions(n, K, seed=1) -> np.ndarray:
+    """K x D sample coordinates, uniform on [0, n_d - 1] per mode (coefficient
+    grid units, Z27): t[k, d] = (n_d - 1) * u(seed, STREAM_SCATTER, k D + d)."""
+    D = len(n)
+    u = counter_uniform(seed, STREAM_SCATTER, np.arange(K * D, dtype=np.uint64)).reshape(K, D)
+    return u * (np.asarray(n, dtype=np.float64) - 1.0)[None, :]
+
+
 def random_tensor(shape, seed, stream=7) -> np.ndarray:
     """Generic seeded N(0,1) test tensor (streams >= 7 are test-only)."""
     return normals(seed, stream, int(np.prod(shape))).reshape(shape)

@@ -553,3 +553,95 @@ def test_P15_jacobi_steps_and_solution(n):
     ref = np.linalg.solve(K, b)
     assert st == oracle.OK and h[-1] <= 1e-24
     assert np.linalg.norm(uo.ravel() - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+# ---------------------------------------------------------------- P16: scattered-data operator (reading Z27)
+def scipy_sample_matrix(n, t):
+    """Dense K x N sample matrix W[k, i] = prod_d beta3(t[k,d] - i_d), the cubic
+    B-spline from scipy's BSpline.basis_element on knots (-2,-1,0,1,2) (an
+    evaluation independent of the oracle's)."""
+    from scipy.interpolate import BSpline
+    b = BSpline.basis_element([-2.0, -1.0, 0.0, 1.0, 2.0], extrapolate=False)
+    per = []
+    for d, nd in enumerate(n):
+        v = b(t[:, d][:, None] - np.arange(nd)[None, :])
+        per.append(np.nan_to_num(v, nan=0.0))
+    W = per[0]
+    for d in range(1, len(n)):
+        W = (W[:, :, None] * per[d][:, None, :]).reshape(t.shape[0], -1)
+    return W
+
+
+@pytest.mark.parametrize("n,K", [((5, 4, 6), 40), ((4, 3, 5, 6), 60), ((9,), 7), ((6, 7), 25)])
+def test_P16_scattered_equals_dense_sample_matrix(n, K):
+    t = synth.scattered_positions(n, K, seed=3)
+    t[0] = np.floor(t[0])   # a sample on grid points (3 nonzeros per mode)
+    W = scipy_sample_matrix(n, t)
+    L = [synth.second_difference(k) for k in n]
+    o = oracle.ScatteredOperator(n, t, L, 0.1)
+    x = synth.random_tensor(n, seed=41).ravel()
+    yk = synth.random_tensor((K,), seed=42)
+    R = 0
+    for d in range(len(n)):
+        P = np.ones((1, 1))
+        for e in range(len(n)):
+            P = np.kron(P, (L[e].T @ L[e]) if e == d else np.eye(n[e]))
+        R = R + P
+    ref = W.T @ (W @ x) + 0.1 * (R @ x)
+    assert np.linalg.norm(o.apply(x).ravel() - ref) <= 1e-14 * np.linalg.norm(ref)
+    assert np.linalg.norm(o.rhs(yk).ravel() - W.T @ yk) <= 1e-14 * np.linalg.norm(W.T @ yk)
+    assert np.linalg.norm(o.forward(x) - W @ x) <= 1e-14 * np.linalg.norm(W @ x)
+
+
+def test_P16_full_grid_samples_equal_kronecker_operator():
+    """Samples on the whole tensor grid of Z5's positions: sum_k w_k w_k^T =
+    kron_d A_d^T A_d and sum_k y_k w_k = (kron A_d^T) y (Eq. 4), the gridded
+    operator pinned by P1-P7."""
+    n, m = (6, 5, 7), (11, 9, 12)
+    A, L = synth.mode_matrices(n, m)
+    pos = [synth.sample_positions(nd, md) for nd, md in zip(n, m)]
+    t = np.array(list(itertools.product(*pos)))
+    so = oracle.ScatteredOperator(n, t, L, 1e-2)
+    go = oracle.Operator(A, L, 1e-2)
+    x = synth.random_tensor(n, seed=43)
+    ref = go.apply(x)
+    assert np.linalg.norm(so.apply(x) - ref) <= 1e-13 * np.linalg.norm(ref)
+    y = synth.random_tensor(m, seed=44)
+    ref = go.rhs(y)
+    assert np.linalg.norm(so.rhs(y.ravel()) - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_P16_partition_of_unity_and_energy():
+    """sum_i beta3(t - i) = 1 for t in [1, n-2] (cubic B-spline partition of
+    unity): W 1 = 1 on interior samples; <x, W^T W x> = ||W x||^2 >= 0."""
+    n = (8, 9, 7, 6)
+    t = synth.scattered_positions(n, 300, seed=5)
+    o = oracle.ScatteredOperator(n, t, None, 0.0)
+    one = o.forward(np.ones(n))
+    inside = np.all((t >= 1.0) & (t <= np.asarray(n) - 2.0), axis=1)
+    assert inside.sum() > 20
+    assert np.allclose(one[inside], 1.0, rtol=0, atol=1e-14)
+    assert np.all(one[~inside] < 1.0 + 1e-14)
+    x = synth.random_tensor(n, seed=45)
+    wx = o.forward(x)
+    assert np.isclose(float(np.sum(x * o.data(x))), float(wx @ wx), rtol=1e-13)
+
+
+def test_P16_scattered_cg_equals_dense_solve():
+    n = (5, 4, 6, 3)
+    t = synth.scattered_positions(n, 500, seed=6)
+    L = [synth.second_difference(k) for k in n]
+    o = oracle.ScatteredOperator(n, t, L, 1e-2)
+    W = scipy_sample_matrix(n, t)
+    R = 0
+    for d in range(len(n)):
+        P = np.ones((1, 1))
+        for e in range(len(n)):
+            P = np.kron(P, (L[e].T @ L[e]) if e == d else np.eye(n[e]))
+        R = R + P
+    M = W.T @ W + 1e-2 * R
+    b = synth.random_tensor(n, seed=46)
+    x, k, st, hist = o.cg(b, rtol=1e-13, max_iters=2000)
+    assert st == oracle.OK
+    ref = np.linalg.solve(M, b.ravel())
+    assert np.linalg.norm(x.ravel() - ref) <= 1e-9 * np.linalg.norm(ref)
