@@ -161,6 +161,35 @@ tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo,
  * takes the generic path for a call whose x or y is not 16-byte aligned. */
 int tca_operator_apply_path(const tca_operator *op);
 
+/*
+ * Scattered-data operator (reading Z27 and 6.6):
+ * the normal equations of a cubic B-spline fit to K scattered samples, Sec. 4
+ * of the paper, held as its rank-1 (CANDECOMP) sample
+ * terms, never as a matrix:
+ *   M x = sum_k w_k <w_k, x> + lambda sum_d (mode-d L_d^T L_d) x,
+ *   w_k = a_{k,1} (x) ... (x) a_{k,D},  a_{k,d}[i] = beta3(t[k*order+d] - i)
+ * with beta3 the centred cubic B-spline of reading Z5.
+ *   n: order extents (<= 4096 each); t: HOST array K x order (row-major),
+ *      sample coordinates in coefficient-grid units, each in [0, n_d - 1];
+ *      copied (bucketed by tile) at create, the caller may free it.
+ *   L: as in tca_operator_create (NULL: no regulariser).
+ * On such an operator tca_apply / tca_cg_solve / tca_cgsr_solve use M;
+ * tca_rhs takes ydata = K sample values (device, original sample order) and
+ * forms sum_k y_k w_k; tca_forward_model writes the K values <w_k, x> (+ noise)
+ * (x NULL: the seed's x_true); tca_solve_host(_batch) takes K host values.
+ * PCG, Jacobi and the preconditioner calls return TCA_ERR_INVALID_ARG.
+ * Single GPU (no dist).  Sums use atomics: results are reproducible to
+ * rounding, not bit-for-bit.  Errors: TCA_ERR_INVALID_ARG (NULL/non-finite/
+ * out-of-range t, bad L), TCA_ERR_SHAPE (n, or a last mode too long for the
+ * shared-memory tile), TCA_ERR_CUDA.
+ */
+tca_status tca_operator_create_scattered(tca_operator **op, int order,
+                                         const int64_t *n, int64_t K,
+                                         const double *t,
+                                         const double *const *L,
+                                         double lambda, tca_dtype dtype,
+                                         void *stream);
+
 /* Whether CG / PCG solves on this operator run the fused step B1' (SURVEY.md
  * 8(a) a5): ONE kernel per iteration forms P := R|Z + beta P,
  * applies the pending C := C + alpha P and computes Q = M P with <P, Q>

@@ -307,6 +307,7 @@ static tca_status apply_dispatch(const tca_operator *op, const void *x, void *y,
             launch_ksum_apply<float>((const float *)x, (float *)y, op->N, op->n, (const float *)op->ks_taps,
                                      op->ks_off, done, s);
         TCA_CUDA_TRY(cudaGetLastError());
+        if (op->scat) return launch_scatter(op, 0, x, y, nullptr, done, s);   // + sum_k w_k <w_k, x>
         return TCA_OK;
     }
     if (fused_used(op, x, y)) return launch_fused_apply(op, x, y, done, pq_part, s);
@@ -880,7 +881,7 @@ void tca_operator_destroy(tca_operator *op)
     // every stream that used the operator is done before its memory goes back
     cudaDeviceSynchronize();
     void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp, op->sr_s, op->p2,
-                      op->jac_e};   // stream-ordered pool
+                      op->jac_e, op->sc_t, op->sc_perm, op->sc_tstart};   // stream-ordered pool
     for (void *b : pooled)
         if (b) cudaFreeAsync(b, 0);
     dev_put(op->part, sizeof(double) * kRedBlocks * 2);
@@ -1181,6 +1182,60 @@ tca_status tca_operator_create_gram(tca_operator **out, int order, const int64_t
     return create_impl(out, order, n, n, Ap, nullptr, lambda, dtype, dist, stream, true, G, R);
 }
 
+tca_status tca_operator_create_scattered(tca_operator **out, int order, const int64_t *n, int64_t K,
+                                        const double *t, const double *const *L, double lambda, tca_dtype dtype,
+                                        void *stream)
+{
+    if (!out) return fail(TCA_ERR_INVALID_ARG, "op (output pointer) is NULL");
+    *out = nullptr;
+    if (order < 1 || order > 4 || !n) return fail(TCA_ERR_INVALID_ARG, "order must be in 1..4 and n non-NULL");
+    if (K < 0) return fail(TCA_ERR_INVALID_ARG, "K must be >= 0");
+    if (K > 0 && !t) return fail(TCA_ERR_INVALID_ARG, "t is NULL");
+    std::vector<std::vector<double>> eye((size_t)order), R((size_t)order);
+    const double *Ap[4] = {nullptr, nullptr, nullptr, nullptr}, *Rp[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int d = 0; d < order; ++d) {
+        if (n[d] < 1 || n[d] > 4096) return fail(TCA_ERR_SHAPE, "n[" + std::to_string(d) + "] out of range");
+        eye[d].assign((size_t)(n[d] * n[d]), 0.0);
+        for (int64_t i = 0; i < n[d]; ++i) eye[d][(size_t)(i * n[d] + i)] = 1.0;
+        Ap[d] = eye[d].data();
+        if (L && L[d] && n[d] >= 3) {   // R_d = L_d^T L_d (reading Z7)
+            const int64_t nd = n[d];
+            if (!all_finite(L[d], (size_t)((nd - 2) * nd)))
+                return fail(TCA_ERR_INVALID_ARG, "L[" + std::to_string(d) + "] has non-finite entries");
+            R[d].assign((size_t)(nd * nd), 0.0);
+            for (int64_t k = 0; k < nd - 2; ++k)
+                for (int64_t i = 0; i < nd; ++i) {
+                    const double a = L[d][k * nd + i];
+                    if (a == 0.0) continue;
+                    for (int64_t j = 0; j < nd; ++j) R[d][(size_t)(i * nd + j)] += a * L[d][k * nd + j];
+                }
+            Rp[d] = R[d].data();
+        }
+    }
+    for (int64_t k = 0; k < K; ++k)
+        for (int d = 0; d < order; ++d) {
+            const double v = t[k * order + d];
+            if (!(v >= 0.0 && v <= (double)(n[d] - 1)))
+                return fail(TCA_ERR_INVALID_ARG, "t[" + std::to_string(k) + "][" + std::to_string(d) +
+                                                     "] outside [0, n_d - 1] (or not finite)");
+        }
+    tca_operator *op = nullptr;
+    TCA_TRY(create_impl(&op, order, n, n, Ap, nullptr, lambda, dtype, nullptr, stream, true, nullptr, Rp));
+    if (op->apply_path != 2) {
+        tca_operator_destroy(op);
+        return fail(TCA_ERR_INVALID_ARG, "scattered operator: L_d must give banded R_d (half-bandwidth <= 2)");
+    }
+    op->scat = true;
+    op->Mloc = K;
+    tca_status st = scatter_prepare(op, K, t, (cudaStream_t)stream);
+    if (st != TCA_OK) {
+        tca_operator_destroy(op);
+        return st;
+    }
+    *out = op;
+    return TCA_OK;
+}
+
 tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo, int64_t *own_hi,
                               int64_t *data_lo, int64_t *data_hi, int *banded_mask,
                               int *half_bw, size_t *device_bytes)
@@ -1253,9 +1308,13 @@ int64_t tca_kernel_launches(void) { return g_launches.load(); }
 tca_status tca_rhs(const tca_operator *op, const void *ydata, void *b, void *stream)
 {
     TCA_TRY(check_op(op));
-    if (op->gram_form) return fail(TCA_ERR_INVALID_ARG, "tca_rhs: operator was created from its factors (no A_d)");
     if (!ydata || !b) return fail(TCA_ERR_INVALID_ARG, "ydata and b must be non-NULL device pointers");
     cudaStream_t s = (cudaStream_t)stream;
+    if (op->scat) {   // b = sum_k y_k w_k
+        TCA_CUDA_TRY(cudaMemsetAsync(b, 0, (size_t)op->N * op->esize, s));
+        return launch_scatter(op, 1, nullptr, b, ydata, nullptr, s);
+    }
+    if (op->gram_form) return fail(TCA_ERR_INVALID_ARG, "tca_rhs: operator was created from its factors (no A_d)");
     if (op->dtype == TCA_F64) TCA_TRY(rhs_t<double>(op, (const double *)ydata, (double *)b, s));
     else TCA_TRY(rhs_t<float>(op, (const float *)ydata, (float *)b, s));
     TCA_CUDA_TRY(cudaGetLastError());
@@ -1280,6 +1339,10 @@ static tca_status solve_common(tca_operator *op, const void *b, void *x, double 
         TCA_CUDA_TRY(dev_get((void **)&op->hist, sizeof(double) * (max_iters + 1)));
         op->hist_cap = max_iters + 1;
     }
+    if ((pcg == 1 || pcg == 3) && op->scat)
+        return fail(TCA_ERR_INVALID_ARG, pcg == 1 ? "tca_pcg_solve: no Kronecker-factor preconditioner for a scattered-data "
+                                                    "operator"
+                                                  : "tca_jacobi_solve: not available for a scattered-data operator");
     if (pcg == 3 && (op->nranks > 1 || op->transport))
         return fail(TCA_ERR_INVALID_ARG, "tca_jacobi_solve: not available on a sharded operator");
     if (pcg == 3 && rtol < 0.0) return fail(TCA_ERR_INVALID_ARG, "tca_jacobi_solve: threshold must be >= 0");
@@ -1322,8 +1385,8 @@ tca_status tca_precond_apply(tca_operator *op, const void *r, void *z, void *str
 {
     TCA_TRY(check_op(op));
     if (!r || !z) return fail(TCA_ERR_INVALID_ARG, "r and z must be non-NULL device pointers");
-    if (op->nranks > 1)
-        return fail(TCA_ERR_INVALID_ARG, "tca_precond_apply: not available on a sharded operator");
+    if (op->nranks > 1 || op->scat)
+        return fail(TCA_ERR_INVALID_ARG, "tca_precond_apply: not available on a sharded or scattered-data operator");
     cudaStream_t s = (cudaStream_t)stream;
     TCA_TRY(precond_prepare(op, s));
     if (op->dtype == TCA_F64) return apply_precond<double>(op, (const double *)r, (double *)z, nullptr, s);
@@ -1333,8 +1396,8 @@ tca_status tca_precond_apply(tca_operator *op, const void *r, void *z, void *str
 tca_status tca_precond_info(tca_operator *op, double *eps, int *lower_bandwidth, void *stream)
 {
     TCA_TRY(check_op(op));
-    if (op->nranks > 1)
-        return fail(TCA_ERR_INVALID_ARG, "tca_precond_info: not available on a sharded operator");
+    if (op->nranks > 1 || op->scat)
+        return fail(TCA_ERR_INVALID_ARG, "tca_precond_info: not available on a sharded or scattered-data operator");
     TCA_TRY(precond_prepare(op, (cudaStream_t)stream));
     for (int d = 0; d < op->order; ++d) {
         if (eps) eps[d] = op->pc_eps[d];
@@ -1464,8 +1527,29 @@ tca_status tca_forward_model(const tca_operator *op, const void *x, void *ydata,
                              uint64_t seed, void *stream)
 {
     TCA_TRY(check_op(op));
-    if (op->gram_form) return fail(TCA_ERR_INVALID_ARG, "tca_forward_model: operator was created from its factors");
     if (!ydata) return fail(TCA_ERR_INVALID_ARG, "ydata is NULL");
+    if (op->scat) {   // y_k = <w_k, x> + sigma noise_k (x NULL: x_true of the seed)
+        cudaStream_t s = (cudaStream_t)stream;
+        void *xt = nullptr;
+        if (!x) {
+            TCA_CUDA_TRY(cudaMallocAsync(&xt, std::max<int64_t>(op->N, 1) * op->esize, s));
+            if (op->dtype == TCA_F64) launch_gen_normal<double>((double *)xt, op->N, 0, stream_key(seed, 0), 1.0, false, s);
+            else launch_gen_normal<float>((float *)xt, op->N, 0, stream_key(seed, 0), 1.0, false, s);
+            x = xt;
+        }
+        TCA_CUDA_TRY(cudaMemsetAsync(ydata, 0, (size_t)op->sc_K * op->esize, s));
+        TCA_TRY(launch_scatter(op, 2, x, ydata, nullptr, nullptr, s));
+        if (sigma != 0.0) {
+            if (op->dtype == TCA_F64)
+                launch_gen_normal<double>((double *)ydata, op->sc_K, 0, stream_key(seed, 1), sigma, true, s);
+            else
+                launch_gen_normal<float>((float *)ydata, op->sc_K, 0, stream_key(seed, 1), sigma, true, s);
+        }
+        if (xt) TCA_CUDA_TRY(cudaFreeAsync(xt, s));
+        TCA_CUDA_TRY(cudaGetLastError());
+        return TCA_OK;
+    }
+    if (op->gram_form) return fail(TCA_ERR_INVALID_ARG, "tca_forward_model: operator was created from its factors");
     if (op->nranks > 1 && x) return fail(TCA_ERR_INVALID_ARG, "sharded forward model takes x = NULL");
     cudaStream_t s = (cudaStream_t)stream;
     if (op->dtype == TCA_F64) TCA_TRY(forward_t<double>(op, (const double *)x, (double *)ydata, sigma, seed, s));

@@ -96,6 +96,16 @@ struct alignas(64) TmapSlot {
 };
 constexpr int kTmapSlots = 32;
 
+// Scattered-data operator geometry (tca_scatter.cu): 4 internal modes (orders
+// D < 4 padded in front with size-1 modes), tiles of TB cells along modes 1-3.
+struct ScatGeom {
+    int n[4];      // internal extents
+    int real[4];   // 1: B-spline mode, 0: padded mode (weight 1)
+    int TB;        // cells per tile along the real modes among 1-3
+    int nt[3];     // tiles along modes 1-3
+    int F[4];      // shared-memory footprint extents (TB+3 | 1, n4+3)
+};
+
 }  // namespace tca
 
 struct tca_operator {
@@ -175,6 +185,13 @@ struct tca_operator {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int num_sms = 148;
     int band_grid = 0;                   // persistent grid of the fused banded apply
+    // scattered-data operator (tca_operator_create_scattered): sample term on top
+    // of the Kronecker-sum regulariser (apply_path 2)
+    bool scat = false;
+    tca::ScatGeom sg{};
+    int64_t sc_K = 0;
+    int sc_ntiles = 0;
+    void *sc_t = nullptr, *sc_perm = nullptr, *sc_tstart = nullptr;   // samples bucketed by tile
     // fused CG step B1' (apply that also forms P_new and updates C): its own
     // parameter block and schedule (whole tile columns: every CTA at the same
     // mode-1 slab, so the halo re-reads hit L2), two P buffers (P_old is read
@@ -234,6 +251,9 @@ template <typename T>
 void launch_dot_partials(const T *a, const T *b, int64_t N, double *part,
                          const int32_t *done, cudaStream_t s);
 tca_status precond_prepare(tca_operator *op, cudaStream_t s);
+tca_status scatter_prepare(tca_operator *op, int64_t K, const double *t, cudaStream_t s);
+tca_status launch_scatter(const tca_operator *op, int mode, const void *x, void *out, const void *yk,
+                          const int32_t *done, cudaStream_t s);
 // process-wide free list of small pinned host buffers (tca_abi.cu)
 void *pinned_get(size_t bytes);
 // process-wide free list of small device buffers (tca_abi.cu)

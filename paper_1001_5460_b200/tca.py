@@ -29,7 +29,7 @@ EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
             "tca_cg_solve", "tca_solve_host", "tca_solve_host_batch", "tca_operator_destroy", "tca_generate_normal",
             "tca_forward_model", "tca_status_string", "tca_last_error", "tca_version",
             "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches",
-            "tca_operator_apply_path", "tca_operator_cg_fused_step", "tca_shard_layout", "tca_nccl_get_unique_id",
+            "tca_operator_apply_path", "tca_operator_cg_fused_step", "tca_operator_create_scattered", "tca_shard_layout", "tca_nccl_get_unique_id",
             "tca_nccl_comm_create", "tca_nccl_comm_destroy", "tca_local_group_create",
             "tca_local_group_destroy", "tca_pcg_solve", "tca_precond_apply", "tca_precond_info",
             "tca_cgsr_solve", "tca_operator_create_gram", "tca_jacobi_solve"]
@@ -104,6 +104,9 @@ _lib.tca_jacobi_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32
 _lib.tca_operator_create_gram.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _i64p, _dpp, _dpp, ctypes.c_double,
                                           ctypes.c_int, _vp, _vp]
 _lib.tca_precond_info.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), _vp]
+_lib.tca_operator_create_scattered.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _i64p, ctypes.c_int64,
+                                               ctypes.POINTER(ctypes.c_double),
+                                               _dpp, ctypes.c_double, ctypes.c_int, _vp]
 _lib.tca_operator_apply_path.restype = ctypes.c_int
 for _name in ("tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
               "tca_cg_solve", "tca_solve_host", "tca_solve_host_batch", "tca_generate_normal", "tca_forward_model",
@@ -225,6 +228,38 @@ class Operator:
                                            _vp(_stream_ptr(stream)))
         _check(st, "tca_operator_create_gram")
         self._finish()
+        return self
+
+    @classmethod
+    def scattered(cls, n, t, L=None, lam=0.0, dtype="f64", stream=None):
+        """Scattered-data operator (tca_operator_create_scattered, reading Z27):
+        M x = sum_k w_k <w_k, x> + lam sum_d (mode-d L_d^T L_d) x for the K x D
+        sample coordinates t (grid units, in [0, n_d - 1]).  Its "data" are the K
+        sample values: rhs / forward_model / solve_host use shape (K,)."""
+        self = cls.__new__(cls)
+        self._h = _vp()
+        n = tuple(int(v) for v in n)
+        D = len(n)
+        t = np.ascontiguousarray(t, dtype=np.float64).reshape(-1, D)
+        K = t.shape[0]
+        self.order = D
+        self.n = n
+        self.lam = float(lam)
+        self.dtype_code = _dtype_code(dtype)
+        self.dtype = "f64" if self.dtype_code == TCA_F64 else "f32"
+        dp = ctypes.POINTER(ctypes.c_double)
+        Ls = None if L is None else [None if l is None else np.ascontiguousarray(l, dtype=np.float64) for l in L]
+        L_arr = None if Ls is None else (dp * D)(*[ctypes.cast(None, dp) if l is None else l.ctypes.data_as(dp)
+                                                   for l in Ls])
+        n_arr = (ctypes.c_int64 * D)(*n)
+        st = _lib.tca_operator_create_scattered(ctypes.byref(self._h), D, n_arr, K, t.ctypes.data_as(dp), L_arr,
+                                                self.lam, self.dtype_code, _vp(_stream_ptr(stream)))
+        _check(st, "tca_operator_create_scattered")
+        self.m = (K,)
+        self._finish()
+        self.K = K
+        self.local_m = (K,)
+        self.Mloc = K
         return self
 
     def _finish(self):
