@@ -881,7 +881,7 @@ void tca_operator_destroy(tca_operator *op)
     // every stream that used the operator is done before its memory goes back
     cudaDeviceSynchronize();
     void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp, op->sr_s, op->p2,
-                      op->jac_e, op->sc_t, op->sc_perm, op->sc_tstart};   // stream-ordered pool
+                      op->jac_e, op->sc_t, op->sc_perm, op->sc_tstart, op->sc_coef};   // stream-ordered pool
     for (void *b : pooled)
         if (b) cudaFreeAsync(b, 0);
     dev_put(op->part, sizeof(double) * kRedBlocks * 2);

@@ -192,6 +192,7 @@ struct tca_operator {
     int64_t sc_K = 0;
     int sc_ntiles = 0;
     void *sc_t = nullptr, *sc_perm = nullptr, *sc_tstart = nullptr;   // samples bucketed by tile
+    void *sc_coef = nullptr;             // <w_k, x> per sorted sample (apply scratch)
     // fused CG step B1' (apply that also forms P_new and updates C): its own
     // parameter block and schedule (whole tile columns: every CTA at the same
     // mode-1 slab, so the halo re-reads hit L2), two P buffers (P_old is read

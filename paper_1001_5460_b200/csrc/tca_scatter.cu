@@ -11,11 +11,11 @@
 // tile of coefficient cells they fall in -- TB x TB x TB cells of modes 1-3, the
 // whole of mode 4.  One CTA per non-empty tile stages the tile's coefficient
 // footprint (TB+3 per tiled mode, n4+3 along mode 4, zero outside the domain)
-// in shared memory, runs one sample per warp (each lane two of the 4x4x4
-// (i1,i2,i3) support rows, 4 contiguous i4 taps each): gather <w_k, x> from
-// shared memory, warp reduction, scatter-add into a shared accumulator (fp64
-// shared-memory atomics), and adds the accumulator to HBM once per tile with
-// global atomics (footprints of neighbouring tiles overlap by 3 cells).
+// in shared memory, runs one sample per thread (its 4 x 4 B-spline weights in
+// registers): gather <w_k, x> from shared memory, scatter-add into a shared
+// accumulator (fp64 shared-memory atomics), and adds the accumulator to HBM
+// once per tile with global atomics (footprints of neighbouring tiles overlap
+// by 3 cells).
 // Orders D < 4 run as 4-mode problems with leading size-1 modes whose weight
 // is 1 (not a B-spline).
 #include <algorithm>
@@ -30,31 +30,15 @@ namespace {
 
 constexpr int kScatThreads = 256;
 
-__device__ __forceinline__ double beta3(double u)
-{
-    u = fabs(u);
-    if (u < 1.0) return 2.0 / 3.0 - u * u + 0.5 * u * u * u;
-    if (u < 2.0) {
-        const double v = 2.0 - u;
-        return v * v * v * (1.0 / 6.0);
-    }
-    return 0.0;
-}
-
-__device__ __forceinline__ double warp_sum(double v)
-{
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
 // MODE 0: out += data term of x; 1: out += sum_k yk[perm] w_k (rhs); 2: out[perm[k]] = <w_k, x>
-template <typename T, int MODE>
+// FULL: all four modes are B-spline modes (order 4): compile-time support loops
+template <typename T, int MODE, bool FULL>
 __global__ void __launch_bounds__(kScatThreads)
 scatter_kernel(ScatGeom g, const double4 *__restrict__ ts, const int *__restrict__ perm,
                const int *__restrict__ tstart, const T *__restrict__ x, T *__restrict__ out,
-               const T *__restrict__ yk, const int32_t *done)
+               const T *__restrict__ yk, const int32_t *done, double *__restrict__ coefg)
 {
+#define RL(d) (FULL || g.real[d])
     if (done && *done) return;
     const int tile = blockIdx.x;
     const int s0 = tstart[tile], s1 = tstart[tile + 1];
@@ -62,89 +46,160 @@ scatter_kernel(ScatGeom g, const double4 *__restrict__ ts, const int *__restrict
     extern __shared__ __align__(16) unsigned char scat_smem[];
     T *xs = reinterpret_cast<T *>(scat_smem);
     const int FP = g.F[0] * g.F[1] * g.F[2] * g.F[3];
-    T *qs = xs + (MODE == 1 ? 0 : FP);
+    T *qs = xs;   // one footprint buffer: x for the gather, then the accumulator
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int tc2 = tile % g.nt[2], tc1 = (tile / g.nt[2]) % g.nt[1], tc0 = tile / (g.nt[2] * g.nt[1]);
     // footprint origin (coefficient index of footprint index 0) per mode
-    const int lo[4] = {g.real[0] ? tc0 * g.TB - 1 : 0, g.real[1] ? tc1 * g.TB - 1 : 0,
-                       g.real[2] ? tc2 * g.TB - 1 : 0, -1};
+    const int lo[4] = {RL(0) ? tc0 * g.TB - 1 : 0, RL(1) ? tc1 * g.TB - 1 : 0,
+                       RL(2) ? tc2 * g.TB - 1 : 0, -1};
     const int64_t st3 = g.n[3], st2 = (int64_t)g.n[2] * st3, st1 = (int64_t)g.n[1] * st2;
-    for (int f = tid; f < FP; f += kScatThreads) {
-        const int f3 = f % g.F[3], f2 = (f / g.F[3]) % g.F[2], f1 = (f / (g.F[3] * g.F[2])) % g.F[1],
-                  f0 = f / (g.F[3] * g.F[2] * g.F[1]);
-        const int i0 = lo[0] + f0, i1 = lo[1] + f1, i2 = lo[2] + f2, i3 = lo[3] + f3;
-        const bool in = i0 >= 0 && i0 < g.n[0] && i1 >= 0 && i1 < g.n[1] && i2 >= 0 && i2 < g.n[2] && i3 >= 0 &&
-                        i3 < g.n[3];
-        if (MODE != 1) xs[f] = in ? x[i0 * st1 + i1 * st2 + i2 * st3 + i3] : T(0);
-        if (MODE != 2) qs[f] = T(0);
+    // footprint rows (f0, f1, f2) one warp each, lanes along mode 4 (no divisions per element)
+    const int N12 = g.F[1] * g.F[2];
+    for (int r12 = warp; r12 < N12; r12 += kScatThreads / 32) {   // one division pair per (f1, f2)
+        const int f1 = r12 / g.F[2], f2 = r12 - f1 * g.F[2];
+        const int i1 = lo[1] + f1, i2 = lo[2] + f2;
+        const bool in12 = i1 >= 0 && i1 < g.n[1] && i2 >= 0 && i2 < g.n[2];
+        for (int f0 = 0; f0 < g.F[0]; ++f0) {
+            const int i0 = lo[0] + f0, row = f0 * N12 + r12;
+            const bool rin = in12 && i0 >= 0 && i0 < g.n[0];
+            const T *xr = x + (rin ? i0 * st1 + i1 * st2 + i2 * st3 : 0);
+            for (int f3 = lane; f3 < g.F[3]; f3 += 32) {
+                const int i3 = f3 - 1;
+                if (MODE != 1) xs[row * g.F[3] + f3] = (rin && i3 >= 0 && i3 < g.n[3]) ? xr[i3] : T(0);
+                if (MODE == 1) qs[row * g.F[3] + f3] = T(0);
+            }
+        }
     }
     __syncthreads();
-    // lane -> support rows (j0, j1, j2) and (j0 + 2, j1, j2) of the 4x4x4 rows;
-    // absent modes use row 0 only (weight 1)
+    // Samples in chunks of kScatThreads: (1) gather, one sample per thread (its
+    // 4 x 4 B-spline weights in registers, the 4^D support read from shared
+    // memory) -> coefficient in shared memory; (2) scatter, one sample per warp,
+    // each lane two of the 4x4x4 (i1,i2,i3) support rows x 4 i4 taps, so a
+    // warp's 32 shared-memory atomics of one instruction never collide.
+    const int J0 = RL(0) ? 4 : 1, J1 = RL(1) ? 4 : 1, J2 = RL(2) ? 4 : 1;
+    const int S2 = g.F[3], S1 = g.F[2] * S2, S0 = g.F[1] * S1;
+    double *coefs = coefg;   // per sorted sample (apply); rhs reads yk directly
     const int ja = lane >> 4, jb = (lane >> 2) & 3, jc = lane & 3;
-    for (int s = s0 + warp; s < s1; s += kScatThreads / 32) {
-        const double4 tt = ts[s];
-        const double tv[4] = {tt.x, tt.y, tt.z, tt.w};
-        int fb[4];
-        double wa, wb, w1, w2, w3[4];
+    for (int c0s = s0; c0s < s1; c0s += kScatThreads) {
+        const int cn = min(kScatThreads, s1 - c0s);
+        if (MODE != 1 && tid < cn) {   // <w_k, x>
+            const int s = c0s + tid;
+            const double4 tt = ts[s];
+            const double tv[4] = {tt.x, tt.y, tt.z, tt.w};
+            double w[4][4];
+            int o = 0;
 #pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            const int c = (int)floor(tv[d]);
-            fb[d] = g.real[d] ? c - 1 - lo[d] : 0;   // footprint index of support row 0
-        }
-        {
-            const double c0 = floor(tv[0]), c1 = floor(tv[1]), c2 = floor(tv[2]), c3 = floor(tv[3]);
-            wa = g.real[0] ? beta3(tv[0] - (c0 - 1.0 + ja)) : (ja == 0 ? 1.0 : 0.0);
-            wb = g.real[0] ? beta3(tv[0] - (c0 + 1.0 + ja)) : 0.0;
-            w1 = g.real[1] ? beta3(tv[1] - (c1 - 1.0 + jb)) : (jb == 0 ? 1.0 : 0.0);
-            w2 = g.real[2] ? beta3(tv[2] - (c2 - 1.0 + jc)) : (jc == 0 ? 1.0 : 0.0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) w3[j] = beta3(tv[3] - (c3 - 1.0 + j));
-        }
-        // footprint offsets of the lane's two rows (absent modes: row 0 only)
-        const int r1 = g.real[1] ? jb : 0, r2 = g.real[2] ? jc : 0;
-        const int ra = g.real[0] ? ja : 0, rb = g.real[0] ? ja + 2 : 0;
-        const int base12 = ((fb[1] + r1) * g.F[2] + fb[2] + r2) * g.F[3] + fb[3];
-        const int oa = (fb[0] + ra) * g.F[1] * g.F[2] * g.F[3] + base12;
-        const int ob = (fb[0] + rb) * g.F[1] * g.F[2] * g.F[3] + base12;
-        const double pa = wa * w1 * w2, pb = wb * w1 * w2;
-        double coef;
-        if (MODE != 1) {
-            double sa = 0.0, sb = 0.0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                sa = fma(w3[j], (double)xs[oa + j], sa);
-                sb = fma(w3[j], (double)xs[ob + j], sb);
+            for (int d = 0; d < 4; ++d) {
+                const double c = floor(tv[d]);
+                if (RL(d)) {
+                    // cubic B-spline blending functions of u = t - floor(t):
+                    // beta3(u+1), beta3(u), beta3(1-u), beta3(2-u) (rows c-1 .. c+2)
+                    const double u = tv[d] - c, u2 = u * u, u3 = u2 * u, v = 1.0 - u;
+                    w[d][0] = v * v * v * (1.0 / 6.0);
+                    w[d][1] = fma(0.5, u3, 2.0 / 3.0 - u2);
+                    w[d][2] = fma(-0.5, u3, fma(0.5, u2, fma(0.5, u, 1.0 / 6.0)));
+                    w[d][3] = u3 * (1.0 / 6.0);
+                } else {
+                    w[d][0] = 1.0;
+                    w[d][1] = w[d][2] = w[d][3] = 0.0;
+                }
+                const int fbd = RL(d) ? (int)c - 1 - lo[d] : 0;   // footprint index of support row 0
+                o += fbd * (d == 0 ? S0 : d == 1 ? S1 : d == 2 ? S2 : 1);
             }
-            coef = warp_sum(fma(pa, sa, pb * sb));   // <w_k, x>
-            if (MODE == 2) {
-                if (lane == 0) out[perm[s]] = (T)coef;
-                continue;
+            double acc = 0.0;
+#pragma unroll
+            for (int j0 = 0; j0 < 4; ++j0) {
+                if (j0 >= J0) break;
+#pragma unroll
+                for (int j1 = 0; j1 < 4; ++j1) {
+                    if (j1 >= J1) break;
+                    const double p01 = w[0][j0] * w[1][j1];
+#pragma unroll
+                    for (int j2 = 0; j2 < 4; ++j2) {
+                        if (j2 >= J2) break;
+                        const T *xr = xs + o + j0 * S0 + j1 * S1 + j2 * S2;
+                        double r = 0.0;
+#pragma unroll
+                        for (int j3 = 0; j3 < 4; ++j3) r = fma(w[3][j3], (double)xr[j3], r);
+                        acc = fma(p01 * w[2][j2], r, acc);
+                    }
+                }
             }
-        } else {
-            coef = (double)yk[perm[s]];
+            if (MODE == 2) out[perm[s]] = (T)acc;
+            else coefs[s] = acc;
         }
-        const double ca = coef * pa, cb = coef * pb;
-        if (ca != 0.0) {
+    }
+    if (MODE == 2) return;
+    if (MODE == 0) {   // the footprint buffer becomes the accumulator
+        __syncthreads();
+        for (int f = tid; f < FP; f += kScatThreads) qs[f] = T(0);
+        __syncthreads();
+    }
+    for (int c0s = s0; c0s < s1; c0s += kScatThreads) {
+        const int cn = min(kScatThreads, s1 - c0s);
+        for (int i = warp; i < cn; i += kScatThreads / 32) {
+            const double coef = MODE == 0 ? coefs[c0s + i] : (double)yk[perm[c0s + i]];
+            if (coef == 0.0) continue;
+            const double4 tt = ts[c0s + i];
+            const double tv[4] = {tt.x, tt.y, tt.z, tt.w};
+            int fb[4];
+            double wsel[3][2], w3[4];
+            const int jsel[3][2] = {{ja, ja + 2}, {jb, jb}, {jc, jc}};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) atomicAdd(&qs[oa + j], (T)(ca * w3[j]));
-        }
-        if (cb != 0.0) {
+            for (int d = 0; d < 4; ++d) {
+                const double c = floor(tv[d]);
+                fb[d] = RL(d) ? (int)c - 1 - lo[d] : 0;
+                const double u = tv[d] - c, u2 = u * u, u3 = u2 * u, v = 1.0 - u;
+                const double bl[4] = {v * v * v * (1.0 / 6.0), fma(0.5, u3, 2.0 / 3.0 - u2),
+                                      fma(-0.5, u3, fma(0.5, u2, fma(0.5, u, 1.0 / 6.0))), u3 * (1.0 / 6.0)};
+                if (d == 3) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) atomicAdd(&qs[ob + j], (T)(cb * w3[j]));
+                    for (int j = 0; j < 4; ++j) w3[j] = bl[j];
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int j = jsel[d][h];
+                        // select without local-memory indexing
+                        const double bj = j == 0 ? bl[0] : j == 1 ? bl[1] : j == 2 ? bl[2] : bl[3];
+                        wsel[d][h] = RL(d) ? bj : (j == 0 ? 1.0 : 0.0);
+                    }
+                }
+            }
+            const int r1 = RL(1) ? jb : 0, r2 = RL(2) ? jc : 0;
+            const int ra = RL(0) ? ja : 0, rb = RL(0) ? ja + 2 : 0;
+            const int base12 = (fb[1] + r1) * S1 + (fb[2] + r2) * S2 + fb[3];
+            const double p12 = coef * wsel[1][0] * wsel[2][0];
+            const double ca = p12 * wsel[0][0], cb = RL(0) ? p12 * wsel[0][1] : 0.0;
+            if (ca != 0.0) {
+                T *qa = qs + (fb[0] + ra) * S0 + base12;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) atomicAdd(&qa[j], (T)(ca * w3[j]));
+            }
+            if (cb != 0.0) {
+                T *qb = qs + (fb[0] + rb) * S0 + base12;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) atomicAdd(&qb[j], (T)(cb * w3[j]));
+            }
         }
     }
     if (MODE == 2) return;
     __syncthreads();
-    for (int f = tid; f < FP; f += kScatThreads) {
-        const T v = qs[f];
-        if (v == T(0)) continue;
-        const int f3 = f % g.F[3], f2 = (f / g.F[3]) % g.F[2], f1 = (f / (g.F[3] * g.F[2])) % g.F[1],
-                  f0 = f / (g.F[3] * g.F[2] * g.F[1]);
-        const int i0 = lo[0] + f0, i1 = lo[1] + f1, i2 = lo[2] + f2, i3 = lo[3] + f3;
-        if (i0 >= 0 && i0 < g.n[0] && i1 >= 0 && i1 < g.n[1] && i2 >= 0 && i2 < g.n[2] && i3 >= 0 && i3 < g.n[3])
-            atomicAdd(&out[i0 * st1 + i1 * st2 + i2 * st3 + i3], v);
+    for (int r12 = warp; r12 < N12; r12 += kScatThreads / 32) {
+        const int f1 = r12 / g.F[2], f2 = r12 - f1 * g.F[2];
+        const int i1 = lo[1] + f1, i2 = lo[2] + f2;
+        if (!(i1 >= 0 && i1 < g.n[1] && i2 >= 0 && i2 < g.n[2])) continue;
+        for (int f0 = 0; f0 < g.F[0]; ++f0) {
+            const int i0 = lo[0] + f0, row = f0 * N12 + r12;
+            if (i0 < 0 || i0 >= g.n[0]) continue;
+            T *orow = out + i0 * st1 + i1 * st2 + i2 * st3;
+            for (int f3 = lane; f3 < g.F[3]; f3 += 32) {
+                const int i3 = f3 - 1;
+                const T v = qs[row * g.F[3] + f3];
+                if (v != T(0) && i3 >= 0 && i3 < g.n[3]) atomicAdd(&orow[i3], v);
+            }
+        }
     }
+#undef RL
 }
 
 template <typename T, int MODE>
@@ -153,17 +208,18 @@ tca_status launch_mode(const tca_operator *op, const void *x, void *out, const v
 {
     const ScatGeom &g = op->sg;
     const size_t fp = (size_t)g.F[0] * g.F[1] * g.F[2] * g.F[3];
-    const size_t smem = fp * sizeof(T) * (MODE == 0 ? 2 : 1);
-    static size_t attr = 0;
-    if (smem > attr) {
-        TCA_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
-        attr = smem;
+    const size_t smem = fp * sizeof(T);
+    const bool full = op->order == 4;
+    static size_t attr[2] = {0, 0};
+    if (smem > attr[full]) {
+        TCA_CUDA_TRY(cudaFuncSetAttribute(full ? scatter_kernel<T, MODE, true> : scatter_kernel<T, MODE, false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[full] = smem;
     }
     count_launch();
-    scatter_kernel<T, MODE><<<(unsigned)op->sc_ntiles, kScatThreads, smem, s>>>(
+    (full ? scatter_kernel<T, MODE, true> : scatter_kernel<T, MODE, false>)<<<(unsigned)op->sc_ntiles, kScatThreads, smem, s>>>(
         g, (const double4 *)op->sc_t, (const int *)op->sc_perm, (const int *)op->sc_tstart, (const T *)x, (T *)out,
-        (const T *)yk, done);
+        (const T *)yk, done, (double *)op->sc_coef);
     TCA_CUDA_TRY(cudaGetLastError());
     return TCA_OK;
 }
@@ -189,7 +245,7 @@ tca_status scatter_prepare(tca_operator *op, int64_t K, const double *t, cudaStr
         for (int tb : {4, 2, 1}) {
             size_t fp = (size_t)(g.n[3] + 3);
             for (int d = 0; d < 3; ++d) fp *= g.real[d] ? (size_t)(tb + 3) : 1;
-            if (fp * es * 2 <= (size_t)cap) { TB = tb; break; }
+            if (fp * es <= (size_t)cap / 2) { TB = tb; break; }
         }
         if (TB) break;
     }
@@ -236,6 +292,7 @@ tca_status scatter_prepare(tca_operator *op, int64_t K, const double *t, cudaStr
     TCA_CUDA_TRY(cudaMallocAsync(&op->sc_t, bt, s));
     TCA_CUDA_TRY(cudaMallocAsync(&op->sc_perm, bp, s));
     TCA_CUDA_TRY(cudaMallocAsync(&op->sc_tstart, bs, s));
+    TCA_CUDA_TRY(cudaMallocAsync(&op->sc_coef, std::max<size_t>(perm.size(), 1) * sizeof(double), s));
     if (K > 0) {
         TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_t, ts.data(), ts.size() * sizeof(double), cudaMemcpyHostToDevice, s));
         TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_perm, perm.data(), perm.size() * sizeof(int), cudaMemcpyHostToDevice, s));
