@@ -51,9 +51,11 @@ def parse():
                     help="pcg: CG with the Kronecker-factor preconditioner (tca_pcg_solve); "
                          "cgsr: single-reduction CG (tca_cgsr_solve)")
     ap.add_argument("--rtol", type=float, default=None, help="override the config's stop rule")
-    ap.add_argument("--workload", default="fit", choices=["fit", "poisson"],
+    ap.add_argument("--workload", default="fit", choices=["fit", "poisson", "scattered"],
                     help="poisson: Fig. 1c's separable Poisson system 128x129x130 (Eq. 9) with tensor "
-                         "Jacobi (--solver jacobi, threshold --rtol, default 1e-4) or CG")
+                         "Jacobi (--solver jacobi, threshold --rtol, default 1e-4) or CG; scattered: Sec. 4's "
+                         "spline reconstruction from 9e6 scattered samples on 128x128x128x16")
+    ap.add_argument("--samples", type=int, default=None, help="scattered workload: sample count (default 9e6)")
     return ap.parse_args()
 
 
@@ -508,12 +510,93 @@ def run_poisson(args):
     return 0
 
 
+def run_scattered(args):
+    """Sec. 4 workload (reading Z27): spline reconstruction from
+    scattered samples on the paper's 128x128x128x16 grid with 9e6 samples
+    (uniform synthetic coordinates, y = W x_true + N(0, 0.01^2) formed on the GPU
+    by the forward model).  One GPU; a step = create (bucketing + upload of the
+    samples) + rhs + CG + destroy."""
+    import torch
+    from paper_1001_5460_b200 import tca
+    n = synth.SCATTER_SHAPE
+    K = args.samples or synth.SCATTER_K
+    dtype = args.dtype
+    t = synth.scattered_positions(n, K, seed=1)
+    L = [synth.second_difference(k) for k in n]
+    lam = 1e-3
+    iters = args.iters or 100
+    rtol = args.rtol if args.rtol is not None else 0.0
+    op0 = tca.Operator.scattered(n, t, L, lam, dtype=dtype)
+    yk = op0.forward_model(None, sigma=synth.NOISE_SIGMA, seed=1)   # y = W x_true + noise
+    op0.close()
+    stream = torch.cuda.current_stream()
+    state = {}
+
+    def step(timing=False):
+        h0 = time.perf_counter()
+        op = tca.Operator.scattered(n, t, L, lam, dtype=dtype)
+        torch.cuda.synchronize()
+        state["create_ms"] = state.get("create_ms", 0.0) + 1e3 * (time.perf_counter() - h0)
+        if timing:
+            op.set_timing(True)
+        b = op.rhs(yk)
+        x, rep = op.cg_solve(b, rtol=rtol, max_iters=iters)
+        if timing:
+            ms_, cnt = op.get_timing()
+            state["apply_ms"] = state.get("apply_ms", 0.0) + ms_
+            state["apply_cnt"] = state.get("apply_cnt", 0) + cnt
+        state["iters"] = state.get("iters", 0) + rep["iterations"]
+        state["cg_ms"] = state.get("cg_ms", 0.0) + rep["seconds"] * 1e3
+        state["rep"] = rep
+        op.close()
+
+    for _ in range(args.warmup):
+        step()
+    state.clear()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(timing=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    esize = 8 if dtype == "f64" else 4
+    N = int(np.prod(n))
+    apply_us = 1e3 * state["apply_ms"] / max(1, state["apply_cnt"])
+    hbm, src = peaks()
+    abytes = 2 * N * esize + K * (32 + 4 + 16)   # x in, q out; per sample coordinates, index, coefficient scratch
+    rep = state["rep"]
+    line = {"metric": "CG iterations/s, Sec. 4 scattered-data spline reconstruction", "value": state["iters"] / (ms * 1e-3),
+            "unit": "CG iters/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "dtype": dtype,
+            "data": "synthetic: uniform sample coordinates (stream 6), y = W x_true + N(0, 0.01^2) (the paper's "
+                    "measurements are not available)",
+            "config": {"workload": "Sec. 4: 128x128x128x16 cubic B-spline grid, 9e6 scattered samples, lambda 1e-3, "
+                                   "second-difference regulariser", "samples": K, "unknowns": N,
+                       "cg_iters_per_step": iters, "step": "create + rhs + CG + destroy"},
+            "roofline": {"bound": "hbm", "achieved": abytes / (apply_us * 1e-6) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": abytes / (apply_us * 1e-6) / 1e9 / hbm, "us_per_launch": apply_us,
+                         "bytes_per_launch": abytes, "peak_source": src,
+                         "note": "instruction-issue bound (shared-memory CAS atomics of the sample scatter); "
+                                 "see DESIGN.md 6.6"},
+            "apply": {"us": apply_us, "ns_per_sample": 1e3 * apply_us / K, "samples_per_s": K / (apply_us * 1e-6)},
+            "phases": {"create_ms": state["create_ms"] / args.steps, "cg_ms": state["cg_ms"] / args.steps,
+                       "cg_us_per_iteration": 1e3 * state["cg_ms"] / max(1, state["iters"])},
+            "report": {"iterations": rep["iterations"], "converged": rep["converged"], "rho0": rep["rho0"],
+                       "rho_final": rep["rho_final"]}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "poisson":
         return run_poisson(args)
+    if args.workload == "scattered":
+        return run_scattered(args)
     return run_tca(args)
 
 
