@@ -286,8 +286,8 @@ def run_tca(args):
 
     clocks = ClockSampler(dev_index)   # sampling from before the warm-up: no idle gap before timing
     clocks.start()
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):   # the last warm-up step also takes the timed path (event-pair graphs)
+        step(timing=i == args.warmup - 1)
     state.clear()
     barrier()
     t_wall0 = time.time()
