@@ -194,8 +194,11 @@ tca_status tca_operator_create_scattered(tca_operator **op, int order,
  * 8(a) a5): ONE kernel per iteration forms P := R|Z + beta P,
  * applies the pending C := C + alpha P and computes Q = M P with <P, Q>
  * (reads R|Z, P, C; writes P, C, Q), instead of a separate update pass.
- * 1 = yes, 0 = no (sharded operator, non-fused apply path, tables outside the
- * parameter block, or the TCA_NO_B1 environment switch), -1 = not decided yet
+ * Opt-in: used only when the environment has TCA_B1=1 at the operator's first
+ * solve (measured slower than the default three-kernel iteration on config 3,
+ * DESIGN.md 6.5).  1 = yes, 0 = no (not requested, sharded operator, non-fused
+ * apply path, tables outside the parameter block, or a shape whose shared-
+ * memory plan does not fit: fp64 n4 = 16, 32), -1 = not decided yet
  * (no CG solve so far) or op NULL.  Results are the same iterates either way. */
 int tca_operator_cg_fused_step(const tca_operator *op);
 

@@ -302,7 +302,7 @@ tca_status launch_precond_sweep(const tca_operator *op, int d, const T *src, T *
     {
         const size_t es = sizeof(T);
         // ~3 tiles per SM; all 256 threads move a tile, LB of them sweep it
-        int LB = (int)((72 * 1024 / es - 8 * (size_t)len) / (len + 2));
+        int LB = (int)((75 * 1024 / es - 8 * (size_t)len) / (len + 2));
         LB = std::min(256, LB / 32 * 32);
         while (LB > 32 && 256 % LB) LB -= 32;   // LB divides the 256 movers
         if (LB >= 32) {
