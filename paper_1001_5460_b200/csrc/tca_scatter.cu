@@ -18,6 +18,8 @@
 // by 3 cells).
 // Orders D < 4 run as 4-mode problems with leading size-1 modes whose weight
 // is 1 (not a B-spline).
+#include <stdlib.h>
+
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -250,6 +252,12 @@ tca_status scatter_prepare(tca_operator *op, int64_t K, const double *t, cudaStr
         if (TB) break;
     }
     if (!TB) return fail(TCA_ERR_SHAPE, "scattered operator: the last mode is too long for a shared-memory tile");
+    if (const char *e = getenv("TCA_SCAT_TB")) {   // measurement switch: force the tile width
+        const int tb = atoi(e);
+        size_t fp = (size_t)(g.n[3] + 3);
+        for (int d = 0; d < 3; ++d) fp *= g.real[d] ? (size_t)(tb + 3) : 1;
+        if (tb >= 1 && fp * es <= 227 * 1024) TB = tb;
+    }
     g.TB = TB;
     int64_t ntiles = 1;
     for (int d = 0; d < 3; ++d) {
