@@ -39,6 +39,12 @@
 
 #include "tca_internal.cuh"
 
+#include <type_traits>
+
+#ifndef TCA_RING_F2
+#define TCA_RING_F2 1   // fp32 mode-1 ring on FFMA2
+#endif
+
 #ifndef TCA_BAND_DBG
 #define TCA_BAND_DBG 1   // TCA_BAND_DEBUG phase switches compiled in
 #endif
@@ -348,6 +354,46 @@ __device__ __forceinline__ void ring_step(T (&acc)[6][E], const T (&s)[E], const
     for (int e = 0; e < E; ++e) acc[5][e] = g1[6] * s[e];               // o = +3: first term of output j+3
 }
 
+// fp32 shift ring on sm_100's packed FMA (FFMA2: two elements of a segment per
+// instruction, the mode-1 tap broadcast), same summation order as ring_step
+template <int E>
+__device__ __forceinline__ void ring_step_f2(float (&acc)[6][E], const float (&s)[E], const float (&q)[E],
+                                             const float (&pc)[E], const float (&g1)[7], const float (&r1)[5],
+                                             float (&ov)[E], bool dot, double &pq)
+{
+    static_assert(E % 2 == 0, "pairs");
+    float pd[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) pd[e] = dot ? pc[e] : 0.0f;
+#pragma unroll
+    for (int h = 0; h < E / 2; ++h) {
+        const float2 sh = make_float2(s[2 * h], s[2 * h + 1]), ph = make_float2(pc[2 * h], pc[2 * h + 1]);
+        const float2 o = __ffma2_rn(make_float2(g1[0], g1[0]), sh, make_float2(acc[0][2 * h], acc[0][2 * h + 1]));
+        ov[2 * h] = o.x;
+        ov[2 * h + 1] = o.y;
+#pragma unroll
+        for (int k = -2; k <= 2; ++k) {
+            float2 v = make_float2(acc[k + 3][2 * h], acc[k + 3][2 * h + 1]);
+            if (k == 0) {
+                pq = fma((double)pd[2 * h], (double)v.x, pq);
+                pq = fma((double)pd[2 * h + 1], (double)v.y, pq);
+            }
+            v = __ffma2_rn(make_float2(g1[k + 3], g1[k + 3]), sh, v);
+            v = __ffma2_rn(make_float2(r1[k + 2], r1[k + 2]), ph, v);
+            if (k == 0) {
+                v.x += q[2 * h];
+                v.y += q[2 * h + 1];
+                pq = fma((double)pd[2 * h], (double)v.x, pq);
+                pq = fma((double)pd[2 * h + 1], (double)v.y, pq);
+            }
+            acc[k + 2][2 * h] = v.x;
+            acc[k + 2][2 * h + 1] = v.y;
+        }
+        acc[5][2 * h] = g1[6] * s[2 * h];
+        acc[5][2 * h + 1] = g1[6] * s[2 * h + 1];
+    }
+}
+
 // Rotating form (fp64): output slab o lives in slot (o - j0) mod 6; at slab j
 // the slot of j-3 is emitted and reused for j+3; the rotation is a compile-time
 // parameter (6 copies of the code).  Measured on B200 (config 3): fp64 320 us
@@ -450,7 +496,9 @@ __device__ __forceinline__ void pass_c(const PA &a, T (&acc)[6][Cfg<T, N4>::E], 
     }
     T ov[E];
     const bool dot = a.pq_part != nullptr && j >= o0 && j < o1;   // input slab j is one of this CTA's
-    if constexpr (C::RING_SHIFT) {
+    if constexpr (C::RING_SHIFT && std::is_same<T, float>::value && E % 2 == 0 && TCA_RING_F2) {
+        ring_step_f2<E>(acc, s, q, pc, g1, r1, ov, dot, pq);
+    } else if constexpr (C::RING_SHIFT) {
         ring_step<T, E>(acc, s, q, pc, g1, r1, ov, dot, pq);
     } else {
         switch (rot) {
