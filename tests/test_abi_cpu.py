@@ -91,3 +91,37 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", src), f
+
+
+@pytest.mark.parametrize("case", ["t_above", "t_below", "t_nan", "neg_K", "null_t", "L_nan", "order0"])
+def test_create_scattered_validates_before_any_launch(case):
+    """tca_operator_create_scattered rejects bad input before touching the device
+    (so it runs without a GPU): sample coordinates outside [0, n_d - 1] or not
+    finite, K < 0, t NULL with K > 0, non-finite L, bad order."""
+    from paper_1001_5460_b200 import tca
+    dp = ctypes.POINTER(ctypes.c_double)
+    n = (6, 5, 4)
+    t = np.array([[1.0, 2.0, 3.0], [0.5, 0.5, 0.5]])
+    K, order = t.shape[0], 3
+    L = [np.eye(k - 2, k) for k in n]
+    if case == "t_above":
+        t[1, 2] = 3.5
+    elif case == "t_below":
+        t[0, 0] = -1e-9
+    elif case == "t_nan":
+        t[1, 1] = np.nan
+    elif case == "neg_K":
+        K = -1
+    elif case == "L_nan":
+        L[1] = L[1].copy()
+        L[1][0, 0] = np.inf
+    elif case == "order0":
+        order = 0
+    h = ctypes.c_void_p()
+    n_arr = (ctypes.c_int64 * 3)(*n)
+    L_arr = (dp * 3)(*[np.ascontiguousarray(l).ctypes.data_as(dp) for l in L])
+    tp = None if case == "null_t" else np.ascontiguousarray(t).ctypes.data_as(dp)
+    st = tca._lib.tca_operator_create_scattered(ctypes.byref(h), order, n_arr, K, tp, L_arr, 0.1, 0, None)
+    assert st == tca.ERR_INVALID_ARG
+    assert not h.value
+    assert tca._lib.tca_last_error().decode()

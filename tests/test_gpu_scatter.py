@@ -177,3 +177,21 @@ def test_scattered_paper_grid_sampled(tca):
         want = sub.data(x)[p] + reg[p]
         assert abs(y[p] - want) <= 1e-12 * max(1.0, abs(want))
     g.close()
+
+
+def test_scattered_host_batch(tca):
+    """Pipelined host solves (tca_solve_host_batch) on a scattered operator: K
+    sample values per item in, x out; each item equals its single solve."""
+    n, K, lam = (8, 7, 9, 16), 2500, 1e-2
+    t = samples(n, K)
+    L = [synth.second_difference(k) for k in n]
+    o = oracle.ScatteredOperator(n, t, L, lam)
+    g = tca.Operator.scattered(n, t, L, lam)
+    ys = [torch.from_numpy(o.forward(synth.random_tensor(n, seed=s))).contiguous().pin_memory() for s in (21, 22)]
+    xs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in ys]
+    reps = g.solve_host_batch(ys, xs, rtol=0.0, max_iters=30)
+    assert [r["iterations"] for r in reps] == [30, 30]
+    for y, x in zip(ys, xs):
+        xr, _, _, _ = o.cg(o.rhs(y.numpy()), rtol=0.0, max_iters=30)
+        assert rel(x.numpy(), xr) <= 1e-8
+    g.close()
