@@ -11,6 +11,7 @@
 #include <mutex>
 
 #include "tca_band_impl.cuh"
+#include "tca_band2.cuh"
 #include "tca_fused.cuh"
 
 namespace tca {
@@ -46,6 +47,18 @@ extern template tca_status launch_dispatch_fu<Params<float>>(const tca_operator 
 extern template int fu_ok_for<double>(int);
 extern template int fu_ok_for<float>(int);
 }  // namespace band
+namespace band2 {
+extern template tca_status launch_dispatch<band::Params<double>>(const tca_operator *, const band::Params<double> &,
+                                                                 cudaStream_t, const CUtensorMap *, const CUtensorMap *);
+extern template tca_status launch_dispatch<band::Params<float>>(const tca_operator *, const band::Params<float> &,
+                                                                cudaStream_t, const CUtensorMap *, const CUtensorMap *);
+extern template tca_status launch_dispatch<band::ParamsG<double>>(const tca_operator *, const band::ParamsG<double> &,
+                                                                  cudaStream_t, const CUtensorMap *, const CUtensorMap *);
+extern template tca_status launch_dispatch<band::ParamsG<float>>(const tca_operator *, const band::ParamsG<float> &,
+                                                                 cudaStream_t, const CUtensorMap *, const CUtensorMap *);
+extern template int pp_for<double>(int);
+extern template int pp_for<float>(int);
+}  // namespace band2
 
 namespace {
 
@@ -64,8 +77,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
     return fn;
 }
 
+// tile extents of the kernel the operator uses (v2: tca_band2.cuh)
+int t2_of(const tca_operator *op) { return op->band_v2 ? band2::T2 : band::T2; }
+
 int t3_of(const tca_operator *op)
 {
+    if (op->band_v2) return band2::T3;
     return op->dtype == TCA_F64 ? band::t3_for<double>((int)op->n[3]) : band::t3_for<float>((int)op->n[3]);
 }
 
@@ -92,7 +109,7 @@ TableLayout table_layout(const tca_operator *op)
 {
     TableLayout L{};
     const int t3 = t3_of(op);
-    const int extra[kD] = {0, band::T2, t3, 0};
+    const int extra[kD] = {0, t2_of(op), t3, 0};
     const int order[kD] = {3, 2, 1, 0};
     int off = 0;
     for (int i = 0; i < kD; ++i) {
@@ -126,7 +143,8 @@ void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob, in
     p->n2 = (int)op->n[1];
     p->n3 = (int)op->n[2];
     p->tiles3 = (p->n3 + t3 - 1) / t3;
-    const long long tiles2 = (p->n2 + band::T2 - 1) / band::T2;
+    const int t2 = t2_of(op);
+    const long long tiles2 = (p->n2 + t2 - 1) / t2;
     const long long total = tiles2 * p->tiles3 * p->n1;
     // persistent grid over the (tile-major, slab-minor) unit order.  A CTA's
     // cost is its units plus 6 ramp slabs per tile it touches (mode-1 halo of
@@ -135,7 +153,9 @@ void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob, in
     //          ranges cross tile boundaries) -- long mode 1 (one GPU);
     //   whole: CTA b owns tile b entirely (tiles <= G) -- short mode 1 (a
     //          mode-1 shard of 16 rows: 22 slab passes instead of up to 26).
-    const int minb = op->dtype == TCA_F64 ? band::minb_for<double>((int)op->n[3]) : band::minb_for<float>((int)op->n[3]);
+    const int minb = op->band_v2 ? 1
+                                 : op->dtype == TCA_F64 ? band::minb_for<double>((int)op->n[3])
+                                                        : band::minb_for<float>((int)op->n[3]);
     const int G = (int)std::min<long long>(std::min(op->num_sms * minb, band::MAXG), total);
     const long long tiles = tiles2 * p->tiles3;
     long long split_cost = 0;
@@ -144,7 +164,8 @@ void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob, in
         const long long segs = u1 > u0 ? (u1 - 1) / p->n1 - u0 / p->n1 + 1 : 0;
         split_cost = std::max(split_cost, (u1 - u0) + 2 * band::KH1 * segs);
     }
-    const long long whole_cost = tiles <= band::MAXG ? p->n1 + 2 * band::KH1 : (1ll << 60);
+    const long long whole_cost =
+        tiles <= std::min<long long>(band::MAXG, (long long)op->num_sms * minb) ? p->n1 + 2 * band::KH1 : (1ll << 60);
     // measurement switch: TCA_BAND_SCHED=whole|split forces a schedule
     // B1' prefers whole tile columns: all CTAs advance through mode 1 together,
     // so the halo re-reads of D and P_old hit L2 (config 3 plain apply: DRAM
@@ -231,6 +252,28 @@ tca_status make_tmap(const tca_operator *op, const void *ptr, int kind, CUtensor
         box[2] = 1;
     }
     cuuint32_t es[4] = {1, 1, 1, 1};
+    if (op->band_v2) {   // tca_band2.cuh: slab box (UNIT, PP/UNIT, PR, 1) of a 4-D view; store box (T3 n4, T2, 1)
+        const auto dt = op->dtype == TCA_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        CUresult r;
+        if (kind == 0) {
+            const cuuint64_t unit = band2::UNIT, F = (cuuint64_t)(op->n[2] * op->n[3]);
+            const int pp = op->dtype == TCA_F64 ? band2::pp_for<double>(n4) : band2::pp_for<float>(n4);
+            cuuint64_t d4[4] = {unit, F / unit, (cuuint64_t)op->n[1], (cuuint64_t)slabs};
+            cuuint64_t s4[3] = {unit * op->esize, F * op->esize, F * (cuuint64_t)op->n[1] * op->esize};
+            cuuint32_t b4[4] = {(cuuint32_t)unit, (cuuint32_t)(pp / unit), (cuuint32_t)band2::PR, 1};
+            r = encode(m, dt, 4, const_cast<void *>(ptr), d4, s4, b4, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        } else {
+            box[0] = (cuuint32_t)(band2::T3 * n4);
+            box[1] = band2::T2;
+            box[2] = 1;
+            r = encode(m, dt, 3, const_cast<void *>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        }
+        if (r != CUDA_SUCCESS)
+            return fail(TCA_ERR_CUDA, "cuTensorMapEncodeTiled (v2) failed (" + std::to_string((int)r) + ")");
+        return TCA_OK;
+    }
     const bool pitched = (op->dtype == TCA_F64 ? band::pitched_for<double>(n4) : band::pitched_for<float>(n4)) != 0;
     if (kind == 0 && (onebox_of(op) || pitched)) {   // whole staged slab (PR rows x PP elements) as one box
         // chunk: Cfg::UNIT elements, or 16 B for a pitched fp32 slab whose n3 n4 is not a multiple of UNIT
@@ -331,8 +374,14 @@ tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_
         static const char *e = getenv("TCA_BAND_DEBUG");
         p->dbg = e ? atoi(e) : 0;
     }
-    if (op->band_gt) TCA_TRY(band::launch_dispatch(op, *static_cast<band::ParamsG<T> *>(p), s, xm, ym));
-    else TCA_TRY(band::launch_dispatch(op, *static_cast<band::Params<T> *>(p), s, xm, ym));
+    if (op->band_v2) {
+        if (op->band_gt) TCA_TRY(band2::launch_dispatch(op, *static_cast<band::ParamsG<T> *>(p), s, xm, ym));
+        else TCA_TRY(band2::launch_dispatch(op, *static_cast<band::Params<T> *>(p), s, xm, ym));
+    } else if (op->band_gt) {
+        TCA_TRY(band::launch_dispatch(op, *static_cast<band::ParamsG<T> *>(p), s, xm, ym));
+    } else {
+        TCA_TRY(band::launch_dispatch(op, *static_cast<band::Params<T> *>(p), s, xm, ym));
+    }
     // the slots are in use until this launch completes; a launch captured into a
     // CUDA graph keeps using them for the graph's lifetime: pin them instead
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -360,8 +409,22 @@ bool fused_shape_supported(const tca_operator *op)
     return get_encode() != nullptr;   // (tables that do not fit the parameter block go to global memory)
 }
 
+// The warp-specialised kernel (tca_band2.cuh) takes 9 <= n4 <= 16 (instantiated:
+// 15, 16) when the slab is one TMA box of 8-element chunks.  Opt-in
+// (TCA_BAND_V2=1): measured slower than band_apply_kernel on config 3 (DESIGN.md
+// 6.1, shared-memory traffic per unknown 31 vs 24 words).
+static bool v2_eligible(const tca_operator *op)
+{
+    static const char *e = getenv("TCA_BAND_V2");
+    if (!(e && e[0] == '1')) return false;
+    const int n4 = (int)op->n[3];
+    if (n4 != 15 && n4 != 16) return false;
+    return (op->n[2] * op->n[3]) % band2::UNIT == 0;
+}
+
 tca_status fused_prepare(tca_operator *op)
 {
+    op->band_v2 = v2_eligible(op) ? 1 : 0;
     if (op->dtype == TCA_F64) build_params<double>(op, op->band_params, op->band_grid, false);
     else build_params<float>(op, op->band_params, op->band_grid, false);
     return TCA_OK;
@@ -369,6 +432,7 @@ tca_status fused_prepare(tca_operator *op)
 
 bool fused_b1_supported(const tca_operator *op)
 {
+    if (op->band_v2) return false;   // B1' is an instantiation of the first kernel
     if (op->ghost != 0 || op->band_gt || op->band_params.empty()) return false;   // one GPU, block tables
     const int n4 = (int)op->n[3];
     const bool pitched = (op->dtype == TCA_F64 ? band::pitched_for<double>(n4) : band::pitched_for<float>(n4)) != 0;

@@ -203,6 +203,7 @@ struct tca_operator {
     void *p2 = nullptr;                  // second P buffer
     int pcur = 0;                        // 0: P in p_own, 1: P in p2
     int apply_path = 0;                  // 0 = generic multi-pass, 1 = fused banded, 2 = Kronecker-sum stencil
+    int band_v2 = 0;                     // fused banded apply: 1 = warp-specialised kernel (tca_band2.cuh)
     // CUDA-graph replay of CG chunks
     // (two instances when timing: each carries its own captured event pairs, so
     // one can be harvested while the other runs)
