@@ -90,12 +90,16 @@ typedef struct {
  * optional (NULL), and must hold history_capacity >= max_iters+1 doubles. */
 typedef struct {
     int32_t iterations;   /* completed CG iterations k                       */
-    int32_t converged;    /* 1 if rho_k <= rtol^2 rho_0 or rho_k == 0         */
+    int32_t converged;    /* 1 if rho_k <= rtol^2 <b, b> or rho_k == 0        */
     int32_t status;       /* tca_status of the solve                         */
     int32_t pad;
-    double rho0;          /* <r0, r0> = <b, b>                               */
+    double rho0;          /* <r0, r0> (= <b, b> when x0 = 0)                 */
     double rho_final;     /* recursive <r_k, r_k>                            */
-    double seconds;       /* device time of the solve (CUDA events)          */
+    double relres_final;  /* true residual |b - M x_k|_2 / |b|_2 (reading Z2),
+                             from one extra apply after the solve; 0 when
+                             b = 0 and M x_k = 0                              */
+    double seconds;       /* device time of the solve (CUDA events; the
+                             relres_final apply is not included)            */
     double *rho_history;  /* rho_0 .. rho_k (optional)                       */
     int32_t history_capacity;
     int32_t pad2;
@@ -215,17 +219,27 @@ tca_status tca_rhs(const tca_operator *op, const void *ydata, void *b,
                    void *stream);
 
 /*
- * Solve M x = b by tensor CG (Fig. 2) from x0 = 0 (reading Z3).
- *   rtol > 0: stop when rho_k <= rtol^2 * rho_0 (reading Z2) or rho_k == 0,
+ * Solve M x = b by tensor CG (Fig. 2).
+ *   x0_zero != 0: start from C = 0 (reading Z3; the initial apply is skipped,
+ *             R := B); x is output only.
+ *   x0_zero == 0: x holds the start C on entry (warm start): R := B - A*C
+ *             (Fig. 2's first line) with one apply.
+ *   rtol > 0: stop when rho_k <= rtol^2 * <b, b> (reading Z2; <b, b> = rho_0
+ *             when x0 = 0, reading Z28 for a warm start) or rho_k == 0,
  *             status TCA_NOT_CONVERGED if max_iters is reached first;
  *   rtol <= 0: run exactly max_iters iterations (stopping early only if
  *             rho_k == 0, reading Z12).
- * b, x: device tensors of the local shape.  The iteration runs entirely on
- * the device (scalars in device memory, no host round trip per iteration).
- * Synchronises `stream` before filling *rep (rep may be NULL).
+ * b, x: device tensors of the local shape (not aliasing).  The iteration runs
+ * entirely on the device (scalars in device memory, no host round trip per
+ * iteration).  With rep != NULL the report's relres_final costs one more
+ * apply after the solve.  Synchronises `stream` before filling *rep.
+ * Errors: TCA_ERR_INVALID_ARG (NULL/aliasing tensors, max_iters < 0,
+ * non-finite rtol), TCA_ERR_BREAKDOWN (<p, Mp> <= 0),
+ * TCA_ERR_NONFINITE (NaN/Inf in a dot product), TCA_NOT_CONVERGED (x valid).
  */
-tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol,
-                        int32_t max_iters, tca_cg_report *rep, void *stream);
+tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, int x0_zero,
+                        double rtol, int32_t max_iters, tca_cg_report *rep,
+                        void *stream);
 
 /*
  * Preconditioned CG (reading Z22) with the
@@ -238,14 +252,16 @@ tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol,
  *   R := B, Z := P^-1 R, P := Z, rho := R+*Z; repeat Q := M P,
  *   alpha := rho / P+*Q, C += alpha P, R -= alpha Q, [stop test on R+*R exactly
  *   as tca_cg_solve's], Z := P^-1 R, rho1 := R+*Z, P := Z + (rho1/rho) P.
- * Arguments, stop rule, report and stream semantics as tca_cg_solve (the
- * report's rho values and history are R+*R).  The factors are formed on the
+ * Arguments (x0_zero included: R := B - A*C before Z := P^-1 R), stop rule,
+ * report and stream semantics as tca_cg_solve (the report's rho values and
+ * history are R+*R).  The factors are formed on the
  * first call (host fp64 Cholesky, n_d <= 256) and kept by the operator.
  * TCA_ERR_INVALID_ARG on a sharded operator (nranks > 1: the mode-1 solve
  * would cross shards); TCA_ERR_BREAKDOWN if R+*Z <= 0.
  */
-tca_status tca_pcg_solve(tca_operator *op, const void *b, void *x, double rtol,
-                         int32_t max_iters, tca_cg_report *rep, void *stream);
+tca_status tca_pcg_solve(tca_operator *op, const void *b, void *x, int x0_zero,
+                         double rtol, int32_t max_iters, tca_cg_report *rep,
+                         void *stream);
 
 /*
  * Tensor Jacobi (Fig. 1a/1b), the paper's stationary solver:
@@ -270,11 +286,13 @@ tca_status tca_jacobi_solve(tca_operator *op, const void *b, void *x, double thr
  *   alpha := gamma1 / (delta - beta gamma1 / alpha).
  * Both inner products of an iteration are reduced together after the apply:
  * one reduction point per iteration (one all-reduce of two fp64 values on a
- * sharded operator) instead of two.  Arguments, stop rule, report (rho =
- * R+*R) and stream semantics as tca_cg_solve; works on sharded operators.
+ * sharded operator) instead of two.  Arguments (x0_zero: R := B - A*C),
+ * stop rule, report (rho = R+*R) and stream semantics as tca_cg_solve; works
+ * on sharded operators.
  */
-tca_status tca_cgsr_solve(tca_operator *op, const void *b, void *x, double rtol,
-                          int32_t max_iters, tca_cg_report *rep, void *stream);
+tca_status tca_cgsr_solve(tca_operator *op, const void *b, void *x, int x0_zero,
+                          double rtol, int32_t max_iters, tca_cg_report *rep,
+                          void *stream);
 
 /* z = P^-1 r with the PCG preconditioner above (device tensors of the local
  * shape, z may equal r).  Stream-ordered. */

@@ -77,6 +77,11 @@ def lib():
                                   ctypes.c_double, _dp, _dp, ctypes.c_double, ctypes.c_int, _dp,
                                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
             L.orc_pcg.restype = ctypes.c_int
+            for nm in ("orc_cg_x0", "orc_pcg_x0", "orc_cgsr_x0"):
+                getattr(L, nm).argtypes = [ctypes.c_int, _i64p, ctypes.POINTER(_dp), ctypes.POINTER(_dp),
+                                           ctypes.c_double, _dp, _dp, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                           _dp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+                getattr(L, nm).restype = ctypes.c_int
             L.orc_cgsr.argtypes = L.orc_cg.argtypes
             L.orc_cgsr.restype = ctypes.c_int
             L.orc_jacobi.argtypes = L.orc_cg.argtypes
@@ -207,28 +212,25 @@ class Operator:
         ia, ip = _i64(idx)
         return lib().orc_rhs_point(self.D, self._np, self._mp, self._A, _p(ydata), ip)
 
-    def cg(self, b, rtol: float, max_iters: int):
-        """Fig. 2 CG from x0 = 0.  Returns (x, iters, status, rho_history)."""
+    def _krylov(self, fn, b, rtol, max_iters, x0):
         b = _f64(b).reshape(self.n)
-        x = np.empty(self.n)
+        x = np.zeros(self.n) if x0 is None else _f64(x0).reshape(self.n).copy()
         hist = np.zeros(max_iters + 1)
         it = ctypes.c_int(0)
         rf = ctypes.c_double(0.0)
-        st = lib().orc_cg(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(x),
-                          float(rtol), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
+        st = fn(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(x), 1 if x0 is None else 0,
+                float(rtol), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
         return x, it.value, st, hist[: it.value + 1]
 
-    def cgsr(self, b, rtol: float, max_iters: int):
-        """Single-reduction (Chronopoulos-Gear) CG from x0 = 0 (reading Z24).
+    def cg(self, b, rtol: float, max_iters: int, x0=None):
+        """Fig. 2 CG from x0 = 0, or from x0 (R := B - A*C; stop reference <b, b>,
+        reading Z28).  Returns (x, iters, status, rho_history)."""
+        return self._krylov(lib().orc_cg_x0, b, rtol, max_iters, x0)
+
+    def cgsr(self, b, rtol: float, max_iters: int, x0=None):
+        """Single-reduction (Chronopoulos-Gear) CG from x0 = 0 or x0 (reading Z24).
         Returns (x, iters, status, rr_history)."""
-        b = _f64(b).reshape(self.n)
-        x = np.empty(self.n)
-        hist = np.zeros(max_iters + 1)
-        it = ctypes.c_int(0)
-        rf = ctypes.c_double(0.0)
-        st = lib().orc_cgsr(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(x),
-                            float(rtol), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
-        return x, it.value, st, hist[: it.value + 1]
+        return self._krylov(lib().orc_cgsr_x0, b, rtol, max_iters, x0)
 
     def jacobi(self, b, threshold: float, max_iters: int):
         """Tensor Jacobi (Fig. 1) from U = 0, stopping when R+*R <= threshold.
@@ -262,16 +264,9 @@ class Operator:
         lib().orc_precond_apply(self.D, self._np, _ptr_array(C), _p(r), _p(z))
         return z
 
-    def pcg(self, b, rtol: float, max_iters: int):
-        """Preconditioned CG from x0 = 0.  Returns (x, iters, status, rr_history)."""
-        b = _f64(b).reshape(self.n)
-        x = np.empty(self.n)
-        hist = np.zeros(max_iters + 1)
-        it = ctypes.c_int(0)
-        rf = ctypes.c_double(0.0)
-        st = lib().orc_pcg(self.D, self._np, self._G, self._R, self.lam, _p(b), _p(x),
-                           float(rtol), int(max_iters), _p(hist), ctypes.byref(it), ctypes.byref(rf))
-        return x, it.value, st, hist[: it.value + 1]
+    def pcg(self, b, rtol: float, max_iters: int, x0=None):
+        """Preconditioned CG from x0 = 0 or x0.  Returns (x, iters, status, rr_history)."""
+        return self._krylov(lib().orc_pcg_x0, b, rtol, max_iters, x0)
 
 
 def cholesky(F) -> np.ndarray:

@@ -306,7 +306,8 @@ double orc_dot(int64_t N, const double *a, const double *b)
 
 /*
  * Tensor CG, Fig. 2, step by step:
- *   R := B - A*C  (C = 0, Z3: R = B);  P := R;  rho := R+*R
+ *   R := B - A*C  (x0_zero: C = 0, Z3: R = B; else C is the caller's x);
+ *   P := R;  rho := R+*R
  *   REPEAT  Q := A*(P*D)              (D: frame relabel only, Z4)
  *           alpha := rho / (P+*Q)
  *           C := C + alpha*P*D
@@ -314,25 +315,32 @@ double orc_dot(int64_t N, const double *a, const double *b)
  *           rho1 := R+*R
  *           [stop test, Z1/Z2/Z12/Z20]
  *           P := R + (rho1/rho)*P;  rho := rho1
- * Stop: rho1 == 0, or rtol > 0 and rho1 <= rtol^2 * rho0, or k+1 == max_iters.
+ * Stop: rho1 == 0, or rtol > 0 and rho1 <= rtol^2 * <b, b> (= rho0 when C = 0;
+ * reading Z28), or k+1 == max_iters.
  * hist (optional, >= max_iters+1 entries) receives rho_0 .. rho_k.
  * Returns the status; *iters = completed iterations.
  */
-int orc_cg(int D, const int64_t *n, const double *const *G,
-           const double *const *R, double lam, const double *b, double *x,
-           double rtol, int max_iters, double *hist, int *iters,
-           double *rho_final)
+int orc_cg_x0(int D, const int64_t *n, const double *const *G,
+              const double *const *R, double lam, const double *b, double *x,
+              int x0_zero, double rtol, int max_iters, double *hist, int *iters,
+              double *rho_final)
 {
     int64_t N = prod(n, D);
     double *r = (double *)malloc(sizeof(double) * N);
     double *p = (double *)malloc(sizeof(double) * N);
     double *q = (double *)malloc(sizeof(double) * N);
     int status = ORC_OK;
-    memcpy(r, b, sizeof(double) * N);           /* R := B - A*0 */
-    memset(x, 0, sizeof(double) * N);           /* C := 0 */
+    if (x0_zero) {
+        memcpy(r, b, sizeof(double) * N);       /* R := B - A*0 */
+        memset(x, 0, sizeof(double) * N);       /* C := 0 */
+    } else {                                    /* warm start: x holds C */
+        orc_apply(D, n, G, R, lam, x, q);
+        for (int64_t i = 0; i < N; i++) r[i] = b[i] - q[i];   /* R := B - A*C */
+    }
     memcpy(p, r, sizeof(double) * N);           /* P := R */
     double rho = orc_dot(N, r, r);              /* rho := R+*R */
-    double rho0 = rho;
+    /* stop reference (Z2, Z28): <b, b>, which is rho_0 when C = 0 */
+    double rho0 = x0_zero ? rho : orc_dot(N, b, b);
     if (hist) hist[0] = rho;
     *iters = 0;
     if (!isfinite(rho)) {
@@ -367,6 +375,15 @@ int orc_cg(int D, const int64_t *n, const double *const *G,
     free(p);
     free(q);
     return status;
+}
+
+/* Fig. 2 from C = 0 (reading Z3). */
+int orc_cg(int D, const int64_t *n, const double *const *G,
+           const double *const *R, double lam, const double *b, double *x,
+           double rtol, int max_iters, double *hist, int *iters,
+           double *rho_final)
+{
+    return orc_cg_x0(D, n, G, R, lam, b, x, 1, rtol, max_iters, hist, iters, rho_final);
 }
 
 /* ------------------------------------------------------------------------
@@ -466,7 +483,8 @@ void orc_precond_apply(int D, const int64_t *n, const double *const *C, const do
 
 /*
  * Preconditioned CG (the textbook preconditioned form of Fig. 2's iteration):
- *   C := 0;  R := B;  Z := P^-1 R;  P := Z;  rho := R+*Z;  rr0 := R+*R
+ *   C := 0 (or the caller's x);  R := B - A*C;  Z := P^-1 R;  P := Z;
+ *   rho := R+*Z;  stop reference <b, b>
  *   REPEAT  Q := A*P;  alpha := rho / (P+*Q)
  *           C := C + alpha*P;  R := R - alpha*Q;  rr := R+*R
  *           [stop test on rr exactly as orc_cg's on rho1 (Z1/Z2/Z12/Z20)]
@@ -474,9 +492,9 @@ void orc_precond_apply(int D, const int64_t *n, const double *const *C, const do
  *           P := Z + (rho1/rho)*P;  rho := rho1
  * hist receives rr_0 .. rr_k; *rr_final the last rr.
  */
-int orc_pcg(int D, const int64_t *n, const double *const *G,
-            const double *const *R, double lam, const double *b, double *x,
-            double rtol, int max_iters, double *hist, int *iters, double *rr_final)
+int orc_pcg_x0(int D, const int64_t *n, const double *const *G,
+               const double *const *R, double lam, const double *b, double *x,
+               int x0_zero, double rtol, int max_iters, double *hist, int *iters, double *rr_final)
 {
     int64_t N = prod(n, D);
     double *Fs[8] = {0}, *Cs[8] = {0}, eps[8];
@@ -491,9 +509,14 @@ int orc_pcg(int D, const int64_t *n, const double *const *G,
     double *z = (double *)malloc(sizeof(double) * N);
     double *p = (double *)malloc(sizeof(double) * N);
     double *q = (double *)malloc(sizeof(double) * N);
-    memset(x, 0, sizeof(double) * N);
-    memcpy(r, b, sizeof(double) * N);
-    double rr = orc_dot(N, r, r), rr0 = rr;
+    if (x0_zero) {
+        memset(x, 0, sizeof(double) * N);
+        memcpy(r, b, sizeof(double) * N);
+    } else {   /* warm start: R := B - A*C */
+        orc_apply(D, n, G, R, lam, x, q);
+        for (int64_t i = 0; i < N; i++) r[i] = b[i] - q[i];
+    }
+    double rr = orc_dot(N, r, r), rr0 = x0_zero ? rr : orc_dot(N, b, b);
     if (hist) hist[0] = rr;
     *iters = 0;
     if (bad) {
@@ -543,12 +566,19 @@ int orc_pcg(int D, const int64_t *n, const double *const *G,
     return status;
 }
 
+int orc_pcg(int D, const int64_t *n, const double *const *G,
+            const double *const *R, double lam, const double *b, double *x,
+            double rtol, int max_iters, double *hist, int *iters, double *rr_final)
+{
+    return orc_pcg_x0(D, n, G, R, lam, b, x, 1, rtol, max_iters, hist, iters, rr_final);
+}
+
 /* ------------------------------------------------------------------------
  * Single-reduction CG (Chronopoulos & Gear's rearrangement of Fig. 2's CG;
  * SURVEY.md 8(f)2, reading Z24).  Same Krylov iterates as Fig. 2 in
  * exact arithmetic; the two inner products of an iteration are taken together
  * after the one apply, so a distributed solve needs one reduction per step:
- *   C := 0;  R := B;  W := A*R;  gamma := R+*R;  delta := R+*W
+ *   C := 0 (or the caller's x);  R := B - A*C;  W := A*R;  gamma := R+*R;  delta := R+*W
  *   alpha := gamma / delta;  beta := 0;  P := 0;  S := 0
  *   REPEAT  P := R + beta*P;  S := W + beta*S        (S = A*P)
  *           C := C + alpha*P;  R := R - alpha*S
@@ -558,9 +588,9 @@ int orc_pcg(int D, const int64_t *n, const double *const *G,
  *           gamma := gamma1
  * (alpha's denominator <= 0 or non-finite: breakdown).  hist: gamma_0..gamma_k.
  * ---------------------------------------------------------------------- */
-int orc_cgsr(int D, const int64_t *n, const double *const *G,
-             const double *const *R, double lam, const double *b, double *x,
-             double rtol, int max_iters, double *hist, int *iters, double *rr_final)
+int orc_cgsr_x0(int D, const int64_t *n, const double *const *G,
+                const double *const *R, double lam, const double *b, double *x,
+                int x0_zero, double rtol, int max_iters, double *hist, int *iters, double *rr_final)
 {
     int64_t N = prod(n, D);
     double *r = (double *)malloc(sizeof(double) * N);
@@ -568,9 +598,14 @@ int orc_cgsr(int D, const int64_t *n, const double *const *G,
     double *p = (double *)calloc(N, sizeof(double));
     double *s = (double *)calloc(N, sizeof(double));
     int status = ORC_OK;
-    memset(x, 0, sizeof(double) * N);
-    memcpy(r, b, sizeof(double) * N);
-    double gamma = orc_dot(N, r, r), gamma0 = gamma;
+    if (x0_zero) {
+        memset(x, 0, sizeof(double) * N);
+        memcpy(r, b, sizeof(double) * N);
+    } else {   /* warm start: R := B - A*C */
+        orc_apply(D, n, G, R, lam, x, w);
+        for (int64_t i = 0; i < N; i++) r[i] = b[i] - w[i];
+    }
+    double gamma = orc_dot(N, r, r), gamma0 = x0_zero ? gamma : orc_dot(N, b, b);
     if (hist) hist[0] = gamma;
     *iters = 0;
     if (!isfinite(gamma)) {
@@ -613,6 +648,13 @@ int orc_cgsr(int D, const int64_t *n, const double *const *G,
     free(p);
     free(s);
     return status;
+}
+
+int orc_cgsr(int D, const int64_t *n, const double *const *G,
+             const double *const *R, double lam, const double *b, double *x,
+             double rtol, int max_iters, double *hist, int *iters, double *rr_final)
+{
+    return orc_cgsr_x0(D, n, G, R, lam, b, x, 1, rtol, max_iters, hist, iters, rr_final);
 }
 
 /* ------------------------------------------------------------------------

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -144,6 +145,22 @@ static bool cholesky_ok(const std::vector<double> &G, int64_t n)
         }
     }
     return true;
+}
+
+static std::mutex g_attr_mu;
+static std::map<std::pair<const void *, int>, size_t> g_attr_set;
+
+tca_status set_max_dynamic_smem(const void *func, size_t bytes)
+{
+    int dev = 0;
+    TCA_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    size_t &cur = g_attr_set[{func, dev}];
+    if (bytes > cur) {
+        TCA_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        cur = bytes;
+    }
+    return TCA_OK;
 }
 
 template <typename T>
@@ -440,6 +457,27 @@ static tca_status timed_apply(tca_operator *op, const void *x, void *y, const in
     return timed_call(op, s, [&] { return apply_dispatch(op, x, y, done, s, pq_part); });
 }
 
+// y = M x for a caller tensor x of the local shape: a sharded operator first
+// copies x into its ghosted buffer and exchanges the halo (tca_apply's path)
+static tca_status apply_any(tca_operator *o, const void *x, void *y, cudaStream_t s, bool timed)
+{
+    if (o->transport) {
+        const size_t sb = (size_t)o->slab * o->esize;
+        const size_t xb = (size_t)(o->nloc1 + 2 * o->ghost) * sb;
+        if (!o->x_ext) {
+            TCA_CUDA_TRY(cudaMallocAsync(&o->x_ext, xb, s));
+            TCA_CUDA_TRY(cudaMemsetAsync(o->x_ext, 0, xb, s));
+            o->device_bytes += xb;
+        }
+        TCA_CUDA_TRY(cudaMemcpyAsync((char *)o->x_ext + (size_t)o->ghost * sb, x, (size_t)o->nloc1 * sb,
+                                     cudaMemcpyDeviceToDevice, s));
+        TCA_TRY(o->transport->halo(1, (char *)o->x_ext, sb, o->nloc1, s));
+        x = o->x_ext;
+    }
+    if (timed) return timed_apply(o, x, y, nullptr, s);
+    return apply_dispatch(o, x, y, nullptr, s);
+}
+
 static tca_status harvest_pairs(tca_operator *op, const cudaEvent_t *ev, size_t n)
 {
     for (size_t i = 0; i + 1 < n; i += 2) {
@@ -619,6 +657,10 @@ static void destroy_graphs(tca_operator *op)
         op->gev[g].clear();
     }
     op->gx = nullptr;
+    // the captured launches were the only users of pinned tensor-map slots
+    // (launches after the caller's stream joined the graph stream are ordered
+    // after any replay, so the slots may be recycled again)
+    op->tmap_pinned = 0;
 }
 
 template <typename T>
@@ -727,8 +769,9 @@ static tca_status jacobi_prepare(tca_operator *op, cudaStream_t s)
 
 template <typename T>
 static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t max_iters,
-                       tca_cg_report *rep, cudaStream_t s, int pcg = 0)
+                       tca_cg_report *rep, cudaStream_t s, int pcg = 0, int x0_zero = 1)
 {
+    double *part_bb = op->part + 2 * kRedBlocks;   // <b, b> partials (warm start, report)
     CgScalars h{};
     h.rtol2 = rtol > 0.0 ? rtol * rtol : 0.0;
     h.max_iters = max_iters;
@@ -764,16 +807,27 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
         TCA_TRY(timed_apply(op, x, (T *)op->q, nullptr, s));
         launch_jacobi_resid<T>((T *)op->r, (const T *)op->q, b, op->N, op->part, nullptr, s);
         launch_jacobi_finalize(0, op->part, kRedBlocks, op->sc, op->hist, s);
-    } else if (pcg == 2) {   // single-reduction CG: R := B (ghosted), C := 0, P := 0, S := 0, W := A*R
+    } else if (pcg == 2) {   // single-reduction CG: R := B - A*C (ghosted), P := 0, S := 0, W := A*R
         if (!op->sr_s) TCA_CUDA_TRY(cudaMallocAsync(&op->sr_s, (size_t)op->N * op->esize, s));
-        launch_cg_init<T>(b, x, (T *)op->p_own, (T *)op->r, op->N, op->part, s);   // gamma0 partials
+        if (x0_zero) {
+            launch_cg_init<T>(b, x, (T *)op->p_own, (T *)op->r, op->N, op->part, s);   // gamma0 partials
+        } else {   // warm start (Fig. 2's R := B - A*C)
+            TCA_TRY(apply_any(op, x, op->q, s, false));
+            launch_resid2<T>(b, (const T *)op->q, (T *)op->p_own, nullptr, op->N, op->part, part_bb, s);
+        }
         TCA_CUDA_TRY(cudaMemsetAsync(op->r, 0, (size_t)op->N * op->esize, s));
         TCA_CUDA_TRY(cudaMemsetAsync(op->sr_s, 0, (size_t)op->N * op->esize, s));
         TCA_TRY(halo_p(op, s));
         TCA_TRY(cgsr_apply_reduce<T>(op, 7, s));
-    } else {
+        if (!x0_zero) TCA_TRY(cg_reduce(op, 8, part_bb, kRedBlocks, s));           // stop reference <b, b>
+    } else if (x0_zero) {
         launch_cg_init<T>(b, x, (T *)op->r, (T *)op->p_own, op->N, op->part, s);   // C := 0, R := B, P := R
         TCA_TRY(cg_reduce(op, 0, op->part, kRedBlocks, s));                       // rho0 := R+*R
+    } else {   // warm start: R := B - A*C, P := R (Fig. 2; reading Z28)
+        TCA_TRY(apply_any(op, x, op->q, s, false));
+        launch_resid2<T>(b, (const T *)op->q, (T *)op->r, (T *)op->p_own, op->N, op->part, part_bb, s);
+        TCA_TRY(cg_reduce(op, 0, op->part, kRedBlocks, s));                       // rho0 := R+*R
+        TCA_TRY(cg_reduce(op, 8, part_bb, kRedBlocks, s));                        // stop reference <b, b>
     }
     if (pcg == 1) {   // Z := P^-1 R, P := Z, rho := R+*Z
         T *z = (T *)op->z;
@@ -808,6 +862,13 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     op->b1 = b1_saved;
     TCA_CUDA_TRY(cudaGetLastError());
     TCA_CUDA_TRY(cudaEventRecord(op->ev1, s));
+    if (rep) {   // true residual |b - M x_k| / |b| (reading Z2): one more apply, after the timed solve
+        TCA_TRY(apply_any(op, x, op->q, s, false));
+        launch_resid2<T>(b, (const T *)op->q, nullptr, nullptr, op->N, op->part, part_bb, s);
+        launch_cg_finalize(8, op->part, kRedBlocks, op->sc, nullptr, s, 1);
+        launch_cg_finalize(9, part_bb, kRedBlocks, op->sc, nullptr, s, 1);
+        if (op->transport) TCA_TRY(op->transport->allreduce(&op->sc->red[8], 2, s));
+    }
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
     TCA_CUDA_TRY(cudaStreamSynchronize(s));
     if (op->timing) TCA_TRY(harvest_timing(op));
@@ -820,6 +881,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
         rep->status = r.status;
         rep->rho0 = r.rho0;
         rep->rho_final = r.rr;
+        rep->relres_final = r.red[9] > 0.0 ? sqrt(r.red[8] / r.red[9]) : (r.red[8] > 0.0 ? INFINITY : 0.0);
         rep->seconds = ms * 1e-3;
         if (rep->rho_history && rep->history_capacity > 0) {
             const int cnt = std::min(rep->history_capacity, r.iters + 1);
@@ -884,7 +946,7 @@ void tca_operator_destroy(tca_operator *op)
                       op->jac_e, op->sc_t, op->sc_perm, op->sc_tstart, op->sc_coef};   // stream-ordered pool
     for (void *b : pooled)
         if (b) cudaFreeAsync(b, 0);
-    dev_put(op->part, sizeof(double) * kRedBlocks * 2);
+    dev_put(op->part, sizeof(double) * kRedBlocks * 3);
     dev_put(op->sc, sizeof(CgScalars));
     dev_put(op->hist, sizeof(double) * op->hist_cap);
     dev_put(op->tmap_dev, sizeof(TmapSlot::map) * kTmapSlots);
@@ -1117,7 +1179,13 @@ static tca_status create_impl(tca_operator **out, int order, const int64_t *n, c
                     "dist: sharded operators need the fused banded path (all modes banded, supported n4, "
                     "n3*n4*esize a multiple of 16 B)");
     }
-    if (op->apply_path == 1) fused_prepare(op);
+    if (op->apply_path == 1) {
+        const tca_status fs = fused_prepare(op);
+        if (fs != TCA_OK) {
+            tca_operator_destroy(op);
+            return fs;
+        }
+    }
     if (sharded) op->transport = make_transport(dist);
 
     const size_t vb = (size_t)op->N * op->esize;
@@ -1131,7 +1199,7 @@ static tca_status create_impl(tca_operator **out, int order, const int64_t *n, c
     if (e == cudaSuccess) e = cudaMemsetAsync(op->p, 0, pb, s);   // ghosts beyond the domain stay 0
     if (e == cudaSuccess) op->p_own = (char *)op->p + (size_t)op->ghost * op->slab * op->esize;
     if (e == cudaSuccess) e = cudaMallocAsync(&op->q, vb, s);
-    if (e == cudaSuccess) e = dev_get((void **)&op->part, sizeof(double) * kRedBlocks * 2);
+    if (e == cudaSuccess) e = dev_get((void **)&op->part, sizeof(double) * kRedBlocks * 3);
     if (e == cudaSuccess) e = dev_get((void **)&op->sc, sizeof(CgScalars));
     if (e == cudaSuccess) {
         op->sc_host = (CgScalars *)pinned_get(sizeof(CgScalars));
@@ -1263,21 +1331,7 @@ tca_status tca_apply(const tca_operator *op, const void *x, void *y, void *strea
     if (x == y) return fail(TCA_ERR_INVALID_ARG, "x and y must not alias");
     cudaStream_t s = (cudaStream_t)stream;
     tca_operator *o = const_cast<tca_operator *>(op);
-    if (o->transport) {   // sharded: ghosted copy of x, halo exchange, then the apply
-        const size_t sb = (size_t)o->slab * o->esize;
-        const size_t xb = (size_t)(o->nloc1 + 2 * o->ghost) * sb;
-        if (!o->x_ext) {
-            TCA_CUDA_TRY(cudaMallocAsync(&o->x_ext, xb, s));
-            TCA_CUDA_TRY(cudaMemsetAsync(o->x_ext, 0, xb, s));
-            o->device_bytes += xb;
-        }
-        TCA_CUDA_TRY(cudaMemcpyAsync((char *)o->x_ext + (size_t)o->ghost * sb, x, (size_t)o->nloc1 * sb,
-                                     cudaMemcpyDeviceToDevice, s));
-        TCA_TRY(o->transport->halo(1, (char *)o->x_ext, sb, o->nloc1, s));
-        TCA_TRY(timed_apply(o, o->x_ext, y, nullptr, s));
-    } else {
-        TCA_TRY(timed_apply(o, x, y, nullptr, s));
-    }
+    TCA_TRY(apply_any(o, x, y, s, true));   // sharded: ghosted copy of x, halo exchange, then the apply
     TCA_CUDA_TRY(cudaGetLastError());
     return TCA_OK;
 }
@@ -1322,7 +1376,7 @@ tca_status tca_rhs(const tca_operator *op, const void *ydata, void *b, void *str
 }
 
 static tca_status solve_common(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
-                               tca_cg_report *rep, void *stream, int pcg)
+                               tca_cg_report *rep, void *stream, int pcg, int x0_zero = 1)
 {
     TCA_TRY(check_op(op));
     if (!b || !x) return fail(TCA_ERR_INVALID_ARG, "b and x must be non-NULL device pointers");
@@ -1353,20 +1407,20 @@ static tca_status solve_common(tca_operator *op, const void *b, void *x, double 
         TCA_TRY(precond_prepare(op, s));
     }
     if (op->dtype == TCA_F64)
-        return cg_t<double>(op, (const double *)b, (double *)x, rtol, max_iters, rep, s, pcg);
-    return cg_t<float>(op, (const float *)b, (float *)x, rtol, max_iters, rep, s, pcg);
+        return cg_t<double>(op, (const double *)b, (double *)x, rtol, max_iters, rep, s, pcg, x0_zero);
+    return cg_t<float>(op, (const float *)b, (float *)x, rtol, max_iters, rep, s, pcg, x0_zero);
 }
 
-tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
-                        tca_cg_report *rep, void *stream)
+tca_status tca_cg_solve(tca_operator *op, const void *b, void *x, int x0_zero, double rtol,
+                        int32_t max_iters, tca_cg_report *rep, void *stream)
 {
-    return solve_common(op, b, x, rtol, max_iters, rep, stream, 0);
+    return solve_common(op, b, x, rtol, max_iters, rep, stream, 0, x0_zero);
 }
 
-tca_status tca_pcg_solve(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
-                         tca_cg_report *rep, void *stream)
+tca_status tca_pcg_solve(tca_operator *op, const void *b, void *x, int x0_zero, double rtol,
+                        int32_t max_iters, tca_cg_report *rep, void *stream)
 {
-    return solve_common(op, b, x, rtol, max_iters, rep, stream, 1);
+    return solve_common(op, b, x, rtol, max_iters, rep, stream, 1, x0_zero);
 }
 
 tca_status tca_jacobi_solve(tca_operator *op, const void *b, void *x, double threshold, int32_t max_iters,
@@ -1375,10 +1429,10 @@ tca_status tca_jacobi_solve(tca_operator *op, const void *b, void *x, double thr
     return solve_common(op, b, x, threshold, max_iters, rep, stream, 3);
 }
 
-tca_status tca_cgsr_solve(tca_operator *op, const void *b, void *x, double rtol, int32_t max_iters,
-                          tca_cg_report *rep, void *stream)
+tca_status tca_cgsr_solve(tca_operator *op, const void *b, void *x, int x0_zero, double rtol,
+                        int32_t max_iters, tca_cg_report *rep, void *stream)
 {
-    return solve_common(op, b, x, rtol, max_iters, rep, stream, 2);
+    return solve_common(op, b, x, rtol, max_iters, rep, stream, 2, x0_zero);
 }
 
 tca_status tca_precond_apply(tca_operator *op, const void *r, void *z, void *stream)
@@ -1420,7 +1474,7 @@ tca_status tca_solve_host(tca_operator *op, const void *ydata_host, void *x_host
     TCA_CUDA_TRY(cudaMemcpyAsync(yd, ydata_host, yb, cudaMemcpyHostToDevice, s));
     tca_status st = tca_rhs(op, yd, bd, stream);
     if (st == TCA_OK || st == TCA_NOT_CONVERGED) {
-        st = tca_cg_solve(op, bd, xd, rtol, max_iters, rep, stream);
+        st = tca_cg_solve(op, bd, xd, 1, rtol, max_iters, rep, stream);
         cudaMemcpyAsync(x_host, xd, vb, cudaMemcpyDeviceToHost, s);
     }
     cudaFreeAsync(yd, s);
@@ -1448,7 +1502,10 @@ tca_status tca_solve_host_batch(tca_operator *op, int count, const void *const *
     cudaStream_t cs = nullptr;
     void *yd[2] = {nullptr, nullptr}, *xs[2] = {nullptr, nullptr}, *bd = nullptr, *xd = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_rhs[2] = {}, ev_x[2] = {}, ev_d2h[2] = {};
+    // st: the first error (CUDA or a solver error); a non-converged item only sets
+    // any_nc, so later items still run and every x_host[i] is written
     tca_status st = TCA_OK;
+    bool any_nc = false;
     auto cu = [&](cudaError_t e, const char *what) {
         if (e != cudaSuccess && st == TCA_OK) st = cuda_fail(e, what);
         return st == TCA_OK;
@@ -1477,9 +1534,9 @@ tca_status tca_solve_host_batch(tca_operator *op, int count, const void *const *
         tca_status r = tca_rhs(op, yd[k], bd, stream);
         if (r != TCA_OK) { st = r; break; }
         if (!(ok = cu(cudaEventRecord(ev_rhs[k], s), "event"))) break;
-        r = tca_cg_solve(op, bd, xd, rtol, max_iters, reps ? &reps[i] : nullptr, stream);
-        if (r != TCA_OK && r != TCA_NOT_CONVERGED) { st = r; break; }
-        if (r == TCA_NOT_CONVERGED && st == TCA_OK) st = r;
+        r = tca_cg_solve(op, bd, xd, 1, rtol, max_iters, reps ? &reps[i] : nullptr, stream);
+        if (r == TCA_NOT_CONVERGED) any_nc = true;
+        else if (r != TCA_OK) { st = r; break; }
         // x -> staging k (free once item i-2's D2H is done), D2H on the copy stream
         if (!(ok = cu(cudaStreamWaitEvent(s, ev_d2h[k], 0), "wait") &&
                    cu(cudaMemcpyAsync(xs[k], xd, vb, cudaMemcpyDeviceToDevice, s), "x staging copy") &&
@@ -1490,7 +1547,7 @@ tca_status tca_solve_host_batch(tca_operator *op, int count, const void *const *
     }
     if (cs) {
         cudaError_t e = cudaStreamSynchronize(cs);
-        if (e != cudaSuccess && (st == TCA_OK || st == TCA_NOT_CONVERGED)) st = cuda_fail(e, "copy stream");
+        if (e != cudaSuccess && st == TCA_OK) st = cuda_fail(e, "copy stream");
         cudaEventRecord(ev_h2d[0], cs);
         cudaStreamWaitEvent(s, ev_h2d[0], 0);
     }
@@ -1501,11 +1558,12 @@ tca_status tca_solve_host_batch(tca_operator *op, int count, const void *const *
     if (bd) cudaFreeAsync(bd, s);
     if (xd) cudaFreeAsync(xd, s);
     cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess && (st == TCA_OK || st == TCA_NOT_CONVERGED)) st = cuda_fail(e, "stream");
+    if (e != cudaSuccess && st == TCA_OK) st = cuda_fail(e, "stream");
     for (int k = 0; k < 2; ++k)
         for (cudaEvent_t ev : {ev_h2d[k], ev_rhs[k], ev_x[k], ev_d2h[k]})
             if (ev) cudaEventDestroy(ev);
     if (cs) cudaStreamDestroy(cs);
+    if (st == TCA_OK && any_nc) return TCA_NOT_CONVERGED;
     return st;
 }
 

@@ -128,11 +128,11 @@ bool tables_fit(const tca_operator *op);
 // the parameter block (Params, when they fit in TAP_BYTES) or in a device
 // buffer (ParamsG, n_d ~ 256: config 4).
 template <typename T>
-void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob, int &grid, bool fu)
+tca_status build_params(const tca_operator *op_c, std::vector<unsigned char> &blob, int &grid, bool fu)
 {
     tca_operator *op = const_cast<tca_operator *>(op_c);
     const bool in_block = tables_fit(op);
-    if (fu && !in_block) return;   // B1' takes parameter-block tables only
+    if (fu && !in_block) return TCA_OK;   // B1' takes parameter-block tables only (caller checks the blob)
     if (!fu) op->band_gt = !in_block;
     blob.assign(in_block ? sizeof(band::Params<T>) : sizeof(band::ParamsG<T>), 0);
     auto *p = reinterpret_cast<band::ParamsBase<T> *>(blob.data());
@@ -215,12 +215,12 @@ void build_params(const tca_operator *op_c, std::vector<unsigned char> &blob, in
         std::memcpy(reinterpret_cast<band::Params<T> *>(blob.data())->taps, taps.data(), taps.size() * sizeof(T));
     } else if (!fu) {   // global tables (uploaded once; freed with the operator)
         const size_t nb = taps.size() * sizeof(T);
-        if (dev_get(&op->band_gtaps, nb) == cudaSuccess) {
-            op->band_gtaps_bytes = nb;
-            cudaMemcpy(op->band_gtaps, taps.data(), nb, cudaMemcpyHostToDevice);
-        }
+        TCA_CUDA_TRY(dev_get(&op->band_gtaps, nb));
+        op->band_gtaps_bytes = nb;
+        TCA_CUDA_TRY(cudaMemcpy(op->band_gtaps, taps.data(), nb, cudaMemcpyHostToDevice));
         reinterpret_cast<band::ParamsG<T> *>(blob.data())->gtaps = (const T *)op->band_gtaps;
     }
+    return TCA_OK;
 }
 
 bool tables_fit(const tca_operator *op)
@@ -425,9 +425,8 @@ static bool v2_eligible(const tca_operator *op)
 tca_status fused_prepare(tca_operator *op)
 {
     op->band_v2 = v2_eligible(op) ? 1 : 0;
-    if (op->dtype == TCA_F64) build_params<double>(op, op->band_params, op->band_grid, false);
-    else build_params<float>(op, op->band_params, op->band_grid, false);
-    return TCA_OK;
+    if (op->dtype == TCA_F64) return build_params<double>(op, op->band_params, op->band_grid, false);
+    return build_params<float>(op, op->band_params, op->band_grid, false);
 }
 
 bool fused_b1_supported(const tca_operator *op)
@@ -488,8 +487,8 @@ tca_status fused_b1_prepare(const tca_operator *op_c, const void *const *ptrs, c
 {
     tca_operator *op = const_cast<tca_operator *>(op_c);
     if (op->band_params_fu.empty()) {
-        if (op->dtype == TCA_F64) build_params<double>(op, op->band_params_fu, op->band_grid_fu, true);
-        else build_params<float>(op, op->band_params_fu, op->band_grid_fu, true);
+        if (op->dtype == TCA_F64) TCA_TRY(build_params<double>(op, op->band_params_fu, op->band_grid_fu, true));
+        else TCA_TRY(build_params<float>(op, op->band_params_fu, op->band_grid_fu, true));
         if (op->band_params_fu.empty()) return fail(TCA_ERR_INVALID_ARG, "fused CG step: tables not in block");
     }
     for (int i = 0; i < n; ++i) {

@@ -545,14 +545,7 @@ tca_status launch_n4(const tca_operator *op, const PA &prm, cudaStream_t s, cons
                      const CUtensorMap *ym)
 {
     using C = Cfg<T, N4>;
-    static bool attr_set[64] = {};
-    int dev = 0;
-    TCA_CUDA_TRY(cudaGetDevice(&dev));
-    if (dev < 64 && !attr_set[dev]) {
-        TCA_CUDA_TRY(cudaFuncSetAttribute(band2_kernel<T, N4, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)C::smem_bytes));
-        attr_set[dev] = true;
-    }
+    TCA_TRY(set_max_dynamic_smem((const void *)band2_kernel<T, N4, PA>, C::smem_bytes));
     count_launch();
     band2_kernel<T, N4, PA><<<(unsigned)op->band_grid, NTHR, C::smem_bytes, s>>>(xm, ym, prm);
     TCA_CUDA_TRY(cudaGetLastError());

@@ -913,12 +913,7 @@ tca_status launch_n4(const tca_operator *op, const PA &prm, cudaStream_t s, cons
         return fail(TCA_ERR_INVALID_ARG, "fused CG step: shape does not fit shared memory");
     } else {
         constexpr size_t smem = FU ? C::smem_fu : C::smem_bytes;
-        static bool attr_set = false;
-        if (!attr_set) {
-            TCA_CUDA_TRY(cudaFuncSetAttribute(band_apply_kernel<T, N4, PA, FU>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr_set = true;
-        }
+        TCA_TRY(set_max_dynamic_smem((const void *)band_apply_kernel<T, N4, PA, FU>, smem));
         count_launch();
         band_apply_kernel<T, N4, PA, FU>
             <<<(unsigned)(FU ? op->band_grid_fu : op->band_grid), C::NTHR, smem, s>>>(xm, ym, prm, rm, fa);

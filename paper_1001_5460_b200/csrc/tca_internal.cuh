@@ -67,7 +67,8 @@ struct CgScalars {
     int32_t pcg;     // 1: preconditioned (rho = <r, z>; beta set by finalize 3)
     double thr;      // tensor Jacobi: absolute threshold on R+*R
     int32_t pad;
-    double red[5];   // reduced dot products (stage sum -> all-reduce -> stage apply)
+    double ref;      // stop reference: rtol is relative to <b, b> (= rho0 when x0 = 0; reading Z28)
+    double red[10];  // reduced dot products (stage sum -> all-reduce -> stage apply); 8, 9: |b - Mx|^2, |b|^2
 };
 
 // Exchange steps of a mode-1 sharded operator (tca_dist.cu).
@@ -176,7 +177,7 @@ struct tca_operator {
     void *p = nullptr;        // ghosted: [ghost | nloc1 own | ghost] slabs
     void *p_own = nullptr;    // p + ghost slabs
     void *t0 = nullptr, *t1 = nullptr;   // multi-pass temporaries (lazy)
-    double *part = nullptr;              // kRedBlocks reduction partials (x2)
+    double *part = nullptr;              // kRedBlocks reduction partials (x3)
     tca::CgScalars *sc = nullptr;        // device scalars
     tca::CgScalars *sc_host = nullptr;   // pinned mirror
     double *hist = nullptr;              // device rho history
@@ -289,16 +290,27 @@ tca_status launch_precond_sweep(const tca_operator *op, int d, const T *src, T *
 tca_status make_dense_mat(tca_dtype dt, const std::vector<double> &M, int n, BandMat *out, size_t *bytes);
 template <typename T>
 void launch_cg_update_r(T *r, const T *q, int64_t N, const CgScalars *sc, double *part, cudaStream_t s);
+// d = b - q: r and p (either may be NULL) receive d; part_dd / part_bb the
+// per-block partials of <d, d> and <b, b> (warm start R := B - A*C, and the
+// true residual of the report)
+template <typename T>
+void launch_resid2(const T *b, const T *q, T *r, T *p, int64_t N, double *part_dd, double *part_bb, cudaStream_t s);
 template <typename T>
 void launch_cg_update_xp(T *x, T *p, const T *r, int64_t N, const CgScalars *sc, cudaStream_t s);
 
-// finalisers (one block): 0 = init rho, 1 = pq -> alpha, 2 = rr -> beta/stop
+// finalisers (one block): 0 = init rho, 1 = pq -> alpha, 2 = rr -> beta/stop,
+// 8 = stop reference <b, b> of a warm start (stage 1 only: red[8], red[9] for the report)
 // stage: 0 = sum the partials and apply (single GPU), 1 = sum into sc->red[which]
 // only, 2 = apply from sc->red[which] (after the all-reduce)
 void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc,
                         double *hist, cudaStream_t s, int stage = 0);
 
 uint64_t stream_key(uint64_t seed, uint32_t stream_id);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) once per (kernel,
+// device, size): the attribute is per device, and the library may drive
+// several devices from several host threads (tca_abi.cu)
+tca_status set_max_dynamic_smem(const void *func, size_t bytes);
 
 // process-wide count of kernel launches issued by the library
 extern std::atomic<int64_t> g_launches;

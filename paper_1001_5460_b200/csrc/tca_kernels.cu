@@ -345,6 +345,37 @@ cg_init_kernel(const T *__restrict__ b, T *__restrict__ x, T *__restrict__ r,
     if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// d = b - q (r, p optional outputs), partials of <d, d> and <b, b>
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+resid2_kernel(const T *__restrict__ b, const T *__restrict__ q, T *__restrict__ r, T *__restrict__ p, int64_t N,
+              double *part_dd, double *part_bb)
+{
+    double dd = 0.0, bb = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const T bv = b[i];
+        const T d = bv - q[i];
+        if (r) r[i] = d;
+        if (p) p[i] = d;
+        dd += (double)d * (double)d;
+        bb += (double)bv * (double)bv;
+    }
+    const double s1 = block_sum(dd);
+    __syncthreads();
+    const double s2 = block_sum(bb);
+    if (threadIdx.x == 0) {
+        part_dd[blockIdx.x] = s1;
+        part_bb[blockIdx.x] = s2;
+    }
+}
+
+template <typename T>
+void launch_resid2(const T *b, const T *q, T *r, T *p, int64_t N, double *part_dd, double *part_bb, cudaStream_t s)
+{
+    count_launch();
+    resid2_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(b, q, r, p, N, part_dd, part_bb);
+}
+
 // 16-byte vector views (2 doubles or 4 floats) for the streaming CG kernels:
 // each thread moves VW elements per access; a scalar tail covers N % VW.
 template <typename T> struct Vec;
@@ -550,7 +581,7 @@ void launch_cg_update_xp(T *x, T *p, const T *r, int64_t N, const CgScalars *sc,
 __global__ void __launch_bounds__(kRedThreads)
 cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgScalars *sc, double *hist, int stage)
 {
-    if (which != 0 && which != 7 && sc->done) {
+    if (which != 0 && which != 7 && which < 8 && sc->done) {
         // stopped in an earlier iteration: this iteration's x update is void
         if (which == 1 && stage != 1 && threadIdx.x == 0) sc->xupd = 0;
         return;
@@ -569,9 +600,14 @@ cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgSca
         if (threadIdx.x != 0) return;
         s = sc->red[which];
     }
+    if (which == 8) {                      // warm start: stop reference <b, b> (reading Z28)
+        sc->ref = s;
+        return;
+    }
     if (which == 0) {                      // rho := R+*R
         sc->rho = s;
         sc->rho0 = s;
+        sc->ref = s;
         sc->rr = s;
         sc->iters = 0;
         sc->converged = 0;
@@ -595,7 +631,7 @@ cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgSca
         if (hist) hist[k] = s;
         if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; if (!sc->pcg) sc->rho = s; return; }
         if (s == 0.0) { sc->converged = 1; sc->done = 1; if (!sc->pcg) sc->rho = s; return; }   // Z12
-        if (sc->rtol2 > 0.0 && s <= sc->rtol2 * sc->rho0) {                                   // Z1, Z2
+        if (sc->rtol2 > 0.0 && s <= sc->rtol2 * sc->ref) {                                    // Z1, Z2, Z28
             sc->converged = 1; sc->done = 1; if (!sc->pcg) sc->rho = s; return;
         }
         if (k >= sc->max_iters) {
@@ -648,9 +684,10 @@ cgsr_finalize_kernel(int which, const double *__restrict__ prr, int nrr, const d
         g = sc->red[3];
         dl = sc->red[4];
     }
-    if (which == 7) {   // gamma0 = <b, b>, delta0 = <b, A b>
+    if (which == 7) {   // gamma0 = <r0, r0>, delta0 = <r0, A r0> (r0 = b when x0 = 0)
         sc->rho = g;
         sc->rho0 = g;
+        sc->ref = g;
         sc->rr = g;
         sc->iters = 0;
         sc->converged = 0;
@@ -673,7 +710,7 @@ cgsr_finalize_kernel(int which, const double *__restrict__ prr, int nrr, const d
     if (hist) hist[k] = g;
     if (!isfinite(g)) { sc->rho = g; sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
     if (g == 0.0) { sc->rho = g; sc->converged = 1; sc->done = 1; return; }
-    if (sc->rtol2 > 0.0 && g <= sc->rtol2 * sc->rho0) { sc->rho = g; sc->converged = 1; sc->done = 1; return; }
+    if (sc->rtol2 > 0.0 && g <= sc->rtol2 * sc->ref) { sc->rho = g; sc->converged = 1; sc->done = 1; return; }
     if (k >= sc->max_iters) {
         sc->rho = g;
         sc->done = 1;
@@ -860,6 +897,8 @@ void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc
                                        cudaStream_t);                                     \
     template void launch_cg_init<T>(const T *, T *, T *, T *, int64_t, double *,          \
                                     cudaStream_t);                                        \
+    template void launch_resid2<T>(const T *, const T *, T *, T *, int64_t, double *,      \
+                                   double *, cudaStream_t);                               \
     template void launch_dot_partials<T>(const T *, const T *, int64_t, double *,         \
                                          const int32_t *, cudaStream_t);                  \
     template void launch_cg_update_r<T>(T *, const T *, int64_t, const CgScalars *,       \

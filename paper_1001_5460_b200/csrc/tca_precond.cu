@@ -311,12 +311,7 @@ tca_status launch_precond_sweep(const tca_operator *op, int d, const T *src, T *
         }
         if (LB >= 32) {
             const size_t smem = (8 * (size_t)len + (size_t)len * (LB + 1)) * es;
-            static bool attr = false;
-            if (!attr) {
-                TCA_CUDA_TRY(cudaFuncSetAttribute(precond_sweep_smem_kernel<T>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
-                attr = true;
-            }
+            TCA_TRY(set_max_dynamic_smem((const void *)precond_sweep_smem_kernel<T>, 110 * 1024));
             count_launch();
             precond_sweep_smem_kernel<T><<<(unsigned)((lines + LB - 1) / LB), 256, smem, s>>>(
                 src, dst, outer, len, inner, (const T *)op->pc_tab[d], LB, done);

@@ -212,12 +212,8 @@ tca_status launch_mode(const tca_operator *op, const void *x, void *out, const v
     const size_t fp = (size_t)g.F[0] * g.F[1] * g.F[2] * g.F[3];
     const size_t smem = fp * sizeof(T);
     const bool full = op->order == 4;
-    static size_t attr[2] = {0, 0};
-    if (smem > attr[full]) {
-        TCA_CUDA_TRY(cudaFuncSetAttribute(full ? scatter_kernel<T, MODE, true> : scatter_kernel<T, MODE, false>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr[full] = smem;
-    }
+    TCA_TRY(set_max_dynamic_smem(full ? (const void *)scatter_kernel<T, MODE, true>
+                                      : (const void *)scatter_kernel<T, MODE, false>, smem));
     count_launch();
     (full ? scatter_kernel<T, MODE, true> : scatter_kernel<T, MODE, false>)<<<(unsigned)op->sc_ntiles, kScatThreads, smem, s>>>(
         g, (const double4 *)op->sc_t, (const int *)op->sc_perm, (const int *)op->sc_tstart, (const T *)x, (T *)out,
@@ -239,15 +235,15 @@ tca_status scatter_prepare(tca_operator *op, int64_t K, const double *t, cudaStr
         g.n[d] = e >= 0 ? (int)op->n[e] : 1;
         g.real[d] = e >= 0 ? 1 : 0;
     }
-    // tile: TB cells of the real modes among 1-3; the footprint pair (xs, qs)
-    // fits two CTAs per SM when it can, one otherwise
+    // tile: TB cells of the real modes among 1-3; the kernel's one footprint
+    // buffer fits two CTAs per SM (113 KB each) when it can, one (227 KB) otherwise
     const size_t es = op->esize;
     int TB = 0;
     for (int cap : {113 * 1024, 227 * 1024}) {
         for (int tb : {4, 2, 1}) {
             size_t fp = (size_t)(g.n[3] + 3);
             for (int d = 0; d < 3; ++d) fp *= g.real[d] ? (size_t)(tb + 3) : 1;
-            if (fp * es <= (size_t)cap / 2) { TB = tb; break; }
+            if (fp * es <= (size_t)cap) { TB = tb; break; }
         }
         if (TB) break;
     }
@@ -307,7 +303,7 @@ tca_status scatter_prepare(tca_operator *op, int64_t K, const double *t, cudaStr
     }
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_tstart, cnt.data(), bs, cudaMemcpyHostToDevice, s));
     TCA_CUDA_TRY(cudaStreamSynchronize(s));   // host vectors go out of scope
-    op->device_bytes += bt + bp + bs;
+    op->device_bytes += bt + bp + bs + std::max<size_t>(perm.size(), 1) * sizeof(double);   // + sc_coef
     return TCA_OK;
 }
 

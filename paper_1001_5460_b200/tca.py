@@ -39,11 +39,16 @@ _i64p = ctypes.POINTER(ctypes.c_int64)
 _dpp = ctypes.POINTER(ctypes.POINTER(ctypes.c_double))
 
 
+def _report(rep):
+    return dict(iterations=rep.iterations, converged=bool(rep.converged), status=rep.status, rho0=rep.rho0,
+                rho_final=rep.rho_final, relres_final=rep.relres_final, seconds=rep.seconds)
+
+
 class CgReport(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
                 ("status", ctypes.c_int32), ("pad", ctypes.c_int32),
                 ("rho0", ctypes.c_double), ("rho_final", ctypes.c_double),
-                ("seconds", ctypes.c_double),
+                ("relres_final", ctypes.c_double), ("seconds", ctypes.c_double),
                 ("rho_history", ctypes.POINTER(ctypes.c_double)),
                 ("history_capacity", ctypes.c_int32), ("pad2", ctypes.c_int32)]
 
@@ -62,7 +67,7 @@ _lib.tca_operator_query.argtypes = [_vp, _i64p, _i64p, _i64p, _i64p,
                                     ctypes.POINTER(ctypes.c_size_t)]
 _lib.tca_apply.argtypes = [_vp, _vp, _vp, _vp]
 _lib.tca_rhs.argtypes = [_vp, _vp, _vp, _vp]
-_lib.tca_cg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32,
+_lib.tca_cg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int32,
                               ctypes.POINTER(CgReport), _vp]
 _lib.tca_solve_host.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32,
                                 ctypes.POINTER(CgReport), _vp]
@@ -97,9 +102,9 @@ _lib.tca_local_group_destroy.restype = None
 _lib.tca_operator_apply_path.argtypes = [_vp]
 _lib.tca_operator_cg_fused_step.argtypes = [_vp]
 _lib.tca_operator_cg_fused_step.restype = ctypes.c_int
-_lib.tca_pcg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
+_lib.tca_pcg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int32, _vp, _vp]
 _lib.tca_precond_apply.argtypes = [_vp, _vp, _vp, _vp]
-_lib.tca_cgsr_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
+_lib.tca_cgsr_solve.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int32, _vp, _vp]
 _lib.tca_jacobi_solve.argtypes = [_vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp]
 _lib.tca_operator_create_gram.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _i64p, _dpp, _dpp, ctypes.c_double,
                                           ctypes.c_int, _vp, _vp]
@@ -346,14 +351,16 @@ class Operator:
         return b
 
     def cg_solve(self, b, x=None, rtol=0.0, max_iters=100, history=False, stream=None,
-                 raise_on=("breakdown", "nonfinite")):
-        """Fig. 2 CG from x0 = 0.  Returns (x, report dict)."""
-        return self._solve(_lib.tca_cg_solve, "tca_cg_solve", b, x, rtol, max_iters, history, stream, raise_on)
+                 raise_on=("breakdown", "nonfinite"), x0=None):
+        """Fig. 2 CG from x0 = 0, or from the device tensor x0 (warm start: R := B - A*C).
+        Returns (x, report dict)."""
+        return self._solve(_lib.tca_cg_solve, "tca_cg_solve", b, x, rtol, max_iters, history, stream, raise_on, x0)
 
     def pcg_solve(self, b, x=None, rtol=0.0, max_iters=100, history=False, stream=None,
-                  raise_on=("breakdown", "nonfinite")):
+                  raise_on=("breakdown", "nonfinite"), x0=None):
         """CG preconditioned with the Kronecker-factor P (tca_pcg_solve).  Returns (x, report dict)."""
-        return self._solve(_lib.tca_pcg_solve, "tca_pcg_solve", b, x, rtol, max_iters, history, stream, raise_on)
+        return self._solve(_lib.tca_pcg_solve, "tca_pcg_solve", b, x, rtol, max_iters, history, stream, raise_on,
+                           x0)
 
     def jacobi_solve(self, b, x=None, threshold=1e-4, max_iters=100000, history=False, stream=None):
         """Tensor Jacobi (Fig. 1, tca_jacobi_solve): x <- U with R+*R <= threshold."""
@@ -361,30 +368,34 @@ class Operator:
                            ("nonfinite",))
 
     def cgsr_solve(self, b, x=None, rtol=0.0, max_iters=100, history=False, stream=None,
-                   raise_on=("breakdown", "nonfinite")):
+                   raise_on=("breakdown", "nonfinite"), x0=None):
         """Single-reduction (Chronopoulos-Gear) CG (tca_cgsr_solve).  Returns (x, report dict)."""
-        return self._solve(_lib.tca_cgsr_solve, "tca_cgsr_solve", b, x, rtol, max_iters, history, stream, raise_on)
+        return self._solve(_lib.tca_cgsr_solve, "tca_cgsr_solve", b, x, rtol, max_iters, history, stream, raise_on,
+                           x0)
 
-    def _solve(self, fn, name, b, x, rtol, max_iters, history, stream, raise_on):
+    def _solve(self, fn, name, b, x, rtol, max_iters, history, stream, raise_on, x0=None):
         if x is None:
             x = self.empty()
+        if x0 is not None:   # the C ABI's x0_zero = 0: x holds the start on entry
+            _dev_ptr(x0, self.N, self.torch_dtype, "x0")
+            x.copy_(x0)
         rep = CgReport()
         hist = None
         if history:
             hist = np.zeros(max_iters + 1)
             rep.rho_history = hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
             rep.history_capacity = max_iters + 1
-        st = fn(self._h, _dev_ptr(b, self.N, self.torch_dtype, "b"),
-                _dev_ptr(x, self.N, self.torch_dtype, "x"), float(rtol),
-                int(max_iters), ctypes.byref(rep), _vp(_stream_ptr(stream)))
+        args = [self._h, _dev_ptr(b, self.N, self.torch_dtype, "b"), _dev_ptr(x, self.N, self.torch_dtype, "x")]
+        if fn is not _lib.tca_jacobi_solve:
+            args.append(0 if x0 is not None else 1)   # x0_zero
+        st = fn(*args, float(rtol), int(max_iters), ctypes.byref(rep), _vp(_stream_ptr(stream)))
         allow = [NOT_CONVERGED]
         if "breakdown" not in raise_on:
             allow.append(ERR_BREAKDOWN)
         if "nonfinite" not in raise_on:
             allow.append(ERR_NONFINITE)
         _check(st, name, allow=allow)
-        out = dict(iterations=rep.iterations, converged=bool(rep.converged), status=rep.status,
-                   rho0=rep.rho0, rho_final=rep.rho_final, seconds=rep.seconds)
+        out = _report(rep)
         if hist is not None:
             out["rho_history"] = hist[: rep.iterations + 1]
         return x, out
@@ -422,8 +433,7 @@ class Operator:
         st = _lib.tca_solve_host_batch(self._h, n, ys, xs, float(rtol), int(max_iters), reps,
                                        _vp(_stream_ptr(stream)))
         _check(st, "tca_solve_host_batch", allow=[NOT_CONVERGED])
-        return [dict(iterations=r.iterations, converged=bool(r.converged), status=r.status,
-                     rho0=r.rho0, rho_final=r.rho_final, seconds=r.seconds) for r in reps[:n]]
+        return [_report(r) for r in reps[:n]]
 
     def solve_host(self, ydata_host, x_host, rtol=0.0, max_iters=100, stream=None):
         """End-to-end solve from host buffers (torch CPU tensors, pinned recommended)."""
@@ -437,8 +447,7 @@ class Operator:
                                  _vp(_stream_ptr(stream)))
         _check(st, "tca_solve_host", allow=[NOT_CONVERGED])
         del torch
-        return dict(iterations=rep.iterations, converged=bool(rep.converged), status=rep.status,
-                    rho0=rep.rho0, rho_final=rep.rho_final, seconds=rep.seconds)
+        return _report(rep)
 
     def forward_model(self, x=None, ydata=None, sigma=0.01, seed=1, stream=None):
         """ydata = (kron A_d) x + sigma * noise(seed); x None -> x_true(seed) generated on device."""

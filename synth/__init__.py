@@ -19,7 +19,8 @@ Readings of the paper used here:
 
 The counter generator is SplitMix64's output function applied to
 key + idx * GAMMA (mod 2^64); the CUDA generator in the product implements
-the same integer recipe independently (csrc/tca_generate.cu).
+the same integer recipe independently (gen_normal_kernel in
+paper_1001_5460_b200/csrc/tca_kernels.cu).
 """
 from __future__ import annotations
 

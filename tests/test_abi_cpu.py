@@ -73,10 +73,11 @@ def test_null_operator_calls_fail_cleanly():
     from paper_1001_5460_b200 import tca
     assert tca._lib.tca_apply(None, None, None, None) == tca.ERR_INVALID_ARG
     assert tca._lib.tca_rhs(None, None, None, None) == tca.ERR_INVALID_ARG
-    assert tca._lib.tca_cg_solve(None, None, None, 0.0, 1, None, None) == tca.ERR_INVALID_ARG
+    for x0_zero in (0, 1):
+        for fn in (tca._lib.tca_cg_solve, tca._lib.tca_pcg_solve, tca._lib.tca_cgsr_solve):
+            assert fn(None, None, None, x0_zero, 0.0, 1, None, None) == tca.ERR_INVALID_ARG
     assert tca._lib.tca_generate_normal(None, 0, 5, 0, 1, 0, 1.0, None) == tca.ERR_INVALID_ARG
-    for fn in (tca._lib.tca_pcg_solve, tca._lib.tca_cgsr_solve, tca._lib.tca_jacobi_solve):
-        assert fn(None, None, None, 0.0, 1, None, None) == tca.ERR_INVALID_ARG
+    assert tca._lib.tca_jacobi_solve(None, None, None, 0.0, 1, None, None) == tca.ERR_INVALID_ARG
     assert tca._lib.tca_precond_apply(None, None, None, None) == tca.ERR_INVALID_ARG
     assert tca._lib.tca_operator_create_gram(None, 3, None, None, None, 1.0, 0, None, None) == tca.ERR_INVALID_ARG
     assert tca._lib.tca_solve_host_batch(None, 1, None, None, 0.0, 1, None, None) == tca.ERR_INVALID_ARG

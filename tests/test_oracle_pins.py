@@ -645,3 +645,112 @@ def test_P16_scattered_cg_equals_dense_solve():
     assert st == oracle.OK
     ref = np.linalg.solve(M, b.ravel())
     assert np.linalg.norm(x.ravel() - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+# ---------------------------------------------------------------- P17: warm start (Fig. 2's R := B - A*C with C != 0)
+def _numpy_cg(K, b, x0, k):
+    """Textbook CG (the recurrences of Fig. 2) in numpy on a
+    dense SPD matrix, k steps from x0."""
+    x = x0.copy()
+    r = b - K @ x
+    p = r.copy()
+    rho = r @ r
+    for _ in range(k):
+        q = K @ p
+        alpha = rho / (p @ q)
+        x = x + alpha * p
+        r = r - alpha * q
+        rho1 = r @ r
+        p = r + (rho1 / rho) * p
+        rho = rho1
+    return x
+
+
+@pytest.mark.parametrize("n,m", TINY_SHAPES)
+def test_P17_warm_start_iterates_equal_dense_cg_and_first_step_is_steepest_descent(n, m):
+    """R := B - A*C, P := R.  Step 1 from C is the exact
+    steepest-descent step x1 = x0 + (r0.r0 / r0.K r0) r0 (closed form), and
+    steps 2..4 equal textbook CG on the brute-force K from the same x0."""
+    A, L, op = tiny_problem(n, m)
+    K = brute_force_K(A, L, op.lam)
+    b = synth.random_tensor(n, seed=31)
+    x0 = synth.random_tensor(n, seed=32, stream=8)
+    r0 = b.ravel() - K @ x0.ravel()
+    x1_ref = x0.ravel() + (r0 @ r0) / (r0 @ K @ r0) * r0
+    x1, k1, st, hist = op.cg(b, rtol=0.0, max_iters=1, x0=x0)
+    assert k1 == 1 and st == oracle.OK
+    assert abs(hist[0] - r0 @ r0) <= 1e-12 * (r0 @ r0)          # rho_0 = <B - A C, B - A C>
+    assert np.linalg.norm(x1.ravel() - x1_ref) <= 1e-12 * np.linalg.norm(x1_ref)
+    for k in (2, 3, 4):
+        xk, _, _, _ = op.cg(b, rtol=0.0, max_iters=k, x0=x0)
+        ref = _numpy_cg(K, b.ravel(), x0.ravel(), k)
+        assert np.linalg.norm(xk.ravel() - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("solver", ["cg", "pcg", "cgsr"])
+def test_P17_warm_start_converges_to_dense_solve_with_b_relative_stop(solver):
+    """Warm start to tolerance: the stop reference is <b, b> (reading Z28), and
+    the converged solution is the dense direct solve of the brute-force K."""
+    n, m = (5, 4, 3), (8, 7, 6)
+    A, L, op = tiny_problem(n, m)
+    K = brute_force_K(A, L, op.lam)
+    b = synth.random_tensor(n, seed=33)
+    x0 = 3.0 * synth.random_tensor(n, seed=34, stream=8)
+    x, k, st, hist = getattr(op, solver)(b, rtol=1e-12, max_iters=2000, x0=x0)
+    assert st == oracle.OK
+    assert hist[-1] <= 1e-24 * float(b.ravel() @ b.ravel())
+    ref = np.linalg.solve(K, b.ravel())
+    assert np.linalg.norm(x.ravel() - ref) <= 1e-9 * np.linalg.norm(ref)
+    # started at the solution: the initial residual is rounding-level and one step ends it
+    xs, ks, sts, hs = getattr(op, solver)(b, rtol=1e-8, max_iters=50, x0=ref.reshape(n))
+    assert sts == oracle.OK and ks <= 1
+    assert np.linalg.norm(xs.ravel() - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+# ---------------------------------------------------------------- P18: PCG iterates (reading Z22)
+@pytest.mark.parametrize("n,m", TINY_SHAPES[:2] + [((6, 5), (9, 9))])
+def test_P18_pcg_iterates_equal_cg_on_split_preconditioned_system(n, m):
+    """Preconditioned CG with P = C C^T produces x_k = C^-T xh_k where xh_k are
+    plain CG iterates on (C^-1 K C^-T) xh = C^-1 b (textbook equivalence).  P =
+    kron F_d, F_d = G_d + eps_d R_d with G_d, R_d, gbar from numpy only (reading
+    Z22).  A beta built from <r, r> instead of <r, z> fails this from k = 2 on."""
+    A, L, op = tiny_problem(n, m)
+    K = brute_force_K(A, L, op.lam)
+    G = [a.T @ a for a in A]
+    R = [l.T @ l if l is not None and l.shape[0] else np.zeros_like(g) for l, g in zip(L, G)]
+    gbar = [float(np.exp(np.mean(np.log(np.linalg.eigvalsh(g))))) for g in G]
+    P = np.ones((1, 1))
+    for d in range(len(G)):
+        eps = op.lam / float(np.prod([gbar[e] for e in range(len(G)) if e != d]))
+        P = np.kron(P, G[d] + eps * R[d])
+    C = np.linalg.cholesky(P)
+    Ci = np.linalg.inv(C)
+    Kh = Ci @ K @ Ci.T
+    b = synth.random_tensor(n, seed=35).ravel()
+    bh = Ci @ b
+
+    def wrong_beta_pcg(k):   # beta = <r1, r1> / <r, r> with z = P^-1 r directions
+        x = np.zeros_like(b)
+        r = b.copy()
+        z = np.linalg.solve(P, r)
+        p = z.copy()
+        rho, rr = r @ z, r @ r
+        for _ in range(k):
+            q = K @ p
+            alpha = rho / (p @ q)
+            x, r = x + alpha * p, r - alpha * q
+            z = np.linalg.solve(P, r)
+            rr1 = r @ r
+            p = z + (rr1 / rr) * p
+            rho, rr = r @ z, rr1
+        return x
+
+    for k in (1, 2, 3, 4):
+        xk, kk, st, _ = op.pcg(b.reshape(n), rtol=0.0, max_iters=k)
+        assert kk == k and st == oracle.OK
+        ref = Ci.T @ _numpy_cg(Kh, bh, np.zeros_like(bh), k)
+        err = np.linalg.norm(xk.ravel() - ref) / np.linalg.norm(ref)
+        assert err <= 1e-10
+        if k >= 2:   # the pin discriminates the preconditioned beta
+            wrong = wrong_beta_pcg(k)
+            assert np.linalg.norm(wrong - ref) / np.linalg.norm(ref) > 1e3 * max(err, 1e-14)
