@@ -56,7 +56,25 @@ def parse():
                          "Jacobi (--solver jacobi, threshold --rtol, default 1e-4) or CG; scattered: Sec. 4's "
                          "spline reconstruction from 9e6 scattered samples on 128x128x128x16")
     ap.add_argument("--samples", type=int, default=None, help="scattered workload: sample count (default 9e6)")
+    ap.add_argument("--cfg4-iters", type=int, default=20,
+                    help="CG iterations of the config-4 scaling measurement added to the line (0: skip)")
     return ap.parse_args()
+
+
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
+
+
+def spawn_ranks(nproc, script, script_args, env=None):
+    """One process per GPU on this node: re-run `script` under torch.distributed.run
+    (rendezvous on 127.0.0.1) with the same arguments; rank 0 prints the line.
+    Returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", script, *script_args]
+    return subprocess.call(cmd, env=env)
 
 
 def peaks():
@@ -367,6 +385,41 @@ def run_tca(args):
               "cg_us_per_iteration": rep["seconds"] * 1e6 / max(1, rep["iterations"]),
               "apply_us_in_cg": apply_us}
 
+    # ---- north_star's scaling system (config 4: 256^3 x 32 fp64, mode 1 sharded over
+    # the ranks) at this N: ms per CG iteration of the device-resident solve (max
+    # over ranks), outside the config-3 timed region.  SCALE runs compare it over N.
+    scale4 = None
+    if args.cfg4_iters > 0 and args.workload == "fit" and args.solver in ("cg", "cgsr"):
+        c4 = synth.CONFIGS[4]
+        A4, L4 = synth.mode_matrices(c4)
+        op4 = tca.Operator(A4, L4, c4.lam, dtype="f64", dist=dist_arg)
+        y4 = op4.forward_model(None, sigma=synth.NOISE_SIGMA, seed=1)
+        b4 = op4.rhs(y4)
+        del y4
+        fn4 = getattr(op4, solver_fn if args.solver != "pcg" else "cg_solve")
+        fn4(b4, rtol=0.0, max_iters=min(5, args.cfg4_iters))   # warm-up (graph capture)
+        op4.set_timing(True)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        x4, rep4 = fn4(b4, rtol=0.0, max_iters=args.cfg4_iters)
+        e1.record(stream)
+        barrier()
+        ms4 = max_over_ranks(e0.elapsed_time(e1))
+        ams4, acnt4 = op4.get_timing()
+        a4_us = max_over_ranks(1e3 * ams4 / max(1, acnt4))
+        scale4 = {"workload": f"config 4: {'x'.join(map(str, c4.n))} unknowns f64, data {'x'.join(map(str, c4.m))}, "
+                              f"lambda {c4.lam:g}, {args.solver.upper()} from x0 = 0, mode 1 sharded over {world} GPU(s)",
+                  "n_gpus": world, "iterations": rep4["iterations"], "ms": ms4,
+                  "ms_per_iteration": ms4 / max(1, rep4["iterations"]),
+                  "iters_per_s": rep4["iterations"] / (ms4 * 1e-3),
+                  "apply_us_per_rank": a4_us, "local_unknowns": int(np.prod(op4.local_n)),
+                  "timing": "CUDA events around one device-resident solve, max over ranks"}
+        del x4, b4
+        op4.close()
+        torch.cuda.empty_cache()
+
     e2e = None
     if not args.no_e2e and args.solver == "cg":   # (tca_solve_host runs plain CG)
         yh = torch.empty(local_m, dtype=tdt, pin_memory=True)
@@ -377,7 +430,7 @@ def run_tca(args):
         op.close()
         # K steps through the pipelined host API: one operator, K data sets; every
         # step's H2D of y and D2H of x run on a copy stream under its neighbours' compute
-        e_steps = max(2, min(args.steps, 4))
+        e_steps = max(2, args.steps)
         barrier()
         t0 = time.perf_counter()
         e0.record(stream)
@@ -427,11 +480,13 @@ def run_tca(args):
         "apply": apply_info,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "scaling_config4": scale4,
         "gpu_launches": int(launches),
         "clocks": clk,
         "time_to_solution_ms": total_ms / args.steps,
         "cg_report": {"iterations": rep["iterations"], "rho0": rep["rho0"],
-                      "rho_final": rep["rho_final"], "status": rep["status"]},
+                      "rho_final": rep["rho_final"], "relres_final": rep["relres_final"],
+                      "status": rep["status"]},
         "apply_path": state["path"],
         "phases": phases,
         "step_host_ms": state.get("host_ms"),   # [create, rhs enqueue, solve (synchronous), solve device, destroy] per timed step
@@ -591,6 +646,15 @@ def run_scattered(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: start the N ranks here
+        if args.impl == "tca":
+            import torch
+            if torch.cuda.device_count() < args.gpus:
+                print(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} visible CUDA "
+                      f"device(s)", file=sys.stderr)
+                return 2
+        return spawn_ranks(args.gpus, os.path.abspath(__file__), sys.argv[1:])
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "poisson":

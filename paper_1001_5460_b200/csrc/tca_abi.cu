@@ -507,6 +507,16 @@ static tca_status harvest_timing(tca_operator *op)
     return TCA_OK;
 }
 
+// Host wait at the solvers' synchronisation points: on a sharded operator the
+// transport's (NCCL: polls the asynchronous error state, aborts on an error or
+// timeout and returns TCA_ERR_NCCL instead of hanging on a dead peer)
+static tca_status sync_solve(tca_operator *op, cudaStream_t s)
+{
+    if (op->transport) return op->transport->wait(s);
+    TCA_CUDA_TRY(cudaStreamSynchronize(s));
+    return TCA_OK;
+}
+
 // Dot-product finalisation: single GPU one kernel; sharded: local sum, all-reduce
 // of the fp64 scalar over the shards, then the scalar update.
 static tca_status cg_reduce(tca_operator *op, int which, const double *part, int nparts, cudaStream_t s)
@@ -635,6 +645,27 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
         TCA_TRY(cg_reduce(op, 3, op->part, kRedBlocks, s));          // rho1, beta
         d = z;
     }
+    const int64_t hb = (int64_t)kHG * op->slab;   // elements of the 3 boundary slabs
+    if (op->transport && op->transport->async_halo() && op->nloc1 > 2 * kHG && (hb * op->esize) % 16 == 0) {
+        // the boundary slabs of P first; their halo exchange runs on a side
+        // stream under the update of the interior slabs (joined before the
+        // next apply, which is the only reader of the ghost slabs)
+        const int64_t n = op->N;
+        if (!op->hstream) {
+            TCA_CUDA_TRY(cudaStreamCreateWithFlags(&op->hstream, cudaStreamNonBlocking));
+            TCA_CUDA_TRY(cudaEventCreateWithFlags(&op->hfork, cudaEventDisableTiming));
+            TCA_CUDA_TRY(cudaEventCreateWithFlags(&op->hjoin, cudaEventDisableTiming));
+        }
+        launch_cg_update_xp<T>(x, p, d, hb, op->sc, s);                              // slabs [0, 3)
+        launch_cg_update_xp<T>(x + n - hb, p + n - hb, d + n - hb, hb, op->sc, s);   // slabs [nloc-3, nloc)
+        TCA_CUDA_TRY(cudaEventRecord(op->hfork, s));
+        TCA_CUDA_TRY(cudaStreamWaitEvent(op->hstream, op->hfork, 0));
+        TCA_TRY(halo_p(op, op->hstream));
+        TCA_CUDA_TRY(cudaEventRecord(op->hjoin, op->hstream));
+        launch_cg_update_xp<T>(x + hb, p + hb, d + hb, n - 2 * hb, op->sc, s);       // interior
+        TCA_CUDA_TRY(cudaStreamWaitEvent(s, op->hjoin, 0));
+        return TCA_OK;
+    }
     launch_cg_update_xp<T>(x, p, d, op->N, op->sc, s);               // C := C + alpha*P*D, P := R|Z + beta*P
     return halo_p(op, s);                                             // ghost slabs of P
 }
@@ -723,7 +754,7 @@ static tca_status cg_graph_loop(tca_operator *op, T *x, double rtol, int32_t max
         if (rtol > 0.0) {   // tolerance stop: check the device flag once per chunk
             TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost,
                                          op->gstream));
-            TCA_CUDA_TRY(cudaStreamSynchronize(op->gstream));
+            TCA_TRY(sync_solve(op, op->gstream));
             if (op->sc_host->done) break;
         }
         g = (g + 1) % ng;
@@ -852,7 +883,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
             for (int i = 0; i < c; ++i) TCA_TRY(cg_iteration<T>(op, x, s));
             TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars),
                                          cudaMemcpyDeviceToHost, s));
-            TCA_CUDA_TRY(cudaStreamSynchronize(s));
+            TCA_TRY(sync_solve(op, s));
             if (op->timing) TCA_TRY(harvest_timing(op));
             if (op->sc_host->done) break;
         }
@@ -870,7 +901,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
         if (op->transport) TCA_TRY(op->transport->allreduce(&op->sc->red[8], 2, s));
     }
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc_host, op->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
-    TCA_CUDA_TRY(cudaStreamSynchronize(s));
+    TCA_TRY(sync_solve(op, s));
     if (op->timing) TCA_TRY(harvest_timing(op));
     const CgScalars &r = *op->sc_host;
     if (rep) {
@@ -940,6 +971,9 @@ void tca_operator_destroy(tca_operator *op)
     if (op->gstream) cudaStreamDestroy(op->gstream);
     if (op->gfork) cudaEventDestroy(op->gfork);
     if (op->gjoin) cudaEventDestroy(op->gjoin);
+    if (op->hstream) cudaStreamDestroy(op->hstream);
+    if (op->hfork) cudaEventDestroy(op->hfork);
+    if (op->hjoin) cudaEventDestroy(op->hjoin);
     // every stream that used the operator is done before its memory goes back
     cudaDeviceSynchronize();
     void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp, op->sr_s, op->p2,

@@ -12,7 +12,9 @@
 // devices) synchronised on the host -- test transport for hosts with fewer
 // GPUs than shards; it moves the same bytes with cudaMemcpy.
 #include <dlfcn.h>
+#include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #include <condition_variable>
 #include <mutex>
@@ -51,7 +53,7 @@ namespace {
 
 typedef struct { char internal[128]; } ncclUniqueId_t;
 typedef void *ncclComm_t;
-enum { ncclSuccess = 0 };
+enum { ncclSuccess = 0, ncclInProgress = 7 };
 enum { ncclFloat64 = 8 };
 enum { ncclSum = 0 };
 
@@ -66,6 +68,8 @@ struct NcclApi {
     int (*GroupStart)() = nullptr;
     int (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(int) = nullptr;
+    int (*CommGetAsyncError)(ncclComm_t, int *) = nullptr;   // optional (error polling)
+    int (*CommAbort)(ncclComm_t) = nullptr;                  // optional
     bool ok = false;
 };
 
@@ -92,6 +96,8 @@ NcclApi &nccl()
         api.GroupStart = (int (*)())sym("ncclGroupStart");
         api.GroupEnd = (int (*)())sym("ncclGroupEnd");
         api.GetErrorString = (const char *(*)(int))sym("ncclGetErrorString");
+        api.CommGetAsyncError = (int (*)(ncclComm_t, int *))sym("ncclCommGetAsyncError");
+        api.CommAbort = (int (*)(ncclComm_t))sym("ncclCommAbort");
         api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Send && api.Recv &&
                  api.GroupStart && api.GroupEnd;
     });
@@ -114,14 +120,50 @@ class NcclTransport final : public Transport {
   public:
     NcclTransport(void *comm, int rank, int nranks) : comm_(comm), rank_(rank), nranks_(nranks) {}
     bool capturable() const override { return true; }   // NCCL collectives and p2p capture into graphs
+    bool async_halo() const override { return true; }   // stream-ordered: may run on a side stream
     tca_status allreduce(double *dev, int count, cudaStream_t s) override
     {
+        if (aborted_) return fail(TCA_ERR_NCCL, "NCCL communicator aborted after an earlier error");
         TCA_NCCL_TRY(nccl().AllReduce(dev, dev, (size_t)count, ncclFloat64, ncclSum, comm_, s));
         return TCA_OK;
+    }
+    // Host wait for `s` that does not hang on a dead peer: poll the stream and
+    // the communicator's asynchronous error state; on an NCCL error or after
+    // TCA_NCCL_TIMEOUT_S seconds (default 1800) the communicator is aborted
+    // (its kernels return) and TCA_ERR_NCCL is reported.
+    tca_status wait(cudaStream_t s) override
+    {
+        static const double limit = [] {
+            const char *e = getenv("TCA_NCCL_TIMEOUT_S");
+            return e ? atof(e) : 1800.0;
+        }();
+        timespec t0;
+        clock_gettime(CLOCK_MONOTONIC, &t0);
+        for (;;) {
+            const cudaError_t q = cudaStreamQuery(s);
+            if (q == cudaSuccess) return TCA_OK;
+            if (q != cudaErrorNotReady) return cuda_fail(q, "stream (sharded solve)");
+            int ae = ncclSuccess;
+            if (nccl().CommGetAsyncError && nccl().CommGetAsyncError(comm_, &ae) == ncclSuccess &&
+                ae != ncclSuccess && ae != ncclInProgress) {
+                abort_comm();
+                return nccl_fail(ae, "asynchronous NCCL error");
+            }
+            timespec t1;
+            clock_gettime(CLOCK_MONOTONIC, &t1);
+            if ((t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec) > limit) {
+                abort_comm();
+                return fail(TCA_ERR_NCCL, "sharded solve: no completion within TCA_NCCL_TIMEOUT_S (" +
+                                              std::to_string(limit) + " s); communicator aborted");
+            }
+            const timespec nap{0, 50000};
+            nanosleep(&nap, nullptr);
+        }
     }
     tca_status halo(int which, char *ext, size_t slab_bytes, int64_t nloc, cudaStream_t s) override
     {
         (void)which;
+        if (aborted_) return fail(TCA_ERR_NCCL, "NCCL communicator aborted after an earlier error");
         const size_t hb = (size_t)kHG * slab_bytes;   // 3 slabs
         char *own_first = ext + hb, *own_last = ext + (size_t)nloc * slab_bytes;   // [3, 6) and [nloc, nloc+3)
         char *ghost_lo = ext, *ghost_hi = ext + (size_t)(nloc + kHG) * slab_bytes;
@@ -139,8 +181,14 @@ class NcclTransport final : public Transport {
     }
 
   private:
+    void abort_comm()
+    {
+        if (!aborted_ && nccl().CommAbort) nccl().CommAbort(comm_);
+        aborted_ = true;
+    }
     void *comm_;
     int rank_, nranks_;
+    bool aborted_ = false;
 };
 
 }  // namespace

@@ -84,6 +84,14 @@ class Transport {
     // true when the exchanges are stream-ordered device operations that can be
     // captured into a CUDA graph (NCCL); false for host-synchronised ones
     virtual bool capturable() const { return false; }
+    // true when halo() may be issued on a side stream joined by events (overlap)
+    virtual bool async_halo() const { return false; }
+    // host wait for stream s (NCCL: polls the communicator's error state, with a timeout)
+    virtual tca_status wait(cudaStream_t s)
+    {
+        const cudaError_t e = cudaStreamSynchronize(s);
+        return e == cudaSuccess ? TCA_OK : cuda_fail(e, "stream");
+    }
 };
 Transport *make_transport(const tca_dist *d);
 tca_status shard_layout(int64_t n1, const double *A1, int64_t m1, int rank, int nranks, int64_t out[4]);
@@ -220,6 +228,9 @@ struct tca_operator {
     std::vector<cudaEvent_t> gev[2];     // captured (external) event pairs of instance g
     std::vector<cudaEvent_t> *cap_ev = nullptr;   // event list being captured into
     cudaEvent_t gfork = nullptr, gjoin = nullptr;
+    // sharded CG: the halo of p on a side stream under the interior p update
+    cudaStream_t hstream = nullptr;
+    cudaEvent_t hfork = nullptr, hjoin = nullptr;
     // timing instrumentation
     int timing = 0;
     std::vector<cudaEvent_t> tev;        // pairs (start, stop)
