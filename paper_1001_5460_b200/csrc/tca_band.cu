@@ -24,6 +24,10 @@ extern template tca_status launch_dispatch<ParamsG<double>>(const tca_operator *
                                                             const CUtensorMap *, const CUtensorMap *);
 extern template tca_status launch_dispatch<ParamsG<float>>(const tca_operator *, const ParamsG<float> &, cudaStream_t,
                                                            const CUtensorMap *, const CUtensorMap *);
+extern template tca_status launch_dispatch<ParamsH<double>>(const tca_operator *, const ParamsH<double> &, cudaStream_t,
+                                                            const CUtensorMap *, const CUtensorMap *);
+extern template tca_status launch_dispatch<ParamsH<float>>(const tca_operator *, const ParamsH<float> &, cudaStream_t,
+                                                           const CUtensorMap *, const CUtensorMap *);
 extern template int t3_for<double>(int);
 extern template int t3_for<float>(int);
 extern template int boxw_for<double>(int);
@@ -38,6 +42,8 @@ extern template int unit_for<float>(int);
 extern template int pitched_for<double>(int);
 extern template int pitched_for<float>(int);
 extern template int minb_for<float>(int);
+extern template int padded_s3_for<double>(int);
+extern template int padded_s3_for<float>(int);
 extern template tca_status launch_dispatch_fu<Params<double>>(const tca_operator *, const Params<double> &,
                                                               cudaStream_t, const CUtensorMap *, const CUtensorMap *,
                                                               const CUtensorMap *, const FuArgs<double> &);
@@ -55,6 +61,10 @@ extern template tca_status launch_dispatch<band::Params<float>>(const tca_operat
 extern template tca_status launch_dispatch<band::ParamsG<double>>(const tca_operator *, const band::ParamsG<double> &,
                                                                   cudaStream_t, const CUtensorMap *, const CUtensorMap *);
 extern template tca_status launch_dispatch<band::ParamsG<float>>(const tca_operator *, const band::ParamsG<float> &,
+                                                                 cudaStream_t, const CUtensorMap *, const CUtensorMap *);
+extern template tca_status launch_dispatch<band::ParamsH<double>>(const tca_operator *, const band::ParamsH<double> &,
+                                                                  cudaStream_t, const CUtensorMap *, const CUtensorMap *);
+extern template tca_status launch_dispatch<band::ParamsH<float>>(const tca_operator *, const band::ParamsH<float> &,
                                                                  cudaStream_t, const CUtensorMap *, const CUtensorMap *);
 extern template int pp_for<double>(int);
 extern template int pp_for<float>(int);
@@ -133,10 +143,21 @@ tca_status build_params(const tca_operator *op_c, std::vector<unsigned char> &bl
     tca_operator *op = const_cast<tca_operator *>(op_c);
     const bool in_block = tables_fit(op);
     if (fu && !in_block) return TCA_OK;   // B1' takes parameter-block tables only (caller checks the blob)
-    if (!fu) op->band_gt = !in_block;
-    blob.assign(in_block ? sizeof(band::Params<T>) : sizeof(band::ParamsG<T>), 0);
-    auto *p = reinterpret_cast<band::ParamsBase<T> *>(blob.data());
     const TableLayout L = table_layout(op);
+    // records kept in the block: all (Params); else modes 4 and 3 (ParamsH) or mode 4 (ParamsG),
+    // the whole table also in global memory (table order: mode 4, 3, 2, 1)
+    const size_t cap = band::TAP_BYTES / sizeof(T);
+    size_t block_rows = (size_t)L.total;
+    if (!in_block) {
+        if ((size_t)L.off[1] * band::REC <= cap) { op->band_gt = 2; block_rows = (size_t)L.off[1]; }
+        else if ((size_t)L.off[2] * band::REC <= cap) { op->band_gt = 1; block_rows = (size_t)L.off[2]; }
+        else return fail(TCA_ERR_SHAPE, "band apply: the mode-4 tap table does not fit the parameter block");
+    } else if (!fu) {
+        op->band_gt = 0;
+    }
+    blob.assign(op->band_gt == 0 || fu ? sizeof(band::Params<T>) : sizeof(band::ParamsH<T>), 0);
+    static_assert(sizeof(band::ParamsG<float>) == sizeof(band::ParamsH<float>), "one blob size");
+    auto *p = reinterpret_cast<band::ParamsBase<T> *>(blob.data());
     const int t3 = t3_of(op);
     p->n1 = (int)op->nloc1;
     p->onebox = onebox_of(op) ? 1 : 0;
@@ -213,12 +234,14 @@ tca_status build_params(const tca_operator *op_c, std::vector<unsigned char> &bl
     }
     if (in_block) {
         std::memcpy(reinterpret_cast<band::Params<T> *>(blob.data())->taps, taps.data(), taps.size() * sizeof(T));
-    } else if (!fu) {   // global tables (uploaded once; freed with the operator)
+    } else if (!fu) {   // global tables (uploaded once; freed with the operator) + the block's prefix
         const size_t nb = taps.size() * sizeof(T);
         TCA_CUDA_TRY(dev_get(&op->band_gtaps, nb));
         op->band_gtaps_bytes = nb;
         TCA_CUDA_TRY(cudaMemcpy(op->band_gtaps, taps.data(), nb, cudaMemcpyHostToDevice));
-        reinterpret_cast<band::ParamsG<T> *>(blob.data())->gtaps = (const T *)op->band_gtaps;
+        auto *g = reinterpret_cast<band::ParamsH<T> *>(blob.data());   // same layout as ParamsG
+        g->gtaps = (const T *)op->band_gtaps;
+        std::memcpy(g->taps, taps.data(), block_rows * band::REC * sizeof(T));
     }
     return TCA_OK;
 }
@@ -252,6 +275,21 @@ tca_status make_tmap(const tca_operator *op, const void *ptr, int kind, CUtensor
         box[2] = 1;
     }
     cuuint32_t es[4] = {1, 1, 1, 1};
+    const int s3 = op->band_v2 ? 0 : (op->dtype == TCA_F64 ? band::padded_s3_for<double>(n4) : band::padded_s3_for<float>(n4));
+    if (s3) {   // padded staging (Cfg::PADDED): 4-D (n4, n3, n2, slabs) with a fibre box of s3 > n4 (zero fill)
+        const auto dt = op->dtype == TCA_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        cuuint64_t d4[4] = {(cuuint64_t)n4, (cuuint64_t)op->n[2], (cuuint64_t)op->n[1], (cuuint64_t)slabs};
+        cuuint64_t s4[3] = {(cuuint64_t)n4 * op->esize, (cuuint64_t)(op->n[2] * n4) * op->esize,
+                            (cuuint64_t)(op->n[1] * op->n[2] * n4) * op->esize};
+        cuuint32_t b4[4] = {(cuuint32_t)s3, (cuuint32_t)(kind == 0 ? t3 + 6 : t3),
+                            (cuuint32_t)(kind == 0 ? band::PR : band::T2), 1};
+        CUresult r = encode(m, dt, 4, const_cast<void *>(ptr), d4, s4, b4, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return fail(TCA_ERR_CUDA, "cuTensorMapEncodeTiled (padded) failed (" + std::to_string((int)r) + ")");
+        return TCA_OK;
+    }
     if (op->band_v2) {   // tca_band2.cuh: slab box (UNIT, PP/UNIT, PR, 1) of a 4-D view; store box (T3 n4, T2, 1)
         const auto dt = op->dtype == TCA_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
         CUresult r;
@@ -375,9 +413,12 @@ tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_
         p->dbg = e ? atoi(e) : 0;
     }
     if (op->band_v2) {
-        if (op->band_gt) TCA_TRY(band2::launch_dispatch(op, *static_cast<band::ParamsG<T> *>(p), s, xm, ym));
+        if (op->band_gt == 2) TCA_TRY(band2::launch_dispatch(op, *static_cast<band::ParamsH<T> *>(p), s, xm, ym));
+        else if (op->band_gt == 1) TCA_TRY(band2::launch_dispatch(op, *static_cast<band::ParamsG<T> *>(p), s, xm, ym));
         else TCA_TRY(band2::launch_dispatch(op, *static_cast<band::Params<T> *>(p), s, xm, ym));
-    } else if (op->band_gt) {
+    } else if (op->band_gt == 2) {
+        TCA_TRY(band::launch_dispatch(op, *static_cast<band::ParamsH<T> *>(p), s, xm, ym));
+    } else if (op->band_gt == 1) {
         TCA_TRY(band::launch_dispatch(op, *static_cast<band::ParamsG<T> *>(p), s, xm, ym));
     } else {
         TCA_TRY(band::launch_dispatch(op, *static_cast<band::Params<T> *>(p), s, xm, ym));

@@ -43,6 +43,7 @@ namespace band2 {
 using band::Params;
 using band::ParamsBase;
 using band::ParamsG;
+using band::ParamsH;
 using band::tapG;
 using band::tapR;
 
@@ -178,12 +179,12 @@ __device__ __forceinline__ void mode4(const PA &a, const T *u3, const T *rb, con
     for (int k = ulo; k < uhi; ++k)
 #pragma unroll
         for (int e = e0; e < e1; ++e)
-            if (k < N4 && k - e >= -3 && k - e <= 3) s[e - e0] = fma(tapG(a, 0, e, k - e), uw[k], s[e - e0]);
+            if (k < N4 && k - e >= -3 && k - e <= 3) s[e - e0] = fma(tapG<4>(a, 0, e, k - e), uw[k], s[e - e0]);
 #pragma unroll
     for (int k = plo; k < phi; ++k)
 #pragma unroll
         for (int e = e0; e < e1; ++e)
-            if (k < N4 && k - e >= -2 && k - e <= 2) q[e - e0] = fma(tapR(a, 0, e, k - e), pw[k], q[e - e0]);
+            if (k < N4 && k - e >= -2 && k - e <= 2) q[e - e0] = fma(tapR<4>(a, 0, e, k - e), pw[k], q[e - e0]);
 #pragma unroll
     for (int e = 0; e < 4; ++e) pc[e] = (e0 + e < N4) ? pw[e0 + e] : T(0);
 #pragma unroll
@@ -252,11 +253,11 @@ band2_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict_
 #pragma unroll
             for (int rr = 0; rr < 2; ++rr) {
 #pragma unroll
-                for (int k = -3; k <= 3; ++k) gt[rr][k + 3] = tapG(a, a.off2, a2 + R0 + rr, k);
-                rt[rr][0] = tapR(a, a.off2, a2 + R0 + rr, -2);
-                rt[rr][1] = tapR(a, a.off2, a2 + R0 + rr, -1);
-                rt[rr][2] = tapR(a, a.off2, a2 + R0 + rr, 1);
-                rt[rr][3] = tapR(a, a.off2, a2 + R0 + rr, 2);
+                for (int k = -3; k <= 3; ++k) gt[rr][k + 3] = tapG<2>(a, a.off2, a2 + R0 + rr, k);
+                rt[rr][0] = tapR<2>(a, a.off2, a2 + R0 + rr, -2);
+                rt[rr][1] = tapR<2>(a, a.off2, a2 + R0 + rr, -1);
+                rt[rr][2] = tapR<2>(a, a.off2, a2 + R0 + rr, 1);
+                rt[rr][3] = tapR<2>(a, a.off2, a2 + R0 + rr, 2);
             }
             const int ca = (a3 - 3) * N4;                // flat column of staged column 0
             const int delta = ((ca % UNIT) + UNIT) % UNIT;
@@ -366,13 +367,13 @@ band2_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict_
             for (int ol = 0; ol < 2; ++ol) {
                 const int i3 = a3 + 2 * op + ol;
 #pragma unroll
-                for (int k = -3; k <= 3; ++k) gt[ol][k + 3] = tapG(a, a.off3, i3, k);
-                rt[ol][0] = tapR(a, a.off3, i3, -2);
-                rt[ol][1] = tapR(a, a.off3, i3, -1);
-                rt[ol][2] = tapR(a, a.off3, i3, 1);
-                rt[ol][3] = tapR(a, a.off3, i3, 2);
+                for (int k = -3; k <= 3; ++k) gt[ol][k + 3] = tapG<3>(a, a.off3, i3, k);
+                rt[ol][0] = tapR<3>(a, a.off3, i3, -2);
+                rt[ol][1] = tapR<3>(a, a.off3, i3, -1);
+                rt[ol][2] = tapR<3>(a, a.off3, i3, 1);
+                rt[ol][3] = tapR<3>(a, a.off3, i3, 2);
 #pragma unroll
-                for (int rr = 0; rr < 2; ++rr) cen[rr][ol] = tapR(a, a.off2, a2 + 2 * rh + rr, 0) + tapR(a, a.off3, i3, 0);
+                for (int rr = 0; rr < 2; ++rr) cen[rr][ol] = tapR<2>(a, a.off2, a2 + 2 * rh + rr, 0) + tapR<3>(a, a.off3, i3, 0);
             }
             const int jb = max(o0 - 3, -a.xoff), je = min(o1 + 3, a.nin - a.xoff);
             for (int j = o0 - 3; j < o1 + 3; ++j, ++g) {
@@ -463,9 +464,9 @@ band2_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict_
             auto taps1 = [&](int jj) {
                 const int b1 = __shfl_sync(0xffffffffu, a.off1 + jj, 0);
 #pragma unroll
-                for (int k = -3; k <= 3; ++k) g1n[k + 3] = tapG(a, 0, b1 + k, -k);
+                for (int k = -3; k <= 3; ++k) g1n[k + 3] = tapG<1>(a, 0, b1 + k, -k);
 #pragma unroll
-                for (int k = -2; k <= 2; ++k) r1n[k + 2] = tapR(a, 0, b1 + k, -k);
+                for (int k = -2; k <= 2; ++k) r1n[k + 2] = tapR<1>(a, 0, b1 + k, -k);
             };
             taps1(o0 - 3);
             for (int j = o0 - 3; j < o1 + 3; ++j, ++g) {

@@ -7,6 +7,8 @@ template tca_status launch_dispatch<band::Params<float>>(const tca_operator *, c
                                                         const CUtensorMap *, const CUtensorMap *);
 template tca_status launch_dispatch<band::ParamsG<float>>(const tca_operator *, const band::ParamsG<float> &, cudaStream_t,
                                                          const CUtensorMap *, const CUtensorMap *);
+template tca_status launch_dispatch<band::ParamsH<float>>(const tca_operator *, const band::ParamsH<float> &, cudaStream_t,
+                                                         const CUtensorMap *, const CUtensorMap *);
 template int pp_for<float>(int);
 }  // namespace band2
 }  // namespace tca

@@ -7,6 +7,8 @@ template tca_status launch_dispatch<band::Params<double>>(const tca_operator *, 
                                                         const CUtensorMap *, const CUtensorMap *);
 template tca_status launch_dispatch<band::ParamsG<double>>(const tca_operator *, const band::ParamsG<double> &, cudaStream_t,
                                                          const CUtensorMap *, const CUtensorMap *);
+template tca_status launch_dispatch<band::ParamsH<double>>(const tca_operator *, const band::ParamsH<double> &, cudaStream_t,
+                                                         const CUtensorMap *, const CUtensorMap *);
 template int pp_for<double>(int);
 }  // namespace band2
 }  // namespace tca

@@ -13,5 +13,6 @@ template int onebox_for<float>(int);
 template int minb_for<float>(int);
 template int unit_for<float>(int);
 template int pitched_for<float>(int);
+template int padded_s3_for<float>(int);
 }  // namespace band
 }  // namespace tca

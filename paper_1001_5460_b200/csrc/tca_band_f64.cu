@@ -13,5 +13,6 @@ template int onebox_for<double>(int);
 template int minb_for<double>(int);
 template int unit_for<double>(int);
 template int pitched_for<double>(int);
+template int padded_s3_for<double>(int);
 }  // namespace band
 }  // namespace tca

@@ -90,13 +90,23 @@ struct Params : ParamsBase<T> {
     using value_type = T;
     T taps[TAP_BYTES / sizeof(T)];
 };
-// tables too large for the parameter block (n_d ~ 256): the same records in
-// global memory, read through the read-only path (register operands)
-template <typename T>
-struct ParamsG : ParamsBase<T> {
+// tables too large for the parameter block (n_d ~ 256): the whole table in
+// global memory, read through the read-only path (register operands), and the
+// records of its first NBM modes (mode 4; with NBM = 2 also mode 3) in the block
+// as well, so that the mode-4 taps stay compile-time constant-bank operands and
+// mode 3's (pass B) uniform-register ones (config 4: pass C + ring 10.4 -> ... ms,
+// DESIGN.md 6.1)
+template <typename T, int NBM>
+struct ParamsGT : ParamsBase<T> {
     using value_type = T;
+    static constexpr int block_modes = NBM;
     const T *gtaps;
+    T taps[TAP_BYTES / sizeof(T)];
 };
+template <typename T>
+using ParamsG = ParamsGT<T, 1>;   // mode 4 in the block, modes 1-3 global
+template <typename T>
+using ParamsH = ParamsGT<T, 2>;   // modes 4 and 3 in the block, modes 1-2 global
 
 // Fused CG step B1': the apply kernel also
 // forms its own input, P_new = D + beta P_old (D = R, or Z in PCG), applies the
@@ -115,11 +125,18 @@ struct Cfg {
     static constexpr int E = (N4 + NSEG - 1) / NSEG; // elements per segment (<= 4: ring 24 doubles)
     static constexpr int NTHR = N4 > 16 ? 512 : 256;
     static constexpr int MINB = NTHR == 512 ? 1 : 2;  // CTAs per SM
-    static constexpr bool RING_SHIFT = NTHR == 256;   // mode-1 ring form (see ring_step)
+    static constexpr bool RING_SHIFT = true;          // mode-1 ring form (see ring_step; the rotating form is kept for reference)
     static constexpr int T3 = NTHR / (T2 * NSEG);    // mode-3 columns per tile
     static_assert(NTHR % (T2 * NSEG) == 0, "unsupported n4");
-    static constexpr int W = (T3 + 6) * N4;          // halo-extended flat columns
-    static constexpr int WI = T3 * N4;               // interior flat columns
+    // PADDED: when the mode-4 fibre is a multiple of 32 B (n4 = 4, 8, 16, 32 fp64),
+    // the T3 fibres a pass-C warp reads at stride n4 fall on the same banks
+    // (config 4, n4 = 32: 8x the ideal wavefronts); the slab is then staged by a
+    // 4-D TMA box (S3, T3 + 6, PR, 1) whose fibre extent S3 = n4 + 16 B overruns
+    // the tensor (zero fill), so every shared buffer has fibre pitch S3
+    static constexpr bool PADDED = (N4 * (int)sizeof(T)) % 32 == 0;
+    static constexpr int S3 = PADDED ? N4 + 16 / (int)sizeof(T) : N4;   // i3 pitch in shared memory
+    static constexpr int W = (T3 + 6) * S3;          // halo-extended flat columns
+    static constexpr int WI = T3 * S3;               // interior flat columns
     static constexpr int VEC = 16 / (int)sizeof(T);  // TMA coordinate granularity (16 B)
     // two-CTA tiles (PITCHED): the slab box uses 8-element chunks (64 B fp64,
     // 32 B fp32) and a row pitch picked against the pass-B/C bank patterns
@@ -132,7 +149,7 @@ struct Cfg {
     // (host picks it when n3 n4 % UNIT == 0; otherwise NB boxes per row for
     // fp64, 16-B chunks for PITCHED fp32)
     static constexpr bool ONEBOX = true;
-    static constexpr int NEED = W + UNIT - 1;
+    static constexpr int NEED = PADDED ? W : W + UNIT - 1;
     static constexpr int boxw_for_nb(int nb) { return ((NEED + nb - 1) / nb + UNIT - 1) / UNIT * UNIT; }
     static constexpr int pick_nb()
     {
@@ -171,7 +188,7 @@ struct Cfg {
         for (int l = 0; l < 32; ++l) {
             if (pass == 0 && l >= RPW * N4) continue;
             const int idx = pass == 0 ? (l / N4) * X + l % N4        // pass B
-                                      : (l / T3) * X + (l % T3) * N4;  // pass C
+                                      : (l / T3) * X + (l % T3) * S3;  // pass C
             for (int h = 0; h < (int)sizeof(T) / 4; ++h) ++cnt[(idx * ((int)sizeof(T) / 4) + h) % 32];
         }
         for (int b = 0; b < 32; ++b) worst = cnt[b] > worst ? cnt[b] : worst;
@@ -189,6 +206,7 @@ struct Cfg {
     static constexpr int WIP = pick_wip();
     static constexpr int pick_pp()
     {
+        if (PADDED) return W;   // the 4-D box lands densely: [PR][T3 + 6][S3]
         if (!PITCHED) return PP_BOXES;
         const int p0 = (NEED + UNIT - 1) / UNIT * UNIT;
         int best = p0, bc = 1 << 30;
@@ -215,11 +233,13 @@ struct Cfg {
     static constexpr size_t rest_fu = U2E + 2 * WIE + XBE;
     static constexpr int NSTAGE_FU = ((5 * stage_elems + rest_fu) * sizeof(T) + 256 <= SMEM_CAP) ? 3 : 2;
     static constexpr size_t smem_fu = ((2 * NSTAGE_FU - 1) * stage_elems + rest_fu) * sizeof(T) + 128;
-    static constexpr bool FU_OK = smem_fu <= SMEM_CAP;
+    static constexpr bool FU_OK = !PADDED && smem_fu <= SMEM_CAP;
     static_assert(T3 % BL == 0, "T3");
     static_assert(NBLK * WPB <= NTHR / 32, "pass B: one item per warp");
-    static_assert(WI <= 256, "store box");
-    static_assert(PITCHED || ((PR * PP * sizeof(T)) % 128 == 0 && (BOXW * sizeof(T)) % 128 == 0), "TMA alignment");
+    static_assert(PADDED || WI <= 256, "store box");
+    static_assert(!PADDED || (S3 <= 256 && (S3 * sizeof(T)) % 16 == 0), "padded box");
+    static_assert(PADDED || PITCHED || ((PR * PP * sizeof(T)) % 128 == 0 && (BOXW * sizeof(T)) % 128 == 0),
+                  "TMA alignment");
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -268,6 +288,13 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, const void *src, int c0, int c1, int c2, int c3)
+{
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void *src, int c0, int c1, int c2)
 {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];\n" ::"l"(map),
@@ -292,26 +319,30 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // ---------------------------------------------------------------- taps
 // rec(r) = taps + (off + r + PADR) * REC; G(r, k) = G[r, r+k], R(r, k) = lambda R[r, r+k]
 // (symmetric: G[r, r-k] = G[r-k, r]).  Tables are zero outside the domain rows.
-template <typename T>
+// M: the mode the table belongs to (selects block or global records for ParamsGT)
+template <int M, typename T>
 __device__ __forceinline__ T tapG(const Params<T> &a, int off, int r, int k)
 {
     return k >= 0 ? a.taps[(off + r + PADR) * REC + k] : a.taps[(off + r + k + PADR) * REC - k];
 }
-template <typename T>
+template <int M, typename T>
 __device__ __forceinline__ T tapR(const Params<T> &a, int off, int r, int k)
 {
     return k >= 0 ? a.taps[(off + r + PADR) * REC + 4 + k] : a.taps[(off + r + k + PADR) * REC + 4 - k];
 }
-template <typename T>
-__device__ __forceinline__ T tapG(const ParamsG<T> &a, int off, int r, int k)
+template <int M, typename T, int NBM>
+__device__ __forceinline__ T tapG(const ParamsGT<T, NBM> &a, int off, int r, int k)
 {
-    return k >= 0 ? __ldg(a.gtaps + (off + r + PADR) * REC + k) : __ldg(a.gtaps + (off + r + k + PADR) * REC - k);
+    const int i = k >= 0 ? (off + r + PADR) * REC + k : (off + r + k + PADR) * REC - k;
+    if constexpr (M == 4 || (M == 3 && NBM >= 2)) return a.taps[i];
+    else return __ldg(a.gtaps + i);
 }
-template <typename T>
-__device__ __forceinline__ T tapR(const ParamsG<T> &a, int off, int r, int k)
+template <int M, typename T, int NBM>
+__device__ __forceinline__ T tapR(const ParamsGT<T, NBM> &a, int off, int r, int k)
 {
-    return k >= 0 ? __ldg(a.gtaps + (off + r + PADR) * REC + 4 + k)
-                  : __ldg(a.gtaps + (off + r + k + PADR) * REC + 4 - k);
+    const int i = k >= 0 ? (off + r + PADR) * REC + 4 + k : (off + r + k + PADR) * REC + 4 - k;
+    if constexpr (M == 4 || (M == 3 && NBM >= 2)) return a.taps[i];
+    else return __ldg(a.gtaps + i);
 }
 
 // ---------------------------------------------------------------- pass C + ring (per segment)
@@ -454,16 +485,16 @@ __device__ __forceinline__ void pass_c(const PA &a, T (&acc)[6][Cfg<T, N4>::E], 
     T g1[7], r1[5];
     const int b1 = __shfl_sync(0xffffffffu, a.off1 + j, 0);   // uniform table row base (LDCU, UR operands)
 #pragma unroll
-    for (int o = -3; o <= 3; ++o) g1[o + 3] = tapG(a, 0, b1 + o, -o);
+    for (int o = -3; o <= 3; ++o) g1[o + 3] = tapG<1>(a, 0, b1 + o, -o);
 #pragma unroll
-    for (int o = -2; o <= 2; ++o) r1[o + 2] = tapR(a, 0, b1 + o, -o);
+    for (int o = -2; o <= 2; ++o) r1[o + 2] = tapR<1>(a, 0, b1 + o, -o);
     T s[E], q[E], pc[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) { s[e] = T(0); q[e] = T(0); pc[e] = T(0); }
     if (live) {
-        const T *u3 = U3 + i2 * C::WIP + i3 * N4;
-        const T *rb = RB + i2 * C::WIP + i3 * N4;
-        const T *pp = P + (i2 + 3) * C::PP + (i3 + 3) * N4;
+        const T *u3 = U3 + i2 * C::WIP + i3 * C::S3;
+        const T *rb = RB + i2 * C::WIP + i3 * C::S3;
+        const T *pp = P + (i2 + 3) * C::PP + (i3 + 3) * C::S3;
         T uw[uhi - ulo], pw[phi - plo];
 #pragma unroll
         for (int k = ulo; k < uhi; ++k) uw[k - ulo] = u3[k];
@@ -476,13 +507,13 @@ __device__ __forceinline__ void pass_c(const PA &a, T (&acc)[6][Cfg<T, N4>::E], 
         for (int k = ulo; k < uhi; ++k)
 #pragma unroll
             for (int e = e0; e < e1; ++e)
-                if (k - e >= -3 && k - e <= 3) s[e - e0] = fma(tapG(a, 0, e, k - e), uw[k - ulo], s[e - e0]);
+                if (k - e >= -3 && k - e <= 3) s[e - e0] = fma(tapG<4>(a, 0, e, k - e), uw[k - ulo], s[e - e0]);
         // lambda R4 p
 #pragma unroll
         for (int k = plo; k < phi; ++k)
 #pragma unroll
             for (int e = e0; e < e1; ++e)
-                if (k - e >= -2 && k - e <= 2) q[e - e0] = fma(tapR(a, 0, e, k - e), pw[k - plo], q[e - e0]);
+                if (k - e >= -2 && k - e <= 2) q[e - e0] = fma(tapR<4>(a, 0, e, k - e), pw[k - plo], q[e - e0]);
 #pragma unroll
         for (int e = 0; e < NE; ++e) pc[e] = pw[e0 + e - plo];
     }
@@ -492,7 +523,7 @@ __device__ __forceinline__ void pass_c(const PA &a, T (&acc)[6][Cfg<T, N4>::E], 
         out = OUT + qoff + e0;
         st = emit && qoff >= 0;
     } else {
-        out = OUT + (pos / C::T3) * C::WI + (pos % C::T3) * N4 + e0;
+        out = OUT + (pos / C::T3) * C::WI + (pos % C::T3) * C::S3 + e0;
     }
     T ov[E];
     const bool dot = a.pq_part != nullptr && j >= o0 && j < o1;   // input slab j is one of this CTA's
@@ -545,32 +576,32 @@ __device__ __forceinline__ void pass_b(const PA &a, const T *U2, const T *RA, co
         const int i2 = (warp % C::WPB) * C::RPW + lane / N4, i4 = lane % N4;
         if (i2 >= T2) return;
         constexpr int h0 = B * C::BL;
-        const T *u2 = U2 + i2 * C::WP + h0 * N4 + i4;
-        const T *pp = P + (i2 + 3) * C::PP + (h0 + 1) * N4 + i4;
-        const int ob = i2 * C::WIP + h0 * N4 + i4;
+        const T *u2 = U2 + i2 * C::WP + h0 * C::S3 + i4;
+        const T *pp = P + (i2 + 3) * C::PP + (h0 + 1) * C::S3 + i4;
+        const int ob = i2 * C::WIP + h0 * C::S3 + i4;
         T v[C::BL + 6], w[C::BL + 4], u[C::BL], rr[C::BL];
 #pragma unroll
-        for (int m = 0; m < C::BL + 6; ++m) v[m] = u2[m * N4];
+        for (int m = 0; m < C::BL + 6; ++m) v[m] = u2[m * C::S3];
 #pragma unroll
-        for (int m = 0; m < C::BL + 4; ++m) w[m] = pp[m * N4];
+        for (int m = 0; m < C::BL + 4; ++m) w[m] = pp[m * C::S3];
 #pragma unroll
-        for (int o = 0; o < C::BL; ++o) { u[o] = T(0); rr[o] = RA[ob + o * N4]; }
+        for (int o = 0; o < C::BL; ++o) { u[o] = T(0); rr[o] = RA[ob + o * C::S3]; }
         // pull form, one output row at a time: the row's 12 taps can be loaded
         // (uniform) ahead of its 12 DFMAs; same summation order as the push form
         // taps of row o+1 are fetched while row o computes (hand pipelining:
         // the scheduler otherwise issues each LDCU right before its DFMA)
         T tg[2][7], tr[2][5];
 #pragma unroll
-        for (int k = -3; k <= 3; ++k) tg[0][k + 3] = tapG(a, 0, r3, k);
+        for (int k = -3; k <= 3; ++k) tg[0][k + 3] = tapG<3>(a, 0, r3, k);
 #pragma unroll
-        for (int k = -2; k <= 2; ++k) tr[0][k + 2] = tapR(a, 0, r3, k);
+        for (int k = -2; k <= 2; ++k) tr[0][k + 2] = tapR<3>(a, 0, r3, k);
 #pragma unroll
         for (int o = 0; o < C::BL; ++o) {
             if (o + 1 < C::BL) {
 #pragma unroll
-                for (int k = -3; k <= 3; ++k) tg[(o + 1) & 1][k + 3] = tapG(a, 0, r3 + o + 1, k);
+                for (int k = -3; k <= 3; ++k) tg[(o + 1) & 1][k + 3] = tapG<3>(a, 0, r3 + o + 1, k);
 #pragma unroll
-                for (int k = -2; k <= 2; ++k) tr[(o + 1) & 1][k + 2] = tapR(a, 0, r3 + o + 1, k);
+                for (int k = -2; k <= 2; ++k) tr[(o + 1) & 1][k + 2] = tapR<3>(a, 0, r3 + o + 1, k);
             }
 #pragma unroll
             for (int k = -3; k <= 3; ++k) u[o] = fma(tg[o & 1][k + 3], v[o + 3 + k], u[o]);
@@ -579,8 +610,8 @@ __device__ __forceinline__ void pass_b(const PA &a, const T *U2, const T *RA, co
         }
 #pragma unroll
         for (int o = 0; o < C::BL; ++o) {
-            U3[ob + o * N4] = u[o];
-            RB[ob + o * N4] = rr[o];
+            U3[ob + o * C::S3] = u[o];
+            RB[ob + o * C::S3] = rr[o];
         }
     }
 }
@@ -707,6 +738,10 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                 cchunk = (ca - delta) / C::VEC;
             }
         }
+        if constexpr (C::PADDED) {   // 4-D box (fibre, i3, i2, slab): staged column 0 is i3 = a3 - 3
+            delta = 0;
+            cchunk = a3 - 3;
+        }
         const int j0 = o0 - 3, j1 = o1 + 3;
         const int jb = j0 > -a.xoff ? j0 : -a.xoff, je = j1 < a.nin - a.xoff ? j1 : a.nin - a.xoff;
 #pragma unroll
@@ -731,7 +766,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                 ++gi;
                 return;
             }
-            if (onebox) {
+            if (onebox || C::PADDED) {
                 if (tid == 0) {
                     mbar_arrive_expect_tx(bar + st, (unsigned)(PR * PP * sizeof(T)));
                     tma_load_4d(dst, xmp, bar + st, 0, cchunk, a2 - 3, js + a.xoff);
@@ -788,12 +823,12 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     {   // taps of row r+1 fetched while row r computes (see pass B)
                         T tg[2][7];
 #pragma unroll
-                        for (int k = -3; k <= 3; ++k) tg[0][k + 3] = tapG(a, 0, b2, k);
+                        for (int k = -3; k <= 3; ++k) tg[0][k + 3] = tapG<2>(a, 0, b2, k);
 #pragma unroll
                         for (int r = 0; r < T2; ++r) {
                             if (r + 1 < T2) {
 #pragma unroll
-                                for (int k = -3; k <= 3; ++k) tg[(r + 1) & 1][k + 3] = tapG(a, 0, b2 + r + 1, k);
+                                for (int k = -3; k <= 3; ++k) tg[(r + 1) & 1][k + 3] = tapG<2>(a, 0, b2 + r + 1, k);
                             }
 #pragma unroll
                             for (int k = -3; k <= 3; ++k) u[r] = fma(tg[r & 1][k + 3], v[r + 3 + k], u[r]);
@@ -801,18 +836,18 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     }
 #pragma unroll
                     for (int r = 0; r < T2; ++r) U2[r * C::WP + c] = u[r];
-                    const int ci = c - 3 * N4;
+                    const int ci = c - 3 * C::S3;
                     if (ci >= 0 && ci < WI) {
 #pragma unroll
                         for (int r = 0; r < T2; ++r) u[r] = T(0);
                         T tr[2][5];
 #pragma unroll
-                        for (int k = -2; k <= 2; ++k) tr[0][k + 2] = tapR(a, 0, b2, k);
+                        for (int k = -2; k <= 2; ++k) tr[0][k + 2] = tapR<2>(a, 0, b2, k);
 #pragma unroll
                         for (int r = 0; r < T2; ++r) {
                             if (r + 1 < T2) {
 #pragma unroll
-                                for (int k = -2; k <= 2; ++k) tr[(r + 1) & 1][k + 2] = tapR(a, 0, b2 + r + 1, k);
+                                for (int k = -2; k <= 2; ++k) tr[(r + 1) & 1][k + 2] = tapR<2>(a, 0, b2 + r + 1, k);
                             }
 #pragma unroll
                             for (int k = -2; k <= 2; ++k) u[r] = fma(tr[r & 1][k + 2], v[r + 3 + k], u[r]);
@@ -841,7 +876,8 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             if (pending >= 0) {   // uniform: every thread tracks the same pending slab
                 if (tid == 0 && !(dbg & (1 | 256))) {
                     // staging buffer of output slab `pending` (written in pass C of slab pending+3)
-                    tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
+                    if constexpr (C::PADDED) tma_store_4d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, 0, a3, a2, pending);
+                    else tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                     bulk_commit();
                     bulk_wait_read<1>();
                 }
@@ -879,7 +915,8 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         __syncthreads();
         if (!FU && pending >= 0) {
             if (tid == 0 && !(dbg & (1 | 256))) {
-                tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
+                if constexpr (C::PADDED) tma_store_4d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, 0, a3, a2, pending);
+                else tma_store_3d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, a3 * N4, a2, pending);
                 bulk_commit();
             }
             pending = -1;
@@ -1002,6 +1039,18 @@ int boxw_for(int n4)
     switch (n4) {
 #define TCA_CASE(n) \
     case n: return Cfg<T, n>::BOXW;
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return 0;
+}
+
+template <typename T>
+int padded_s3_for(int n4)   // fibre pitch of the padded 4-D staging, 0 when the layout is flat
+{
+    switch (n4) {
+#define TCA_CASE(n) \
+    case n: return Cfg<T, n>::PADDED ? Cfg<T, n>::S3 : 0;
         TCA_BAND_N4_LIST(TCA_CASE)
 #undef TCA_CASE
     }

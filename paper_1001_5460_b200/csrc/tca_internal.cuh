@@ -145,7 +145,7 @@ struct tca_operator {
     std::vector<double> bandG[tca::kD];
     std::vector<double> bandR[tca::kD];
     std::vector<unsigned char> band_params;   // prebuilt kernel-parameter block (tap tables)
-    bool band_gt = false;                     // tap tables in global memory (band_gtaps), not the block
+    int band_gt = 0;                          // tap tables: 0 block; global (band_gtaps) with modes 4 (1) or 4+3 (2) in the block
     void *band_gtaps = nullptr;
     size_t band_gtaps_bytes = 0;
     // dense host G_d, R_d (fp64; R_d empty without a regulariser) for the PCG factors

@@ -47,9 +47,13 @@ def solve(op, b, dt, b1, how="cg", **kw):
 
 
 def expect_b1(n, dt):
-    """B1' needs the parameter-block tap tables and its shared-memory plan (fp64
-    n4 = 16 and 32 do not fit: unfused)."""
-    return not (dt == "f64" and len(n) == 4 and n[3] in (16, 32))
+    """B1' needs the parameter-block tap tables and the unpadded staging layout:
+    a mode-4 fibre that is a multiple of 32 B (fp64 n4 = 4, 8, 16, 32; fp32 n4 =
+    8, 16, 32) is staged with a padded fibre pitch (Cfg::PADDED, DESIGN.md 6.1),
+    which B1' does not take (unfused)."""
+    n4 = n[3] if len(n) == 4 else 1
+    es = 8 if dt == "f64" else 4
+    return (n4 * es) % 32 != 0
 
 
 # fused-path shapes: ragged mode-2/3 tiles (clipped stores), every n4 class, a
