@@ -820,18 +820,17 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     T u[T2];
 #pragma unroll
                     for (int r = 0; r < T2; ++r) u[r] = T(0);
-                    {   // taps of row r+1 fetched while row r computes (see pass B)
-                        T tg[2][7];
+                    // symmetric band (G[r, r+k] = G[r+k, r]): each stored record tap
+                    // G[r, r+k] (k > 0) serves output r (input row r+k) and output r+k
+                    // (input row r) -- 38 uniform tap loads for the 56 DFMAs of G2 on
+                    // 8 rows (the records of halo rows -3..-1 cover the top edge)
 #pragma unroll
-                        for (int k = -3; k <= 3; ++k) tg[0][k + 3] = tapG<2>(a, 0, b2, k);
+                    for (int r = -3; r < T2; ++r) {
 #pragma unroll
-                        for (int r = 0; r < T2; ++r) {
-                            if (r + 1 < T2) {
-#pragma unroll
-                                for (int k = -3; k <= 3; ++k) tg[(r + 1) & 1][k + 3] = tapG<2>(a, 0, b2 + r + 1, k);
-                            }
-#pragma unroll
-                            for (int k = -3; k <= 3; ++k) u[r] = fma(tg[r & 1][k + 3], v[r + 3 + k], u[r]);
+                        for (int k = (r < 0 ? -r : 0); k <= 3; ++k) {
+                            const T t = tapG<2>(a, 0, b2 + r, k);
+                            if (r >= 0) u[r] = fma(t, v[r + 3 + k], u[r]);
+                            if (k > 0 && r + k < T2) u[r + k] = fma(t, v[r + 3], u[r + k]);
                         }
                     }
 #pragma unroll
@@ -840,17 +839,14 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                     if (ci >= 0 && ci < WI) {
 #pragma unroll
                         for (int r = 0; r < T2; ++r) u[r] = T(0);
-                        T tr[2][5];
 #pragma unroll
-                        for (int k = -2; k <= 2; ++k) tr[0][k + 2] = tapR<2>(a, 0, b2, k);
+                        for (int r = -2; r < T2; ++r) {
 #pragma unroll
-                        for (int r = 0; r < T2; ++r) {
-                            if (r + 1 < T2) {
-#pragma unroll
-                                for (int k = -2; k <= 2; ++k) tr[(r + 1) & 1][k + 2] = tapR<2>(a, 0, b2 + r + 1, k);
+                            for (int k = (r < 0 ? -r : 0); k <= 2; ++k) {
+                                const T t = tapR<2>(a, 0, b2 + r, k);
+                                if (r >= 0) u[r] = fma(t, v[r + 3 + k], u[r]);
+                                if (k > 0 && r + k < T2) u[r + k] = fma(t, v[r + 3], u[r + k]);
                             }
-#pragma unroll
-                            for (int k = -2; k <= 2; ++k) u[r] = fma(tr[r & 1][k + 2], v[r + 3 + k], u[r]);
                         }
 #pragma unroll
                         for (int r = 0; r < T2; ++r) RA[r * C::WIP + ci] = u[r];
