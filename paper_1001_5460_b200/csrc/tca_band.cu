@@ -459,7 +459,7 @@ static bool v2_eligible(const tca_operator *op)
     static const char *e = getenv("TCA_BAND_V2");
     if (!(e && e[0] == '1')) return false;
     const int n4 = (int)op->n[3];
-    if (n4 != 15 && n4 != 16) return false;
+    if ((n4 != 15 && n4 != 16) || op->dtype != TCA_F64) return false;
     return (op->n[2] * op->n[3]) % band2::UNIT == 0;
 }
 
