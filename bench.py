@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--samples", type=int, default=None, help="scattered workload: sample count (default 9e6)")
     ap.add_argument("--cfg4-iters", type=int, default=20,
                     help="CG iterations of the config-4 scaling measurement added to the line (0: skip)")
+    ap.add_argument("--small-iters", type=int, default=200,
+                    help="CG iterations of the config-0/1 latency measurement added to the line (0: skip)")
     return ap.parse_args()
 
 
@@ -420,6 +422,27 @@ def run_tca(args):
         op4.close()
         torch.cuda.empty_cache()
 
+    # ---- configs 0 and 1 (small systems: launch-latency bound): us per CG
+    # iteration of a fixed-iteration solve from x0 = 0, rank 0 only, outside the
+    # timed region (config 0 runs the single-block engine of tca_tiny.cu).
+    small = None
+    if args.small_iters > 0 and rank == 0 and args.workload == "fit":
+        small = {}
+        for ci in (0, 1):
+            cs = synth.CONFIGS[ci]
+            As, Ls = synth.mode_matrices(cs)
+            ops = tca.Operator(As, Ls, cs.lam, dtype="f64")
+            bs = ops.rhs(torch.from_numpy(synth.data(As, cs.n, cs.m, seed=1)).cuda())
+            ops.cg_solve(bs, rtol=0.0, max_iters=min(10, args.small_iters))   # warm-up (graph capture)
+            best = None
+            for _ in range(3):
+                _, reps_s = ops.cg_solve(bs, rtol=0.0, max_iters=args.small_iters)
+                us = reps_s["seconds"] * 1e6 / max(1, reps_s["iterations"])
+                best = us if best is None else min(best, us)
+            small[f"config{ci}"] = {"n": list(cs.n), "iterations": args.small_iters, "cg_us_per_iteration": best,
+                                    "engine": "single-block (tca_tiny.cu)" if ops.tiny_engine else "general"}
+            ops.close()
+
     e2e = None
     if not args.no_e2e and args.solver == "cg":   # (tca_solve_host runs plain CG)
         yh = torch.empty(local_m, dtype=tdt, pin_memory=True)
@@ -481,6 +504,7 @@ def run_tca(args):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "scaling_config4": scale4,
+        "small_configs": small,
         "gpu_launches": int(launches),
         "clocks": clk,
         "time_to_solution_ms": total_ms / args.steps,

@@ -206,6 +206,18 @@ tca_status tca_operator_create_scattered(tca_operator **op, int order,
  * (no CG solve so far) or op NULL.  Results are the same iterates either way. */
 int tca_operator_cg_fused_step(const tca_operator *op);
 
+/* Which engine tca_cg_solve uses on this operator: 1 = single-block engine
+ * (tca_tiny.cu: the whole Fig. 2 solve, in ONE kernel launch
+ * by one 1024-thread block: p and two apply temporaries in shared memory, x,
+ * r, q in registers (shared memory above two elements per thread); chosen for
+ * fp64 N <= 4096, fp32 N <= 8192, n_d <= 4095, when the tap tables and vectors
+ * fit 224 KB of shared memory, single GPU, not scattered, not a Kronecker-sum-
+ * only operator;
+ * the environment switch TCA_TINY=0 disables it), 0 = general multi-kernel
+ * engine, -1 = op NULL.  Same iterates, stop rules, guards and report either
+ * way (readings Z1-Z3, Z10, Z12, Z28). */
+int tca_operator_cg_engine(const tca_operator *op);
+
 /* y = M x.  x, y: device tensors of the local shape (rows [own_lo, own_hi)
  * of mode 1 on a sharded operator); x and y must not alias. */
 tca_status tca_apply(const tca_operator *op, const void *x, void *y,

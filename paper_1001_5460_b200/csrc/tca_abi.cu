@@ -212,6 +212,11 @@ static tca_status make_band(tca_dtype dt, const std::vector<double> &M, int rows
     out->cols = cols;
     out->W = W;
     out->dense = (W == cols);
+    out->reach_lo = out->reach_hi = 0;
+    for (int r = 0; r < rows; ++r) {
+        out->reach_lo = std::max(out->reach_lo, -start[r]);
+        out->reach_hi = std::max(out->reach_hi, start[r] + W - cols);
+    }
     for (int r = 0; r < rows && out->dense; ++r)
         if (start[r] != 0) out->dense = false;
     TCA_CUDA_TRY(dev_get((void **)&out->start, sizeof(int) * std::max(rows, 1)));
@@ -798,36 +803,13 @@ static tca_status jacobi_prepare(tca_operator *op, cudaStream_t s)
     return TCA_OK;
 }
 
+// Fig. 2 / PCG / single-reduction CG / tensor Jacobi from the start phase
+// through the last iteration on the general (multi-kernel, graph-captured) path.
 template <typename T>
-static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t max_iters,
-                       tca_cg_report *rep, cudaStream_t s, int pcg = 0, int x0_zero = 1)
+static tca_status cg_run(tca_operator *op, const T *b, T *x, double rtol, int32_t max_iters, CgScalars h,
+                         cudaStream_t s, int pcg, int x0_zero)
 {
-    double *part_bb = op->part + 2 * kRedBlocks;   // <b, b> partials (warm start, report)
-    CgScalars h{};
-    h.rtol2 = rtol > 0.0 ? rtol * rtol : 0.0;
-    h.max_iters = max_iters;
-    h.pcg = pcg == 1;
-    op->solver = pcg;
-    if (op->b1 < 0) {   // fused step B1' for Fig. 2 / PCG on one GPU: opt-in (TCA_B1=1), see DESIGN.md 6.5
-        const char *b1env = getenv("TCA_B1");
-        const bool want_b1 = b1env && b1env[0] == '1';
-        op->b1 = (want_b1 && fused_used(op, op->p_own, op->q) && fused_b1_supported(op)) ? 1 : 0;
-        if (op->b1 == 1) {
-            cudaError_t e = cudaMallocAsync(&op->p2, (size_t)op->N * op->esize, s);
-            if (e != cudaSuccess) { op->b1 = 0; cudaGetLastError(); }
-        }
-    }
-    const int b1_saved = op->b1;
-    if (pcg == 2 || pcg == 3) op->b1 = 0;   // single-reduction CG and Jacobi keep their own steps
-    op->pcur = 0;
-    if (op->b1 == 1) {
-        const void *ptrs[4] = {op->p_own, op->p2, pcg == 1 ? op->z : op->r, op->q};
-        const int kinds[4] = {0, 0, 0, 1};
-        TCA_TRY(fused_b1_prepare(op, ptrs, kinds, 4, s));
-    }
-    *op->sc_host = h;
-    TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
-    TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
+    double *part_bb = op->part + 2 * kRedBlocks;   // <b, b> partials (warm start)
     if (pcg == 3) {   // tensor Jacobi: U := 0, E := InvMainDiag(A), R := A*U - B
         h.thr = rtol;
         *op->sc_host = h;
@@ -890,6 +872,42 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     }
     if (op->b1 == 1)   // the last step's pending C := C + alpha P (x only: done is set)
         launch_cg_update_xp<T>(x, (T *)(op->pcur ? op->p2 : op->p_own), (const T *)op->r, op->N, op->sc, s);
+    return TCA_OK;
+}
+
+template <typename T>
+static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t max_iters,
+                       tca_cg_report *rep, cudaStream_t s, int pcg = 0, int x0_zero = 1)
+{
+    double *part_bb = op->part + 2 * kRedBlocks;   // <b, b> partials (warm start, report)
+    CgScalars h{};
+    h.rtol2 = rtol > 0.0 ? rtol * rtol : 0.0;
+    h.max_iters = max_iters;
+    h.pcg = pcg == 1;
+    op->solver = pcg;
+    const bool tiny = pcg == 0 && tiny_cg_eligible(op);
+    if (op->b1 < 0) {   // fused step B1' for Fig. 2 / PCG on one GPU: opt-in (TCA_B1=1), see DESIGN.md 6.5
+        const char *b1env = getenv("TCA_B1");
+        const bool want_b1 = b1env && b1env[0] == '1';
+        op->b1 = (want_b1 && fused_used(op, op->p_own, op->q) && fused_b1_supported(op)) ? 1 : 0;
+        if (op->b1 == 1) {
+            cudaError_t e = cudaMallocAsync(&op->p2, (size_t)op->N * op->esize, s);
+            if (e != cudaSuccess) { op->b1 = 0; cudaGetLastError(); }
+        }
+    }
+    const int b1_saved = op->b1;
+    if (pcg == 2 || pcg == 3 || tiny) op->b1 = 0;   // single-reduction CG, Jacobi, tiny: their own steps
+    op->pcur = 0;
+    if (op->b1 == 1) {
+        const void *ptrs[4] = {op->p_own, op->p2, pcg == 1 ? op->z : op->r, op->q};
+        const int kinds[4] = {0, 0, 0, 1};
+        TCA_TRY(fused_b1_prepare(op, ptrs, kinds, 4, s));
+    }
+    *op->sc_host = h;
+    TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
+    TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
+    if (tiny) TCA_TRY(launch_tiny_cg(op, b, x, x0_zero, s));   // whole solve in one block (tca_tiny.cu)
+    else TCA_TRY(cg_run<T>(op, b, x, rtol, max_iters, h, s, pcg, x0_zero));
     op->b1 = b1_saved;
     TCA_CUDA_TRY(cudaGetLastError());
     TCA_CUDA_TRY(cudaEventRecord(op->ev1, s));
@@ -1357,6 +1375,8 @@ tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo, int64_t *
 int tca_operator_apply_path(const tca_operator *op) { return op ? op->apply_path : -1; }
 
 int tca_operator_cg_fused_step(const tca_operator *op) { return op ? op->b1 : -1; }
+
+int tca_operator_cg_engine(const tca_operator *op) { return op ? (tiny_cg_eligible(op) ? 1 : 0) : -1; }
 
 tca_status tca_apply(const tca_operator *op, const void *x, void *y, void *stream)
 {

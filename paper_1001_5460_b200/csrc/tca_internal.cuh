@@ -47,6 +47,8 @@ struct BandMat {
     void *taps = nullptr;  // device, rows*W of the operator dtype
     size_t tap_bytes = 0;
     bool dense = false;    // W == cols and start == 0: taps is the dense row-major matrix
+    int reach_lo = 0;      // rows a band row reads before column 0 (max over rows of -start[r])
+    int reach_hi = 0;      // ... and past column cols - 1 (max of start[r] + W - cols); taps there are zero
 };
 
 // Device-resident CG scalars (always fp64, reading Z10).
@@ -322,6 +324,9 @@ uint64_t stream_key(uint64_t seed, uint32_t stream_id);
 // device, size): the attribute is per device, and the library may drive
 // several devices from several host threads (tca_abi.cu)
 tca_status set_max_dynamic_smem(const void *func, size_t bytes);
+// whole-solve single-block CG for small problems (tca_tiny.cu)
+bool tiny_cg_eligible(const tca_operator *op);
+tca_status launch_tiny_cg(const tca_operator *op, const void *b, void *x, int x0_zero, cudaStream_t s);
 
 // process-wide count of kernel launches issued by the library
 extern std::atomic<int64_t> g_launches;

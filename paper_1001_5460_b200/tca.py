@@ -29,7 +29,7 @@ EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
             "tca_cg_solve", "tca_solve_host", "tca_solve_host_batch", "tca_operator_destroy", "tca_generate_normal",
             "tca_forward_model", "tca_status_string", "tca_last_error", "tca_version",
             "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches",
-            "tca_operator_apply_path", "tca_operator_cg_fused_step", "tca_operator_create_scattered", "tca_shard_layout", "tca_nccl_get_unique_id",
+            "tca_operator_apply_path", "tca_operator_cg_engine", "tca_operator_cg_fused_step", "tca_operator_create_scattered", "tca_shard_layout", "tca_nccl_get_unique_id",
             "tca_nccl_comm_create", "tca_nccl_comm_destroy", "tca_local_group_create",
             "tca_local_group_destroy", "tca_pcg_solve", "tca_precond_apply", "tca_precond_info",
             "tca_cgsr_solve", "tca_operator_create_gram", "tca_jacobi_solve"]
@@ -100,6 +100,7 @@ _lib.tca_local_group_create.restype = ctypes.c_int
 _lib.tca_local_group_destroy.argtypes = [_vp]
 _lib.tca_local_group_destroy.restype = None
 _lib.tca_operator_apply_path.argtypes = [_vp]
+_lib.tca_operator_cg_engine.argtypes = [_vp]
 _lib.tca_operator_cg_fused_step.argtypes = [_vp]
 _lib.tca_operator_cg_fused_step.restype = ctypes.c_int
 _lib.tca_pcg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int32, _vp, _vp]
@@ -113,6 +114,7 @@ _lib.tca_operator_create_scattered.argtypes = [ctypes.POINTER(_vp), ctypes.c_int
                                                ctypes.POINTER(ctypes.c_double),
                                                _dpp, ctypes.c_double, ctypes.c_int, _vp]
 _lib.tca_operator_apply_path.restype = ctypes.c_int
+_lib.tca_operator_cg_engine.restype = ctypes.c_int
 for _name in ("tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
               "tca_cg_solve", "tca_solve_host", "tca_solve_host_batch", "tca_generate_normal", "tca_forward_model",
               "tca_operator_set_timing", "tca_operator_get_timing"):
@@ -296,6 +298,12 @@ class Operator:
         """'fused' (one-pass banded kernel), 'ksum' (Kronecker-sum stencil, factor-form
         operators without a product term) or 'multipass' (generic per-mode kernels)."""
         return {1: "fused", 2: "ksum"}.get(_lib.tca_operator_apply_path(self._h), "multipass")
+
+    @property
+    def tiny_engine(self):
+        """True when cg_solve runs the single-block engine (tca_tiny.cu: the whole
+        solve in one kernel launch, vectors in shared memory) on this operator."""
+        return _lib.tca_operator_cg_engine(self._h) == 1
 
     @property
     def cg_fused_step(self):
