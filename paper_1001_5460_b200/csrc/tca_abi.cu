@@ -217,6 +217,15 @@ static tca_status make_band(tca_dtype dt, const std::vector<double> &M, int rows
         out->reach_lo = std::max(out->reach_lo, -start[r]);
         out->reach_hi = std::max(out->reach_hi, start[r] + W - cols);
     }
+    out->win16 = 0;
+    for (int r0 = 0; r0 < rows; r0 += 16) {
+        int lo = start[r0], hi = start[r0];
+        for (int r = r0; r < std::min(rows, r0 + 16); ++r) {
+            lo = std::min(lo, start[r]);
+            hi = std::max(hi, start[r]);
+        }
+        out->win16 = std::max(out->win16, hi + W - lo);
+    }
     for (int r = 0; r < rows && out->dense; ++r)
         if (start[r] != 0) out->dense = false;
     TCA_CUDA_TRY(dev_get((void **)&out->start, sizeof(int) * std::max(rows, 1)));
@@ -362,10 +371,32 @@ static tca_status chain_products(const tca_operator *op, const T *in, T *out,
         TCA_CUDA_TRY(cudaMallocAsync((void **)&tmp[0], maxi * sizeof(T), s));
         if (order.size() > 2) TCA_CUDA_TRY(cudaMallocAsync((void **)&tmp[1], maxi * sizeof(T), s));
     }
+    // the last two products on the two fastest non-trivial modes (d, d+1): one
+    // plane pass (launch_band_plane2) when the plane fits shared memory
+    size_t nsep = order.size();
+    int pd = -1;
+    if (order.size() >= 2) {
+        const int a = order[order.size() - 2], c = order[order.size() - 1];
+        const int d = std::min(a, c);
+        bool trailing_unit = std::max(a, c) == d + 1;
+        for (int e = d + 2; e < kD && trailing_unit; ++e) trailing_unit = ext_in[e] == 1 && ext_out[e] == 1;
+        if (trailing_unit && !mats[d].dense && !mats[d + 1].dense) {
+            pd = d;
+            nsep -= 2;
+        }
+    }
     const T *cur = in;
     for (size_t i = 0; i < order.size(); ++i) {
         const int d = order[i];
         T *dst = (i + 1 == order.size()) ? out : tmp[i & 1];
+        if (i == nsep && pd >= 0) {
+            int64_t planes = 1;
+            for (int e = 0; e < pd; ++e) planes *= ext[e];
+            if (launch_band_plane2<T>(cur, out, planes, (int)ext[pd], (int)ext[pd + 1], mats[pd], mats[pd + 1], s)) {
+                cur = out;
+                break;
+            }
+        }
         mode_product<T>(cur, dst, outer_of(ext, d), mats[d], inner_of(ext, d), 1.0, false, nullptr, s);
         ext[d] = ext_out[d];
         cur = dst;

@@ -49,6 +49,7 @@ struct BandMat {
     bool dense = false;    // W == cols and start == 0: taps is the dense row-major matrix
     int reach_lo = 0;      // rows a band row reads before column 0 (max over rows of -start[r])
     int reach_hi = 0;      // ... and past column cols - 1 (max of start[r] + W - cols); taps there are zero
+    int win16 = 0;         // largest input window (max start + W - min start) of 16 consecutive rows
 };
 
 // Device-resident CG scalars (always fp64, reading Z10).
@@ -249,6 +250,12 @@ template <typename T>
 void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
                               int64_t inner, double alpha, bool accumulate,
                               const int32_t *done, cudaStream_t s);
+
+// the two fastest modes of an (planes, c3, c4) tensor in one pass (M3: rows r3 x
+// cols c3, M4: r4 x c4); false when the plane does not fit shared memory (nothing launched)
+template <typename T>
+bool launch_band_plane2(const T *X, T *Y, int64_t planes, int c3, int c4, const BandMat &M3, const BandMat &M4,
+                        cudaStream_t s);
 
 // dense fp64 mode product on the FP64 tensor cores (DMMA); M row-major rows x cols
 void launch_dense_mode_product_dmma(const double *X, double *Y, int64_t outer, int rows, int cols,

@@ -77,59 +77,287 @@ band_mode_product_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t out
     }
 }
 
-// Row-blocked form for wide fibres (inner >= 256): a block owns RB consecutive
-// output rows x 256 consecutive t and stages the union of their input-row
-// windows (<= KWIN rows) in shared memory once, so each input element is read
-// from memory ~window/RB times instead of W times (config 3's rhs mode 1:
-// 22 staged rows for 8 outputs rows vs 8 taps each).  Falls back to direct
-// loads for a group whose window exceeds KWIN.
-constexpr int kRB = 8, kKWIN = 24;
+// Window-staged form for fibres of >= 32 elements and rows of <= 16 taps: a
+// block of 128 threads owns kRB = 16 consecutive output rows x kCB = 128
+// consecutive (o, t) positions (flattened, t fastest: coalesced rows when
+// inner >= 128, inner-long segments otherwise).  It stages the union of the
+// rows' input windows (BandMat::win16 <= kKWIN rows; rows outside [0, cols)
+// zero-filled) in shared memory with asynchronous copies (LDGSTS, the whole
+// window in flight), so each input element is read ~window / 16 times instead
+// of W times (config 3's rhs modes 1 and 2: 38 staged rows for 16 output rows
+// of 8 taps).  Warp w then owns rows w, w + 4, w + 8, w + 12: their W taps sit
+// in registers and each output costs W shared loads + W FMAs.  Small blocks
+// (39 KB of window in fp64) keep several per SM so one block's loads overlap
+// another's arithmetic.
+constexpr int kRB = 16, kCB = 128, kKWIN = 48;
 
-template <typename T>
-__global__ void __launch_bounds__(256)
-band_mode_product_rows_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t outer, int rows, int cols,
-                              int64_t inner, const int *__restrict__ start, const T *__restrict__ taps, int W,
-                              T alpha, int accumulate, const int32_t *done)
+template <typename T, int WC>
+__global__ void __launch_bounds__(kCB)
+band_mode_product_win_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t total, int rows, int cols,
+                             int64_t inner, const int *__restrict__ start, const T *__restrict__ taps, T alpha,
+                             int accumulate, const int32_t *done)
 {
     if (done && *done) return;
-    __shared__ T sm[kKWIN * 256];
-    const int r0 = blockIdx.y * kRB;
+    extern __shared__ __align__(16) unsigned char win_raw[];
+    T *sm = reinterpret_cast<T *>(win_raw);
+    constexpr int NW = kCB / 32, RPW = kRB / NW;   // warps, rows per warp
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r0 = blockIdx.x * kRB;   // row groups fastest: neighbours share window rows in L2
     const int nr = min(kRB, rows - r0);
-    const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
-    int c0 = cols, c1 = 0;   // union of the group's windows, clipped to [0, cols)
-    for (int k = 0; k < nr; ++k) {
+    int base = __ldg(start + r0), top = base;
+    for (int k = 1; k < nr; ++k) {
         const int sr = __ldg(start + r0 + k);
-        c0 = min(c0, max(sr, 0));
-        c1 = max(c1, min(sr + W, cols));
+        base = min(base, sr);
+        top = max(top, sr);
     }
-    const bool staged = c1 - c0 <= kKWIN;
-    for (int64_t o = blockIdx.z; o < outer; o += gridDim.z) {
-        const T *xo = X + o * (int64_t)cols * inner;
-        T *yo = Y + o * (int64_t)rows * inner;
-        if (staged) {
-            __syncthreads();   // previous o's reads of sm are done
-            if (t < inner)
-                for (int c = c0; c < c1; ++c) sm[(c - c0) * 256 + threadIdx.x] = xo[(int64_t)c * inner + t];
+    top += WC;   // window rows [base, top), <= kKWIN (host-checked win16)
+    T tp[RPW][WC];
+    int off[RPW];
+#pragma unroll
+    for (int h = 0; h < RPW; ++h) {
+        const int k = warp + NW * h;
+        const bool ok = k < nr;
+        off[h] = ok ? __ldg(start + r0 + k) - base : 0;
+#pragma unroll
+        for (int w = 0; w < WC; ++w) tp[h][w] = ok ? __ldg(taps + (int64_t)(r0 + k) * WC + w) : T(0);
+    }
+    const bool aligned = inner % kCB == 0;   // a chunk never straddles two outer indices
+    const int cv0 = max(base, 0), cv1 = min(top, cols);
+    for (int64_t f0 = (int64_t)blockIdx.y * kCB; f0 < total; f0 += (int64_t)gridDim.y * kCB) {
+        const int64_t oc = aligned ? f0 / inner : 0;   // the chunk's outer index (aligned case)
+        {   // stage column f0 + tid of the window
+            const int64_t f = f0 + threadIdx.x;
+            const bool live = f < total;
+            int64_t o, t;
+            if (aligned) { o = oc; t = f - oc * inner; }
+            else { o = live ? f / inner : 0; t = live ? f - o * inner : 0; }
+            __syncthreads();   // previous chunk's reads of sm are done
+            T *row = sm + threadIdx.x;
+            for (int c = base; c < cv0; ++c) row[(c - base) * kCB] = T(0);           // rows before column 0
+            for (int c = max(cv1, base); c < top; ++c) row[(c - base) * kCB] = T(0); // rows past the last column
+            if (live) {
+                const T *src = X + o * (int64_t)cols * inner + t + (int64_t)cv0 * inner;
+                unsigned dst = (unsigned)__cvta_generic_to_shared(row + (cv0 - base) * kCB);
+                for (int c = cv0; c < cv1; ++c, src += inner, dst += kCB * sizeof(T)) {
+                    if (sizeof(T) == 8)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+                    else
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
+                }
+            } else {
+                for (int c = cv0; c < cv1; ++c) row[(c - base) * kCB] = T(0);
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
             __syncthreads();
         }
-        if (t >= inner) continue;
-        for (int k = 0; k < nr; ++k) {
-            const int r = r0 + k;
-            const int sr = __ldg(start + r);
-            const T *tp = taps + (int64_t)r * W;
-            T acc = T(0);
-            for (int w = 0; w < W; ++w) {
-                const int c = sr + w;
-                if (c >= 0 && c < cols)
-                    acc = fma(__ldg(tp + w), staged ? sm[(c - c0) * 256 + threadIdx.x] : __ldg(xo + (int64_t)c * inner + t),
-                              acc);
+        constexpr int NI = kCB / 32;
+        int64_t yb[NI];
+        bool lv[NI];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int64_t f = f0 + i * 32 + lane;
+            lv[i] = f < total;
+            if (aligned) {
+                yb[i] = oc * (int64_t)rows * inner + (f - oc * inner);
+            } else {
+                const int64_t o = lv[i] ? f / inner : 0;
+                yb[i] = o * (int64_t)rows * inner + (f - o * inner);
             }
-            acc *= alpha;
-            T *yp = yo + (int64_t)r * inner + t;
-            if (accumulate) acc += *yp;
-            *yp = acc;
+        }
+#pragma unroll
+        for (int h = 0; h < RPW; ++h) {
+            const int k = warp + NW * h;
+            if (k >= nr) break;
+            const T *sp = sm + off[h] * kCB + lane;
+            T *yr = Y + (int64_t)(r0 + k) * inner;
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                T acc = T(0);
+#pragma unroll
+                for (int w = 0; w < WC; ++w) acc = fma(tp[h][w], sp[w * kCB + i * 32], acc);
+                if (lv[i]) {
+                    acc *= alpha;
+                    if (accumulate) acc += yr[yb[i]];
+                    yr[yb[i]] = acc;
+                }
+            }
         }
     }
+}
+
+template <typename T, int WC>
+static void launch_win(const T *X, T *Y, int64_t outer, const BandMat &M, int64_t inner, double alpha,
+                       bool accumulate, const int32_t *done, cudaStream_t s)
+{
+    const int64_t total = outer * inner;
+    const int64_t bx = (M.rows + kRB - 1) / kRB;
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // ~16 resident blocks per SM over all row groups, each looping over chunks
+    const int64_t by = std::max<int64_t>(1, std::min<int64_t>((total + kCB - 1) / kCB,
+                                                              std::max<int64_t>(1, (int64_t)sms * 16 / bx)));
+    const size_t smem = (size_t)M.win16 * kCB * sizeof(T);
+    set_max_dynamic_smem((const void *)band_mode_product_win_kernel<T, WC>, smem);
+    band_mode_product_win_kernel<T, WC><<<dim3((unsigned)bx, (unsigned)by), kCB, smem, s>>>(
+        X, Y, total, M.rows, M.cols, inner, M.start, (const T *)M.taps, (T)alpha, accumulate ? 1 : 0, done);
+}
+
+// Two fastest modes in one pass (rhs / forward model tail, PAPER.md:83's
+// successive mode products): for each plane o of an (outer, c3, c4) tensor,
+//   Z[a, j] = sum_w M4[j, w] X[o, a, s4[j] + w]        (mode D,   a < c3, j < r4)
+//   Y[o, i, j] = sum_w M3[i, w] Z[s3[i] + w, j]         (mode D-1, i < r3)
+// with the plane and Z in shared memory: the tensor is read once and only the
+// contracted plane is written (config 3's rhs: 256 x 30 -> 128 x 15 per (i1, i2),
+// 1 GB in and 0.25 GB out instead of 1.5 GB + 0.75 GB over two passes).
+// Plane rows have an odd pitch (c4 | 1) so the column reads of stage 1 are
+// conflict-free; stage 1: warp per output column j (its taps in registers),
+// lanes over rows a; stage 2: half-warp per output row i, lanes over j.
+constexpr int kPlaneThreads = 512;
+
+// copies a plane into [row][p4] with the data at column offset g4: one 8- or
+// 4-byte asynchronous copy per element, flat index (row = e / c4 through an fp32
+// reciprocal: exact for e < 2^22)
+template <typename T>
+__device__ __forceinline__ void plane_load_async(T *xs, const T *xp, int nin, int c4, float inv_c4, int p4, int g4)
+{
+    const unsigned base = (unsigned)__cvta_generic_to_shared(xs + g4);
+    for (int e = threadIdx.x; e < nin; e += kPlaneThreads) {
+        const int a = (int)(((float)e + 0.5f) * inv_c4);
+        const unsigned dst = base + (unsigned)((e + a * (p4 - c4)) * (int)sizeof(T));
+        if (sizeof(T) == 8)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(xp + e) : "memory");
+        else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(xp + e) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// Persistent (one block per SM), double-buffered: the next plane's copies are
+// in flight while this one is computed.  Zero guard columns (g4 each side of a
+// plane row) and guard rows (g3 above / below Z) stand in for the columns a
+// band row reaches past the matrix (their taps are zero), so the inner loops
+// have no bounds tests.  Mode-D taps live in registers (warp per column j for
+// the whole kernel); mode-(D-1) taps in a shared table.
+template <typename T, int WC>
+__global__ void __launch_bounds__(kPlaneThreads, 1)
+band_plane2_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t planes, int c3, int c4, int r3, int r4,
+                   const int *__restrict__ s3, const T *__restrict__ t3, int w3, int g3, const int *__restrict__ s4,
+                   const T *__restrict__ t4, int w4, int g4)
+{
+    extern __shared__ __align__(16) unsigned char pl_raw[];
+    const int p4 = (c4 + 2 * g4) | 1;       // odd pitch: conflict-free column reads
+    const int pz = r4 | 1;
+    const int zrows = c3 + 2 * g3;
+    T *xs0 = reinterpret_cast<T *>(pl_raw);  // 2 x [c3][p4]
+    T *zs = xs0 + 2 * (size_t)c3 * p4;      // [zrows][pz]; data rows start at g3
+    T *t3s = zs + (size_t)zrows * pz;       // [r3][WC]
+    int *s3s = reinterpret_cast<int *>(t3s + (size_t)r3 * WC);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = kPlaneThreads / 32;
+    const int nin = c3 * c4, nout = r3 * r4;
+    // one-time: zero guards, stage the mode-(D-1) table
+    for (int e = threadIdx.x; e < 2 * c3 * p4; e += kPlaneThreads) xs0[e] = T(0);
+    for (int e = threadIdx.x; e < zrows * pz; e += kPlaneThreads) zs[e] = T(0);
+    for (int e = threadIdx.x; e < r3 * WC; e += kPlaneThreads) {
+        const int i = e / WC, w = e - i * WC;
+        t3s[e] = w < w3 ? t3[(int64_t)i * w3 + w] : T(0);
+    }
+    for (int i = threadIdx.x; i < r3; i += kPlaneThreads) s3s[i] = s3[i] + g3;
+    __syncthreads();
+    int64_t o = blockIdx.x;
+    const float inv_c4 = 1.0f / (float)c4;
+    if (o < planes) plane_load_async(xs0, X + o * (int64_t)nin, nin, c4, inv_c4, p4, g4);
+    for (int b = 0; o < planes; o += gridDim.x, b ^= 1) {
+        const T *xs = xs0 + (size_t)b * c3 * p4;
+        const int64_t on = o + gridDim.x;
+        if (on < planes) {
+            plane_load_async(xs0 + (size_t)(b ^ 1) * c3 * p4, X + on * (int64_t)nin, nin, c4, inv_c4, p4, g4);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();   // plane o staged (every thread's copies)
+        // stage 1: mode D, warp per output column j, lanes over rows a
+        for (int j = warp; j < r4; j += NW) {
+            const int sj = __ldg(s4 + j) + g4;
+            T tp[WC];
+#pragma unroll
+            for (int w = 0; w < WC; ++w) tp[w] = w < w4 ? __ldg(t4 + (int64_t)j * w4 + w) : T(0);
+            for (int a = lane; a < c3; a += 64) {   // two rows per lane: independent FMA chains
+                const bool two = a + 32 < c3;
+                const T *row = xs + a * p4 + sj;
+                const T *row2 = two ? row + 32 * p4 : row;
+                T acc = T(0), acc2 = T(0);
+#pragma unroll
+                for (int w = 0; w < WC; ++w) {
+                    acc = fma(tp[w], row[w], acc);
+                    acc2 = fma(tp[w], row2[w], acc2);
+                }
+                zs[(a + g3) * pz + j] = acc;
+                if (two) zs[(a + 32 + g3) * pz + j] = acc2;
+            }
+        }
+        __syncthreads();
+        // stage 2: mode D-1, half-warp per output row i, lanes over j
+        T *yp = Y + o * (int64_t)nout;
+        const int half = lane >> 4, hl = lane & 15;
+        for (int i0 = 2 * warp; i0 < r3; i0 += 4 * NW) {   // rows i and i + 2 NW per half-warp
+            const int i = i0 + half, i2 = i + 2 * NW;
+            if (i >= r3) continue;
+            const bool two = i2 < r3;
+            const T *tr = t3s + i * WC, *tr2 = t3s + (two ? i2 : i) * WC;
+            const T *zc = zs + s3s[i] * pz, *zc2 = zs + s3s[two ? i2 : i] * pz;
+            for (int j = hl; j < r4; j += 16) {
+                T acc = T(0), acc2 = T(0);
+#pragma unroll
+                for (int w = 0; w < WC; ++w) {
+                    acc = fma(tr[w], zc[w * pz + j], acc);
+                    acc2 = fma(tr2[w], zc2[w * pz + j], acc2);
+                }
+                yp[i * r4 + j] = acc;
+                if (two) yp[i2 * r4 + j] = acc2;
+            }
+        }
+        __syncthreads();   // zs and xs[b] free before the next plane's stages / copies
+    }
+}
+
+template <typename T, int WC>
+static void launch_plane2_w(const T *X, T *Y, int64_t planes, int c3, int c4, const BandMat &M3, const BandMat &M4,
+                            size_t smem, cudaStream_t s)
+{
+    set_max_dynamic_smem((const void *)band_plane2_kernel<T, WC>, smem);
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(planes, (int64_t)sms));   // one per SM
+    const int g3 = std::max(M3.reach_lo, M3.reach_hi), g4 = std::max(M4.reach_lo, M4.reach_hi);
+    band_plane2_kernel<T, WC><<<(unsigned)grid, kPlaneThreads, smem, s>>>(
+        X, Y, planes, c3, c4, M3.rows, M4.rows, M3.start, (const T *)M3.taps, M3.W, g3, M4.start,
+        (const T *)M4.taps, M4.W, g4);
+}
+
+template <typename T>
+bool launch_band_plane2(const T *X, T *Y, int64_t planes, int c3, int c4, const BandMat &M3, const BandMat &M4,
+                        cudaStream_t s)
+{
+    const int wmax = std::max(M3.W, M4.W);
+    if (wmax > 16 || M3.cols != c3 || M4.cols != c4 || planes <= 0 || (int64_t)c3 * c4 >= (1 << 22)) return false;
+    const int w = wmax <= 4 ? 4 : wmax <= 8 ? 8 : wmax <= 12 ? 12 : 16;
+    const int g3 = std::max(M3.reach_lo, M3.reach_hi), g4 = std::max(M4.reach_lo, M4.reach_hi);
+    const size_t p4 = (size_t)((c4 + 2 * g4) | 1), pz = (size_t)(M4.rows | 1);
+    const size_t smem = (2 * (size_t)c3 * p4 + (size_t)(c3 + 2 * g3) * pz + (size_t)M3.rows * w) * sizeof(T) +
+                        (size_t)M3.rows * sizeof(int);
+    if (smem > 220 * 1024) return false;
+    count_launch();
+    switch (w) {
+    case 4: launch_plane2_w<T, 4>(X, Y, planes, c3, c4, M3, M4, smem, s); break;
+    case 8: launch_plane2_w<T, 8>(X, Y, planes, c3, c4, M3, M4, smem, s); break;
+    case 12: launch_plane2_w<T, 12>(X, Y, planes, c3, c4, M3, M4, smem, s); break;
+    default: launch_plane2_w<T, 16>(X, Y, planes, c3, c4, M3, M4, smem, s); break;
+    }
+    return true;
 }
 
 // Short planes (mode D of a wide tensor: rows x 1) would leave most of every
@@ -179,12 +407,15 @@ void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
             done);
         return;
     }
-    if (inner >= 256 && M.rows >= 2) {
-        const int64_t bx = (inner + 255) / 256, by = (M.rows + kRB - 1) / kRB;
-        const int64_t bz = std::max<int64_t>(1, std::min<int64_t>(outer, std::min<int64_t>(65535, 8 * target / std::max<int64_t>(1, bx * by))));
-        band_mode_product_rows_kernel<T><<<dim3((unsigned)bx, (unsigned)by, (unsigned)bz), 256, 0, s>>>(
-            X, Y, outer, M.rows, M.cols, inner, M.start, (const T *)M.taps, M.W, (T)alpha, accumulate ? 1 : 0, done);
-        return;
+    if (inner >= 32 && M.rows >= 2 && M.W <= 16 && M.win16 <= kKWIN) {
+        switch (M.W) {
+#define TCA_WIN_CASE(w) \
+    case w: launch_win<T, w>(X, Y, outer, M, inner, alpha, accumulate, done, s); return;
+            TCA_WIN_CASE(1) TCA_WIN_CASE(2) TCA_WIN_CASE(3) TCA_WIN_CASE(4) TCA_WIN_CASE(5) TCA_WIN_CASE(6)
+            TCA_WIN_CASE(7) TCA_WIN_CASE(8) TCA_WIN_CASE(9) TCA_WIN_CASE(10) TCA_WIN_CASE(11) TCA_WIN_CASE(12)
+            TCA_WIN_CASE(13) TCA_WIN_CASE(14) TCA_WIN_CASE(15) TCA_WIN_CASE(16)
+#undef TCA_WIN_CASE
+        }
     }
     // plane < 2^32 is guaranteed by the extent limits checked at create
     int64_t bx = (plane + 255) / 256;
@@ -890,6 +1121,8 @@ void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc
 
 // ---------------------------------------------------------------- instantiations
 #define TCA_INST(T)                                                                       \
+    template bool launch_band_plane2<T>(const T *, T *, int64_t, int, int, const BandMat &, \
+                                        const BandMat &, cudaStream_t);                   \
     template void launch_band_mode_product<T>(const T *, T *, int64_t, const BandMat &,    \
                                               int64_t, double, bool, const int32_t *,     \
                                               cudaStream_t);                              \
