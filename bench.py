@@ -422,13 +422,14 @@ def run_tca(args):
         op4.close()
         torch.cuda.empty_cache()
 
-    # ---- configs 0 and 1 (small systems: launch-latency bound): us per CG
-    # iteration of a fixed-iteration solve from x0 = 0, rank 0 only, outside the
-    # timed region (config 0 runs the single-block engine of tca_tiny.cu).
+    # ---- configs 0-2 (small systems: launch-latency bound): us per CG iteration
+    # of a fixed-iteration solve from x0 = 0, rank 0 only, outside the timed
+    # region (config 0 runs the single-block engine of tca_tiny.cu, configs 1-2
+    # the cooperative-grid engine of tca_grid.cu).
     small = None
     if args.small_iters > 0 and rank == 0 and args.workload == "fit":
         small = {}
-        for ci in (0, 1):
+        for ci in (0, 1, 2):
             cs = synth.CONFIGS[ci]
             As, Ls = synth.mode_matrices(cs)
             ops = tca.Operator(As, Ls, cs.lam, dtype="f64")
@@ -440,7 +441,7 @@ def run_tca(args):
                 us = reps_s["seconds"] * 1e6 / max(1, reps_s["iterations"])
                 best = us if best is None else min(best, us)
             small[f"config{ci}"] = {"n": list(cs.n), "iterations": args.small_iters, "cg_us_per_iteration": best,
-                                    "engine": "single-block (tca_tiny.cu)" if ops.tiny_engine else "general"}
+                                    "engine": ops.cg_engine}
             ops.close()
 
     e2e = None

@@ -212,10 +212,14 @@ int tca_operator_cg_fused_step(const tca_operator *op);
  * r, q in registers (shared memory above two elements per thread); chosen for
  * fp64 N <= 4096, fp32 N <= 8192, n_d <= 4095, when the tap tables and vectors
  * fit 224 KB of shared memory, single GPU, not scattered, not a Kronecker-sum-
- * only operator;
- * the environment switch TCA_TINY=0 disables it), 0 = general multi-kernel
- * engine, -1 = op NULL.  Same iterates, stop rules, guards and report either
- * way (readings Z1-Z3, Z10, Z12, Z28). */
+ * only operator; the environment switch TCA_TINY=0 disables it), 2 = one
+ * cooperative grid (tca_grid.cu: the whole solve in ONE persistent kernel, one
+ * block per SM, phases separated by grid-wide barriers, vectors L2-resident;
+ * chosen when the single-block engine is not, for N <= 2^21 and n_d <= 1024
+ * with the tap tables and fibre tiles in 200 KB of shared memory, single GPU,
+ * not scattered, not Kronecker-sum-only; TCA_GRID=0 disables it), 0 = general
+ * multi-kernel engine, -1 = op NULL.  Same iterates, stop rules, guards and
+ * report on every engine (readings Z1-Z3, Z10, Z12, Z28). */
 int tca_operator_cg_engine(const tca_operator *op);
 
 /* y = M x.  x, y: device tensors of the local shape (rows [own_lo, own_hi)

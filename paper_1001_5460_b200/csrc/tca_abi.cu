@@ -917,6 +917,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     h.pcg = pcg == 1;
     op->solver = pcg;
     const bool tiny = pcg == 0 && tiny_cg_eligible(op);
+    const bool gridc = !tiny && pcg == 0 && grid_cg_eligible(op);
     if (op->b1 < 0) {   // fused step B1' for Fig. 2 / PCG on one GPU: opt-in (TCA_B1=1), see DESIGN.md 6.5
         const char *b1env = getenv("TCA_B1");
         const bool want_b1 = b1env && b1env[0] == '1';
@@ -927,7 +928,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
         }
     }
     const int b1_saved = op->b1;
-    if (pcg == 2 || pcg == 3 || tiny) op->b1 = 0;   // single-reduction CG, Jacobi, tiny: their own steps
+    if (pcg == 2 || pcg == 3 || tiny || gridc) op->b1 = 0;   // single-reduction CG, Jacobi, whole-solve engines: own steps
     op->pcur = 0;
     if (op->b1 == 1) {
         const void *ptrs[4] = {op->p_own, op->p2, pcg == 1 ? op->z : op->r, op->q};
@@ -937,7 +938,8 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     *op->sc_host = h;
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
     TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
-    if (tiny) TCA_TRY(launch_tiny_cg(op, b, x, x0_zero, s));   // whole solve in one block (tca_tiny.cu)
+    if (tiny) TCA_TRY(launch_tiny_cg(op, b, x, x0_zero, s));        // whole solve in one block (tca_tiny.cu)
+    else if (gridc) TCA_TRY(launch_grid_cg(op, b, x, x0_zero, s));  // whole solve, one cooperative grid (tca_grid.cu)
     else TCA_TRY(cg_run<T>(op, b, x, rtol, max_iters, h, s, pcg, x0_zero));
     op->b1 = b1_saved;
     TCA_CUDA_TRY(cudaGetLastError());
@@ -1026,7 +1028,7 @@ void tca_operator_destroy(tca_operator *op)
     // every stream that used the operator is done before its memory goes back
     cudaDeviceSynchronize();
     void *pooled[] = {op->r, op->p, op->q, op->t0, op->t1, op->x_ext, op->z, op->pc_tmp, op->sr_s, op->p2,
-                      op->jac_e, op->sc_t, op->sc_perm, op->sc_tstart, op->sc_coef};   // stream-ordered pool
+                      op->jac_e, op->sc_t, op->sc_perm, op->sc_tstart, op->sc_coef, op->grid_ws};   // stream-ordered pool
     for (void *b : pooled)
         if (b) cudaFreeAsync(b, 0);
     dev_put(op->part, sizeof(double) * kRedBlocks * 3);
@@ -1407,7 +1409,12 @@ int tca_operator_apply_path(const tca_operator *op) { return op ? op->apply_path
 
 int tca_operator_cg_fused_step(const tca_operator *op) { return op ? op->b1 : -1; }
 
-int tca_operator_cg_engine(const tca_operator *op) { return op ? (tiny_cg_eligible(op) ? 1 : 0) : -1; }
+int tca_operator_cg_engine(const tca_operator *op)
+{
+    if (!op) return -1;
+    if (tiny_cg_eligible(op)) return 1;
+    return grid_cg_eligible(op) ? 2 : 0;
+}
 
 tca_status tca_apply(const tca_operator *op, const void *x, void *y, void *stream)
 {

@@ -165,6 +165,8 @@ struct tca_operator {
     void *z = nullptr;                           // PCG workspace z = P^-1 r
     void *pc_tmp = nullptr;                      // scratch of the dense-factor mode products
     void *sr_s = nullptr;                        // single-reduction CG: S = A P (lazy)
+    void *grid_ws = nullptr;                     // cooperative-grid CG engine workspace (lazy)
+    size_t grid_ws_bytes = 0;
     void *jac_e = nullptr;                       // tensor Jacobi: E = inverse main diagonal (lazy)
     const void *jac_b = nullptr;                 // tensor Jacobi: B of the running solve
     // generic compressed-band forms
@@ -334,6 +336,9 @@ tca_status set_max_dynamic_smem(const void *func, size_t bytes);
 // whole-solve single-block CG for small problems (tca_tiny.cu)
 bool tiny_cg_eligible(const tca_operator *op);
 tca_status launch_tiny_cg(const tca_operator *op, const void *b, void *x, int x0_zero, cudaStream_t s);
+// whole-solve cooperative-grid CG for mid-size problems (tca_grid.cu)
+bool grid_cg_eligible(const tca_operator *op);
+tca_status launch_grid_cg(tca_operator *op, const void *b, void *x, int x0_zero, cudaStream_t s);
 
 // process-wide count of kernel launches issued by the library
 extern std::atomic<int64_t> g_launches;

@@ -306,6 +306,12 @@ class Operator:
         return _lib.tca_operator_cg_engine(self._h) == 1
 
     @property
+    def cg_engine(self):
+        """Which engine cg_solve runs: 'tiny' (one block, tca_tiny.cu), 'grid' (one
+        cooperative grid, tca_grid.cu) or 'general' (graph-replayed kernels)."""
+        return {1: "tiny", 2: "grid"}.get(_lib.tca_operator_cg_engine(self._h), "general")
+
+    @property
     def cg_fused_step(self):
         """True when CG / PCG solves run the fused step B1' (one kernel per iteration
         forms P, updates C and applies the operator), False otherwise, None before
