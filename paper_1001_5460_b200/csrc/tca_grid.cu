@@ -61,7 +61,11 @@ struct GridArgs {
     int64_t N;
     int order;
     int tile_off;         // byte offset of the fibre tiles in shared memory
-    int dbg;              // measurement switches (TCA_GRID_DBG): 1 skip the fibre phases, 2 skip the update loop
+    // fused first phase (modes D-1 and D on whole planes, D >= 2): planes of
+    // na x nc elements, PT planes per tile, odd pitches
+    int fuse2, na, nc, PT, ptiles, pc, pz;
+    int64_t planes;
+    int dbg;              // measurement switches (TCA_GRID_DBG): 1 skip the fibre phases, 2 the update loop, 4 the phases' arithmetic, 8 their loads
     double lambda;
     GridMode md[kD];
 };
@@ -118,26 +122,53 @@ __device__ __forceinline__ double grid_total(const double *part, double *red)
 }
 
 // sum_w tp[w] col[(s0 + w) * F] over the columns inside [0, n) (taps outside are
-// zero); rows whose window is inside take the unchecked loop with two chains
-template <typename T>
-__device__ __forceinline__ T band_row(const T *tp, int s0, int W, int n, const T *col, int F)
+// zero).  WC > 0: compile-time width (the banded forms, unrolled); WC = 0: any
+// width (dense rows), four independent chains.  Rows whose window lies inside
+// the fibre take the unchecked loop.
+template <int WC, typename T>
+__device__ __forceinline__ T band_row(const T *tp, int s0, int Wrt, int n, const T *col, int F)
 {
-    T a0 = T(0), a1 = T(0);
+    const int W = WC > 0 ? WC : Wrt;
     if (s0 >= 0 && s0 + W <= n) {
         const T *c = col + s0 * F;
+        if (WC > 0) {
+            T a0 = T(0), a1 = T(0);
+#pragma unroll
+            for (int w = 0; w < WC; ++w) {
+                if (w & 1) a1 = fma(tp[w], c[w * F], a1);
+                else a0 = fma(tp[w], c[w * F], a0);
+            }
+            return a0 + a1;
+        }
+        T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
         int w = 0;
-        for (; w + 1 < W; w += 2) {
+        for (; w + 3 < W; w += 4) {
             a0 = fma(tp[w], c[w * F], a0);
             a1 = fma(tp[w + 1], c[(w + 1) * F], a1);
+            a2 = fma(tp[w + 2], c[(w + 2) * F], a2);
+            a3 = fma(tp[w + 3], c[(w + 3) * F], a3);
         }
-        if (w < W) a0 = fma(tp[w], c[w * F], a0);
-    } else {
-        for (int w = 0; w < W; ++w) {
-            const int cc = s0 + w;
-            if (cc >= 0 && cc < n) a0 = fma(tp[w], col[cc * F], a0);
-        }
+        for (; w < W; ++w) a0 = fma(tp[w], c[w * F], a0);
+        return (a0 + a1) + (a2 + a3);
     }
-    return a0 + a1;
+    T a0 = T(0);
+    for (int w = 0; w < W; ++w) {
+        const int cc = s0 + w;
+        if (cc >= 0 && cc < n) a0 = fma(tp[w], col[cc * F], a0);
+    }
+    return a0;
+}
+
+template <typename T>
+__device__ __forceinline__ T band_row_any(const T *tp, int s0, int W, int n, const T *col, int F)
+{
+    switch (W) {
+    case 3: return band_row<3>(tp, s0, W, n, col, F);
+    case 5: return band_row<5>(tp, s0, W, n, col, F);
+    case 7: return band_row<7>(tp, s0, W, n, col, F);
+    case 9: return band_row<9>(tp, s0, W, n, col, F);
+    default: return band_row<0>(tp, s0, W, n, col, F);
+    }
 }
 
 // One phase over the fibres of mode m: for every fibre tile,
@@ -188,7 +219,7 @@ __device__ void fibre_phase(const GridArgs &a, const unsigned char *sm, T *tile,
             else { c = e >> lgF; f = e & (F - 1); }
             const int fb = fbase[f];
             T sv = T(0), pv = T(0), qv = T(0);
-            if (fb >= 0) {
+            if (fb >= 0 && !(a.dbg & 8)) {
                 const int g = fb + c * inner;
                 if (first) {   // P := R + beta P_old, written by the (unique) owner of this element
                     pv = fma(beta, ldcg(pold + g), ldcg(rv + g));
@@ -205,15 +236,15 @@ __device__ void fibre_phase(const GridArgs &a, const unsigned char *sm, T *tile,
             QS[c * PF + f] = qv;
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+        for (int e = threadIdx.x; e < nel && !(a.dbg & 4); e += blockDim.x) {
             int r, f;
             if (cfast) { f = (int)(((float)e + 0.5f) * inv_n); r = e - f * n; }
             else { r = e >> lgF; f = e & (F - 1); }
             const int fb = fbase[f];
             if (fb < 0) continue;
             const int g = fb + r * inner;
-            const T acc = band_row(gt + r * md.gP, gs[r], md.gW, n, S + f, PF);
-            const T reg = md.rW > 0 ? band_row(rt + r * md.rP, rs[r], md.rW, n, PS + f, PF) : T(0);
+            const T acc = band_row_any(gt + r * md.gP, gs[r], md.gW, n, S + f, PF);
+            const T reg = md.rW > 0 ? band_row_any(rt + r * md.rP, rs[r], md.rW, n, PS + f, PF) : T(0);
             if (last) {   // Q += G_1 T + lambda R_1 P (or, D = 1: Q = G P + lambda R P)
                 const T qv = QS[r * PF + f] + fma(lam, reg, acc);
                 q[g] = qv;
@@ -224,6 +255,98 @@ __device__ void fibre_phase(const GridArgs &a, const unsigned char *sm, T *tile,
                 else if (md.rW > 0) q[g] = fma(lam, reg, QS[r * PF + f]);
             }
         }
+    }
+}
+
+// First phase on whole (i_{D-1}, i_D) planes (both fastest modes in one phase):
+//   P := R + beta P_old (own elements), Z = G_D x_D P, RQ = lambda R_D x_D P,
+//   T = G_{D-1} x_{D-1} Z, Q = RQ + lambda R_{D-1} x_{D-1} P   (D > 2: T -> dst)
+//   D == 2 (last): Q += T, <P, Q> partials
+template <typename T>
+__device__ void plane_phase(const GridArgs &a, const unsigned char *sm, T *tile, bool last, const T *pold, T *pn,
+                            T beta, T *dst, double &pq)
+{
+    const GridMode &ma = a.md[a.order - 2], &mc = a.md[a.order - 1];
+    const int na = a.na, nc = a.nc, PT = a.PT, pc = a.pc, pz = a.pz;
+    const int pl = na * nc;
+    T *S = tile;                        // [PT][na][pc] P
+    T *Z = S + (size_t)PT * na * pc;    // [PT][na][pz] G_D P
+    T *RQ = Z + (size_t)PT * na * pz;   // [PT][na][pz] lambda R_D P
+    const T *gtc = reinterpret_cast<const T *>(sm + mc.g_off), *gta = reinterpret_cast<const T *>(sm + ma.g_off);
+    const int *gsc = reinterpret_cast<const int *>(sm + mc.gs_off), *gsa = reinterpret_cast<const int *>(sm + ma.gs_off);
+    const T *rtc = reinterpret_cast<const T *>(sm + mc.r_off), *rta = reinterpret_cast<const T *>(sm + ma.r_off);
+    const int *rsc = reinterpret_cast<const int *>(sm + mc.rs_off), *rsa = reinterpret_cast<const int *>(sm + ma.rs_off);
+    const T *rv = (const T *)a.r;
+    T *q = (T *)a.q;
+    const T lam = (T)a.lambda;
+    const float inv_nc = 1.0f / (float)nc, inv_pl = 1.0f / (float)pl;
+    const int nel = PT * pl;
+    for (int ti = blockIdx.x; ti < a.ptiles; ti += gridDim.x) {
+        const int64_t o0 = (int64_t)ti * PT;
+        const int np = (int)min((int64_t)PT, a.planes - o0);
+        const int ne = np * pl;
+        __syncthreads();   // previous tile's reads done
+        for (int e = threadIdx.x; e < ne; e += blockDim.x) {   // contiguous: the tile's planes are one run
+            const int pp = (int)(((float)e + 0.5f) * inv_pl), w = e - pp * pl;
+            const int ai = (int)(((float)w + 0.5f) * inv_nc), ci = w - ai * nc;
+            const int64_t g = o0 * pl + e;
+            T pv = T(0);
+            if (!(a.dbg & 8)) pv = fma(beta, ldcg(pold + g), ldcg(rv + g));
+            pn[g] = pv;
+            S[((size_t)pp * na + ai) * pc + ci] = pv;
+        }
+        __syncthreads();
+        // stage 1: mode D along the contiguous index
+        for (int e = threadIdx.x; e < ne && !(a.dbg & 4); e += blockDim.x) {
+            const int pp = (int)(((float)e + 0.5f) * inv_pl), w = e - pp * pl;
+            const int ai = (int)(((float)w + 0.5f) * inv_nc), j = w - ai * nc;
+            const T *row = S + ((size_t)pp * na + ai) * pc;
+            Z[((size_t)pp * na + ai) * pz + j] = band_row_any(gtc + j * mc.gP, gsc[j], mc.gW, nc, row, 1);
+            RQ[((size_t)pp * na + ai) * pz + j] =
+                mc.rW > 0 ? lam * band_row_any(rtc + j * mc.rP, rsc[j], mc.rW, nc, row, 1) : T(0);
+        }
+        __syncthreads();
+        // stage 2: mode D-1
+        for (int e = threadIdx.x; e < ne && !(a.dbg & 4); e += blockDim.x) {
+            const int pp = (int)(((float)e + 0.5f) * inv_pl), w = e - pp * pl;
+            const int i = (int)(((float)w + 0.5f) * inv_nc), j = w - i * nc;
+            const T *zc = Z + (size_t)pp * na * pz + j;
+            const T t = band_row_any(gta + i * ma.gP, gsa[i], ma.gW, na, zc, pz);
+            T qv = RQ[((size_t)pp * na + i) * pz + j];
+            if (ma.rW > 0) qv = fma(lam, band_row_any(rta + i * ma.rP, rsa[i], ma.rW, na, S + (size_t)pp * na * pc + j, pc), qv);
+            const int64_t g = o0 * pl + e;
+            if (last) {
+                qv += t;
+                pq += (double)S[((size_t)pp * na + i) * pc + j] * (double)qv;
+            } else {
+                dst[g] = t;
+            }
+            q[g] = qv;
+        }
+    }
+}
+
+// The operator phases of one iteration (Q := A P, P := R + beta P_old formed on
+// the way), D - 1 grid barriers inside (with the fused first phase D - 2); the
+// caller synchronises after.  pq: this thread's <P, Q> partial.
+template <typename T>
+__device__ void operator_phases(const GridArgs &a, const unsigned char *sm, T *tile, T *pold, T *pn, T beta,
+                                T *const *tb, double &pq)
+{
+    const int D = a.order;
+    if (a.fuse2) {
+        plane_phase<T>(a, sm, tile, D == 2, pold, pn, beta, tb[0], pq);
+        for (int k = 2; k < D; ++k) {   // modes D-2 .. 1 (0-based D-1-k)
+            grid_sync(a.bar);
+            const int j = k - 2;
+            fibre_phase<T>(a, sm, tile, D - 1 - k, false, k == D - 1, tb[j & 1], tb[(j + 1) & 1], pn, pn, beta, pq);
+        }
+        return;
+    }
+    for (int k = 0; k < D; ++k) {
+        if (k > 0) grid_sync(a.bar);
+        fibre_phase<T>(a, sm, tile, D - 1 - k, k == 0, k == D - 1, k == 0 ? nullptr : tb[(k - 1) & 1], tb[k & 1],
+                       k == 0 ? pold : pn, pn, beta, pq);
     }
 }
 
@@ -267,12 +390,8 @@ __global__ void __launch_bounds__(kGridThreads, 1) grid_cg_kernel(const __grid_c
         }
         grid_sync(a.bar);
         double dummy = 0.0;
-        for (int k = 0; k < D; ++k) {
-            const int m = D - 1 - k;
-            fibre_phase<T>(a, sm, tile, m, k == 0, k == D - 1, k == 0 ? nullptr : tb[(k - 1) & 1], tb[k & 1], pb[k == 0 ? 0 : 1],
-                           pb[1], T(0), dummy);
-            grid_sync(a.bar);
-        }
+        operator_phases<T>(a, sm, tile, pb[0], pb[1], T(0), tb, dummy);
+        grid_sync(a.bar);
         for (int64_t i = gtid; i < N; i += gstride) {   // Q = A*C
             const T bi = b[i], ri = T(bi - ldcg(q + i));
             r[i] = ri;
@@ -316,14 +435,8 @@ __global__ void __launch_bounds__(kGridThreads, 1) grid_cg_kernel(const __grid_c
         first_it = false;
         double pq = 0.0;
         T *pn = pb[cur ^ 1];
-        for (int k = 0; k < D; ++k) {
-            const int m = D - 1 - k;
-            if (!(a.dbg & 1))
-                fibre_phase<T>(a, sm, tile, m, k == 0, k == D - 1, k == 0 ? nullptr : tb[(k - 1) & 1], tb[k & 1],
-                               k == 0 ? pb[cur] : pn, pn, beta, pq);
-            if (k + 1 < D) grid_sync(a.bar);
-        }
-        if (a.dbg & 1) pq = 1.0;
+        if (!(a.dbg & 1)) operator_phases<T>(a, sm, tile, pb[cur], pn, beta, tb, pq);
+        if (a.dbg & 13) pq = 1.0;
         pq = block_sum(pq, red);
         if (threadIdx.x == 0) part[blockIdx.x] = pq;
         grid_sync(a.bar);
@@ -419,6 +532,30 @@ size_t grid_plan(const tca_operator *op, int grid, GridArgs *out)
             off = (off + 15) & ~(size_t)15;
         }
         inner *= m.n;
+    }
+    // fuse the two fastest modes when a plane (three arrays) fits the tile budget
+    static const bool no_fuse = getenv("TCA_GRID_NOFUSE") != nullptr;   // measurement switch
+    if (op->order >= 2 && !no_fuse) {
+        const int na = (int)op->n[op->order - 2], nc = (int)op->n[op->order - 1];
+        const int pc = nc | 1, pz = nc | 1;
+        auto pbytes = [&](int pt) { return (size_t)pt * na * (pc + 2 * pz) * es; };
+        const int64_t planes = op->N / ((int64_t)na * nc);
+        // only with a plane for every block: fewer, larger tiles lose more to
+        // the idle blocks than the saved phase (config 1: 48 planes, 30.5 vs
+        // 24.7 us per iteration; config 2: 1024 planes, 44.3 vs 50.8 us)
+        if (pbytes(1) <= kTileBudget && planes >= grid) {
+            int PT = 1;
+            while (PT < 64 && pbytes(2 * PT) <= kTileBudget && (planes + PT - 1) / PT > grid) PT *= 2;
+            a.fuse2 = 1;
+            a.na = na;
+            a.nc = nc;
+            a.PT = PT;
+            a.pc = pc;
+            a.pz = pz;
+            a.planes = planes;
+            a.ptiles = (int)((planes + PT - 1) / PT);
+            tile_max = std::max(tile_max, pbytes(PT));
+        }
     }
     a.tile_off = (int)off;
     off += tile_max;
