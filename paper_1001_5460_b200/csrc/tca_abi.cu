@@ -371,24 +371,50 @@ static tca_status chain_products(const tca_operator *op, const T *in, T *out,
         TCA_CUDA_TRY(cudaMallocAsync((void **)&tmp[0], maxi * sizeof(T), s));
         if (order.size() > 2) TCA_CUDA_TRY(cudaMallocAsync((void **)&tmp[1], maxi * sizeof(T), s));
     }
+    std::vector<int> rest = order;
+    const T *cur = in;
+    int tsel = 0;
+    // opt-in (TCA_RHS_FUSE1=1): first pass = mode 1 together with the contiguous
+    // last mode L when mode 1 comes first and L contracts (launch_band_win_last:
+    // the pass writes the tensor with L already contracted).  Measured slower on
+    // config 3 (1.89 ms for the fused pass + 0.59 ms for modes 2-3, vs 1.98 ms
+    // for the default chain)
+    static const bool fuse1 = getenv("TCA_RHS_FUSE1") && getenv("TCA_RHS_FUSE1")[0] == '1';
+    if (fuse1 && rest.size() >= 2 && rest[0] == 0) {
+        const int L = *std::max_element(rest.begin(), rest.end());
+        bool ok = L > 0 && ext_out[L] <= ext_in[L] && !mats[0].dense && !mats[L].dense;
+        for (int e = L + 1; e < kD && ok; ++e) ok = ext_in[e] == 1 && ext_out[e] == 1;
+        if (ok) {
+            int64_t K = 1;
+            for (int e = 1; e < L; ++e) K *= ext[e];
+            T *dst = rest.size() == 2 ? out : tmp[tsel];
+            if (launch_band_win_last<T>(cur, dst, K, (int)ext[L], mats[0], mats[L], s)) {
+                ext[0] = ext_out[0];
+                ext[L] = ext_out[L];
+                cur = dst;
+                tsel ^= 1;
+                rest.erase(std::remove(rest.begin(), rest.end(), L), rest.end());
+                rest.erase(rest.begin());
+            }
+        }
+    }
     // the last two products on the two fastest non-trivial modes (d, d+1): one
     // plane pass (launch_band_plane2) when the plane fits shared memory
-    size_t nsep = order.size();
+    size_t nsep = rest.size();
     int pd = -1;
-    if (order.size() >= 2) {
-        const int a = order[order.size() - 2], c = order[order.size() - 1];
+    if (rest.size() >= 2) {
+        const int a = rest[rest.size() - 2], c = rest[rest.size() - 1];
         const int d = std::min(a, c);
         bool trailing_unit = std::max(a, c) == d + 1;
-        for (int e = d + 2; e < kD && trailing_unit; ++e) trailing_unit = ext_in[e] == 1 && ext_out[e] == 1;
+        for (int e = d + 2; e < kD && trailing_unit; ++e) trailing_unit = ext[e] == 1 && ext_out[e] == 1;
         if (trailing_unit && !mats[d].dense && !mats[d + 1].dense) {
             pd = d;
             nsep -= 2;
         }
     }
-    const T *cur = in;
-    for (size_t i = 0; i < order.size(); ++i) {
-        const int d = order[i];
-        T *dst = (i + 1 == order.size()) ? out : tmp[i & 1];
+    for (size_t i = 0; i < rest.size(); ++i) {
+        const int d = rest[i];
+        T *dst = (i + 1 == rest.size()) ? out : tmp[tsel];
         if (i == nsep && pd >= 0) {
             int64_t planes = 1;
             for (int e = 0; e < pd; ++e) planes *= ext[e];
@@ -400,6 +426,7 @@ static tca_status chain_products(const tca_operator *op, const T *in, T *out,
         mode_product<T>(cur, dst, outer_of(ext, d), mats[d], inner_of(ext, d), 1.0, false, nullptr, s);
         ext[d] = ext_out[d];
         cur = dst;
+        tsel ^= 1;
     }
     if (order.empty()) {
         size_t sz = 1;

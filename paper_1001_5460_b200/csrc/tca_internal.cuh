@@ -253,6 +253,11 @@ void launch_band_mode_product(const T *X, T *Y, int64_t outer, const BandMat &M,
                               int64_t inner, double alpha, bool accumulate,
                               const int32_t *done, cudaStream_t s);
 
+// mode 1 and the contiguous last mode of a (cols, K c4) tensor in one pass (M1: rows x
+// cols, M4: r4 x c4); false when not applicable (nothing launched)
+template <typename T>
+bool launch_band_win_last(const T *X, T *Y, int64_t K, int c4, const BandMat &M1, const BandMat &M4, cudaStream_t s);
+
 // the two fastest modes of an (planes, c3, c4) tensor in one pass (M3: rows r3 x
 // cols c3, M4: r4 x c4); false when the plane does not fit shared memory (nothing launched)
 template <typename T>

@@ -203,6 +203,152 @@ static void launch_win(const T *X, T *Y, int64_t outer, const BandMat &M, int64_
         X, Y, total, M.rows, M.cols, inner, M.start, (const T *)M.taps, (T)alpha, accumulate ? 1 : 0, done);
 }
 
+// Mode 1 (the slowest) and the last mode L (contiguous fibres of c4 elements)
+// in one pass, for the first product of a chain: X is (cols, K c4), Y is
+// (rows, K r4).  The window kernel's staging and mode-1 arithmetic on chunks of
+// FPC = kCB / c4 whole mode-L fibres; the 16 x FPC c4 mode-1 results go to
+// shared memory and are contracted along mode L (M4: r4 x c4 band rows) before
+// the store, so the pass writes the tensor with mode L already contracted
+// (config 3's rhs: 4.0 GB in, 1.0 GB out instead of 2.0 GB).
+template <typename T, int WC>
+__global__ void __launch_bounds__(kCB)
+band_win_last_kernel(const T *__restrict__ X, T *__restrict__ Y, int64_t K, int rows, int cols, int c4, int r4,
+                     const int *__restrict__ start, const T *__restrict__ taps, const int *__restrict__ s4,
+                     const T *__restrict__ t4, int w4)
+{
+    extern __shared__ __align__(16) unsigned char win_raw[];
+    T *sm = reinterpret_cast<T *>(win_raw);
+    constexpr int NW = kCB / 32, RPW = kRB / NW, NI = kCB / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int FPC = kCB / c4, CW = FPC * c4;           // whole fibres per chunk, chunk width
+    const int64_t inner = K * c4, inner_o = K * r4;
+    const int r0 = blockIdx.x * kRB;
+    const int nr = min(kRB, rows - r0);
+    int base = __ldg(start + r0), top = base;
+    for (int k = 1; k < nr; ++k) {
+        const int sr = __ldg(start + r0 + k);
+        base = min(base, sr);
+        top = max(top, sr);
+    }
+    top += WC;
+    T tp[RPW][WC];
+    int off[RPW];
+#pragma unroll
+    for (int h = 0; h < RPW; ++h) {
+        const int k = warp + NW * h;
+        const bool ok = k < nr;
+        off[h] = ok ? __ldg(start + r0 + k) - base : 0;
+#pragma unroll
+        for (int w = 0; w < WC; ++w) tp[h][w] = ok ? __ldg(taps + (int64_t)(r0 + k) * WC + w) : T(0);
+    }
+    const int cv0 = max(base, 0), cv1 = min(top, cols);
+    const int up = CW | 1;   // pitch of the mode-1 results in shared memory
+    for (int64_t ch = blockIdx.y; ch * FPC < K; ch += gridDim.y) {
+        const int64_t f0 = ch * CW;                      // first column of the chunk
+        const int fib = (int)min((int64_t)FPC, K - ch * FPC);
+        const int cw = fib * c4;
+        {   // stage column tid of the window
+            __syncthreads();
+            T *row = sm + threadIdx.x;
+            const bool live = threadIdx.x < cw;
+            for (int c = base; c < cv0; ++c) row[(c - base) * kCB] = T(0);
+            for (int c = max(cv1, base); c < top; ++c) row[(c - base) * kCB] = T(0);
+            if (live) {
+                const T *src = X + f0 + threadIdx.x + (int64_t)cv0 * inner;
+                unsigned dst = (unsigned)__cvta_generic_to_shared(row + (cv0 - base) * kCB);
+                for (int c = cv0; c < cv1; ++c, src += inner, dst += kCB * sizeof(T)) {
+                    if (sizeof(T) == 8)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+                    else
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
+                }
+            } else {
+                for (int c = cv0; c < cv1; ++c) row[(c - base) * kCB] = T(0);
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+            __syncthreads();
+        }
+        T u[RPW][NI];
+#pragma unroll
+        for (int h = 0; h < RPW; ++h) {
+            const T *sp = sm + off[h] * kCB + lane;
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                T acc = T(0);
+#pragma unroll
+                for (int w = 0; w < WC; ++w) acc = fma(tp[h][w], sp[w * kCB + i * 32], acc);
+                u[h][i] = acc;
+            }
+        }
+        __syncthreads();   // window reads done: the buffer takes the mode-1 results
+#pragma unroll
+        for (int h = 0; h < RPW; ++h) {
+            const int k = warp + NW * h;
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int c = i * 32 + lane;
+                if (k < nr && c < CW) sm[k * up + c] = u[h][i];
+            }
+        }
+        __syncthreads();
+        // mode L: Y[r0 + k, (ch FPC + f) r4 + j] = sum_w t4[j, w] U[k, f c4 + s4[j] + w];
+        // thread (half, t): output column t = (f, j) of rows half*8 .. half*8+7,
+        // the row's taps (clipped to the fibre) in registers
+        const int per = fib * r4;
+        const int half = threadIdx.x >> 6;
+        for (int t = threadIdx.x & 63; t < per; t += 64) {
+            const int f = t / r4, j = t - f * r4;
+            const int sj = __ldg(s4 + j);
+            const int wlo = max(0, -sj), whi = min(w4, c4 - sj);
+            T tw[16];
+#pragma unroll
+            for (int w = 0; w < 16; ++w) tw[w] = (w >= wlo && w < whi) ? __ldg(t4 + j * w4 + w) : T(0);
+            const T *ub = sm + f * c4 + sj;
+            for (int k = half * (kRB / 2); k < min(nr, (half + 1) * (kRB / 2)); ++k) {
+                const T *ur = ub + k * up;
+                T acc = T(0);
+#pragma unroll
+                for (int w = 0; w < 16; ++w)
+                    if (w >= wlo && w < whi) acc = fma(tw[w], ur[w], acc);
+                Y[(int64_t)(r0 + k) * inner_o + (ch * FPC + f) * r4 + j] = acc;
+            }
+        }
+    }
+}
+
+template <typename T, int WC>
+static void launch_win_last_w(const T *X, T *Y, int64_t K, int c4, const BandMat &M1, const BandMat &M4,
+                              cudaStream_t s)
+{
+    const int64_t bx = (M1.rows + kRB - 1) / kRB;
+    const int FPC = kCB / c4;
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t chunks = (K + FPC - 1) / FPC;
+    const int64_t by = std::max<int64_t>(1, std::min<int64_t>(chunks, std::max<int64_t>(1, (int64_t)sms * 16 / bx)));
+    const size_t smem = std::max<size_t>((size_t)M1.win16 * kCB, (size_t)kRB * ((FPC * c4) | 1)) * sizeof(T);
+    set_max_dynamic_smem((const void *)band_win_last_kernel<T, WC>, smem);
+    band_win_last_kernel<T, WC><<<dim3((unsigned)bx, (unsigned)by), kCB, smem, s>>>(
+        X, Y, K, M1.rows, M1.cols, c4, M4.rows, M1.start, (const T *)M1.taps, M4.start, (const T *)M4.taps, M4.W);
+}
+
+template <typename T>
+bool launch_band_win_last(const T *X, T *Y, int64_t K, int c4, const BandMat &M1, const BandMat &M4, cudaStream_t s)
+{
+    if (M1.W > 16 || M1.win16 > kKWIN || M1.rows < 2 || c4 > kCB || c4 < 1 || M4.cols != c4 || K <= 0) return false;
+    count_launch();
+    switch (M1.W) {
+#define TCA_WL_CASE(w) \
+    case w: launch_win_last_w<T, w>(X, Y, K, c4, M1, M4, s); return true;
+        TCA_WL_CASE(1) TCA_WL_CASE(2) TCA_WL_CASE(3) TCA_WL_CASE(4) TCA_WL_CASE(5) TCA_WL_CASE(6)
+        TCA_WL_CASE(7) TCA_WL_CASE(8) TCA_WL_CASE(9) TCA_WL_CASE(10) TCA_WL_CASE(11) TCA_WL_CASE(12)
+        TCA_WL_CASE(13) TCA_WL_CASE(14) TCA_WL_CASE(15) TCA_WL_CASE(16)
+#undef TCA_WL_CASE
+    }
+    return false;
+}
+
 // Two fastest modes in one pass (rhs / forward model tail, PAPER.md:83's
 // successive mode products): for each plane o of an (outer, c3, c4) tensor,
 //   Z[a, j] = sum_w M4[j, w] X[o, a, s4[j] + w]        (mode D,   a < c3, j < r4)
@@ -1121,6 +1267,8 @@ void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc
 
 // ---------------------------------------------------------------- instantiations
 #define TCA_INST(T)                                                                       \
+    template bool launch_band_win_last<T>(const T *, T *, int64_t, int, const BandMat &,   \
+                                          const BandMat &, cudaStream_t);                 \
     template bool launch_band_plane2<T>(const T *, T *, int64_t, int, int, const BandMat &, \
                                         const BandMat &, cudaStream_t);                   \
     template void launch_band_mode_product<T>(const T *, T *, int64_t, const BandMat &,    \
