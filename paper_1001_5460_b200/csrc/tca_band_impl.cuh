@@ -323,11 +323,17 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 template <int M, typename T>
 __device__ __forceinline__ T tapG(const Params<T> &a, int off, int r, int k)
 {
+#ifdef TCA_DBG_CONST_TAPS
+    if (M != 4) { off = 0; r = 0; }   // timing experiment: compile-time tap addresses (wrong results)
+#endif
     return k >= 0 ? a.taps[(off + r + PADR) * REC + k] : a.taps[(off + r + k + PADR) * REC - k];
 }
 template <int M, typename T>
 __device__ __forceinline__ T tapR(const Params<T> &a, int off, int r, int k)
 {
+#ifdef TCA_DBG_CONST_TAPS
+    if (M != 4) { off = 0; r = 0; }
+#endif
     return k >= 0 ? a.taps[(off + r + PADR) * REC + 4 + k] : a.taps[(off + r + k + PADR) * REC + 4 - k];
 }
 template <int M, typename T, int NBM>
