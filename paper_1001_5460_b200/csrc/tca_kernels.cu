@@ -636,12 +636,133 @@ dense_mode_product_dmma_kernel(const double *__restrict__ X, double *__restrict_
     }
 }
 
+// Shared-memory tiled form: a block computes a 64-row x 64-fibre tile of Y,
+// stepping K by 16: the M tile (64 x 16) and the X tile (16 x 64: 16 rows of
+// 64 fibres) are staged in shared memory (double-buffered, the next step's
+// global loads in registers while this step's DMMAs run), and each of the 8
+// warps computes a 16 x 32 sub-tile as 2 x 4 m8n8k4 accumulators, so every
+// fragment element loaded from shared memory feeds 2-4 DMMAs (the direct
+// kernel above reloads both operands from global memory for every DMMA).
+constexpr int kDBM = 64, kDBN = 64, kDBK = 16, kDPA = kDBK + 4, kDPB = kDBN + 4;
+
+__global__ void __launch_bounds__(256)
+dense_mode_product_dmma_tiled_kernel(const double *__restrict__ X, double *__restrict__ Y, int64_t nfib, int rows,
+                                     int cols, int64_t inner, const double *__restrict__ M, double alpha,
+                                     int accumulate, const int32_t *done)
+{
+    if (done && *done) return;
+    __shared__ double As[2][kDBM * kDPA];
+    __shared__ double Bs[2][kDBK * kDPB];
+    __shared__ int64_t fbase[kDBN];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r0 = blockIdx.y * kDBM;
+    const int64_t f0 = (int64_t)blockIdx.x * kDBN;
+    if (tid < kDBN) {
+        const int64_t f = f0 + tid;
+        if (f < nfib) {
+            const int64_t o = f / inner, t = f - o * inner;
+            fbase[tid] = o * (int64_t)cols * inner + t;
+        } else {
+            fbase[tid] = -1;
+        }
+    }
+    __syncthreads();
+    const bool kfast = inner == 1;   // fibres contiguous: load each fibre's k-run (coalesced)
+    // this thread's 4 A and 4 B tile elements (global -> registers -> shared)
+    double ra[4], rb[4];
+    auto gload = [&](int k0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = tid + u * 256;
+            const int m = e / kDBK, k = e % kDBK;   // A: k fastest
+            const int rr = r0 + m, kk = k0 + k;
+            ra[u] = (rr < rows && kk < cols) ? __ldg(M + (int64_t)rr * cols + kk) : 0.0;
+            int bk, bn;
+            if (kfast) { bn = e / kDBK; bk = e % kDBK; }
+            else { bk = e / kDBN; bn = e % kDBN; }
+            const int64_t fb = fbase[bn];
+            const int kb = k0 + bk;
+            rb[u] = (fb >= 0 && kb < cols) ? __ldg(X + fb + (int64_t)kb * inner) : 0.0;
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = tid + u * 256;
+            As[buf][(e / kDBK) * kDPA + e % kDBK] = ra[u];
+            int bk, bn;
+            if (kfast) { bn = e / kDBK; bk = e % kDBK; }
+            else { bk = e / kDBN; bn = e % kDBN; }
+            Bs[buf][bk * kDPB + bn] = rb[u];
+        }
+    };
+    const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;   // warp sub-tile origin
+    const int ar = lane >> 2, ak = lane & 3, bk = lane & 3, bn = lane >> 2;
+    double d[2][4][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+    const int nk = (cols + kDBK - 1) / kDBK;
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    for (int ks = 0; ks < nk; ++ks) {
+        const int buf = ks & 1;
+        if (ks + 1 < nk) gload((ks + 1) * kDBK);
+#pragma unroll
+        for (int kk = 0; kk < kDBK; kk += 4) {
+            double af[2], bf[4];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) af[i] = As[buf][(wm + i * 8 + ar) * kDPA + kk + ak];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][(kk + bk) * kDPB + wn + j * 8 + bn];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma884(d[i][j][0], d[i][j][1], af[i], bf[j]);
+        }
+        if (ks + 1 < nk) {
+            sstore(buf ^ 1);   // the other buffer: last read one step ago, before this step's barrier
+            __syncthreads();
+        }
+    }
+    const int dr = lane >> 2, dn = 2 * (lane & 3);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int r = r0 + wm + i * 8 + dr;
+        if (r >= rows) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int fl = wn + j * 8 + dn + h;
+                const int64_t f = f0 + fl;
+                if (f < nfib) {
+                    const int64_t o = f / inner, t = f - o * inner;
+                    double *yp = Y + (o * rows + r) * inner + t;
+                    double v = alpha * d[i][j][h];
+                    if (accumulate) v += *yp;
+                    *yp = v;
+                }
+            }
+    }
+}
+
 void launch_dense_mode_product_dmma(const double *X, double *Y, int64_t outer, int rows, int cols,
                                     int64_t inner, const double *M, double alpha, bool accumulate,
                                     const int32_t *done, cudaStream_t s)
 {
     const int64_t nfib = outer * inner;
     if (nfib == 0 || rows == 0) return;
+    static const bool direct = getenv("TCA_DMMA_DIRECT") != nullptr;   // measurement switch: the untiled kernel
+    if (!direct && rows >= 32 && cols >= 16 && (nfib + kDBN - 1) / kDBN < (1ll << 31) && (rows + kDBM - 1) / kDBM < 65536) {
+        count_launch();
+        dense_mode_product_dmma_tiled_kernel<<<dim3((unsigned)((nfib + kDBN - 1) / kDBN), (unsigned)((rows + kDBM - 1) / kDBM)),
+                                               256, 0, s>>>(X, Y, nfib, rows, cols, inner, M, alpha, accumulate ? 1 : 0,
+                                                            done);
+        return;
+    }
     const int64_t tiles = (int64_t)((rows + 7) / 8) * ((nfib + 7) / 8);
     int64_t blocks = (tiles + 7) / 8;   // 8 warps per block, one tile per warp per pass
     if (blocks > 148 * 16) blocks = 148 * 16;
