@@ -337,7 +337,10 @@ def run_tca(args):
     nloc = int(np.prod(local_n))
     apply_us = 1e3 * state["apply_ms"] / max(1, state["apply_cnt"])
     apply_bytes = 2 * nloc * esize  # read p, write q (algorithmic, this rank's shard)
-    achieved = apply_bytes / (apply_us * 1e-6) / 1e9
+    # (a whole-solve engine -- tca_tiny.cu / tca_grid.cu, small configs -- has no
+    # separate apply launches inside CG: the roofline then uses the standalone apply)
+    in_cg = state["apply_cnt"] > 0
+    achieved = apply_bytes / (apply_us * 1e-6) / 1e9 if in_cg else 0.0
     traffic = None
     try:   # DRAM bytes per launch from the committed ncu --set full capture (tools/ncu_traffic.py)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -378,6 +381,7 @@ def run_tca(args):
         op.apply(xin, yout)
     barrier()
     ams, acnt = op.get_timing()
+    op_engine = op.cg_engine
     op.close()
     a_us = 1e3 * ams / acnt
     apply_info = {"us": a_us, "applies_per_s": 1e6 / a_us,
@@ -385,7 +389,12 @@ def run_tca(args):
                   "frac_hbm": apply_bytes / (a_us * 1e-6) / 1e9 / hbm}
     phases = {"create_ms": create_ms, "rhs_ms": rhs_ms, "cg_ms": rep["seconds"] * 1e3,
               "cg_us_per_iteration": rep["seconds"] * 1e6 / max(1, rep["iterations"]),
-              "apply_us_in_cg": apply_us}
+              "apply_us_in_cg": apply_us if in_cg else None}
+    if not in_cg:
+        roofline.update({"achieved": apply_info["GBps"], "frac": apply_info["frac_hbm"], "us_per_launch": a_us,
+                         "launches_timed": acnt,
+                         "kernel": "operator apply q = M p, standalone (CG ran as one whole-solve kernel, "
+                                   f"engine {op_engine})"})
 
     # ---- north_star's scaling system (config 4: 256^3 x 32 fp64, mode 1 sharded over
     # the ranks) at this N: ms per CG iteration of the device-resident solve (max
@@ -496,8 +505,9 @@ def run_tca(args):
         "config": {"workload": workload_name(cfg, dtype, iters, rtol, args.solver), "solver": args.solver, "config_index": cfg.index,
                    "unknowns": cfg.N, "data_points": cfg.Mdata, "cg_iters_per_step": iters,
                    "step": "tca_operator_create + tca_rhs + tca_cg_solve (or tca_pcg_solve) + tca_operator_destroy",
-                   "l2": "inputs larger than L2 (each vector %d MB, y %d MB)" % (
-                       cfg.N * esize >> 20, cfg.Mdata * esize >> 20),
+                   "l2": ("inputs larger than L2 (each vector %.1f MB, y %.1f MB)" if cfg.N * esize * 5 > 126e6 else
+                          "vectors L2-resident (each vector %.1f MB, y %.1f MB; 126 MB L2)") % (
+                       cfg.N * esize / 2**20, cfg.Mdata * esize / 2**20),
                    "parallelism": "single GPU" if world == 1 else
                    f"mode-1 sharding over {world} GPUs (NCCL halo + all-reduce)"},
         "roofline": roofline,
@@ -512,7 +522,7 @@ def run_tca(args):
         "cg_report": {"iterations": rep["iterations"], "rho0": rep["rho0"],
                       "rho_final": rep["rho_final"], "relres_final": rep["relres_final"],
                       "status": rep["status"]},
-        "apply_path": state["path"],
+        "apply_path": state["path"], "cg_engine": op_engine,
         "phases": phases,
         "step_host_ms": state.get("host_ms"),   # [create, rhs enqueue, solve (synchronous), solve device, destroy] per timed step
     }
