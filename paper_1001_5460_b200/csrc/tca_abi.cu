@@ -966,8 +966,11 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
     TCA_CUDA_TRY(cudaMemcpyAsync(op->sc, op->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
     TCA_CUDA_TRY(cudaEventRecord(op->ev0, s));
     if (tiny) TCA_TRY(launch_tiny_cg(op, b, x, x0_zero, s));        // whole solve in one block (tca_tiny.cu)
-    else if (gridc) TCA_TRY(launch_grid_cg(op, b, x, x0_zero, s));  // whole solve, one cooperative grid (tca_grid.cu)
-    else TCA_TRY(cg_run<T>(op, b, x, rtol, max_iters, h, s, pcg, x0_zero));
+    else {
+        bool launched = false;   // whole solve, one cooperative grid (tca_grid.cu)
+        if (gridc) TCA_TRY(launch_grid_cg(op, b, x, x0_zero, s, &launched));
+        if (!launched) TCA_TRY(cg_run<T>(op, b, x, rtol, max_iters, h, s, pcg, x0_zero));
+    }
     op->b1 = b1_saved;
     TCA_CUDA_TRY(cudaGetLastError());
     TCA_CUDA_TRY(cudaEventRecord(op->ev1, s));

@@ -651,8 +651,9 @@ int grid_blocks(const tca_operator *op)
 }
 
 template <typename T>
-tca_status launch_t(tca_operator *op, const void *b, void *x, int x0_zero, cudaStream_t s)
+tca_status launch_t(tca_operator *op, const void *b, void *x, int x0_zero, cudaStream_t s, bool *launched)
 {
+    *launched = false;
     const int grid = grid_blocks(op);
     GridArgs a{};
     const size_t smem = grid_plan(op, grid, &a);
@@ -687,10 +688,22 @@ tca_status launch_t(tca_operator *op, const void *b, void *x, int x0_zero, cudaS
         a.t0 = op->t0;
     }
     TCA_TRY(set_max_dynamic_smem((const void *)grid_cg_kernel<T>, smem));
-    count_launch();
+    // every block must be co-resident (the grid barrier spins): otherwise (a
+    // shared or partitioned GPU) the caller runs the general engine
+    int per_sm = 0;
+    TCA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)grid_cg_kernel<T>, kGridThreads,
+                                                               smem));
+    if (per_sm * op->num_sms < grid) return TCA_OK;
     void *args[] = {(void *)&a};
-    TCA_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)grid_cg_kernel<T>, dim3(grid), dim3(kGridThreads), args,
-                                             smem, s));
+    const cudaError_t e = cudaLaunchCooperativeKernel((const void *)grid_cg_kernel<T>, dim3(grid), dim3(kGridThreads),
+                                                      args, smem, s);
+    if (e == cudaErrorCooperativeLaunchTooLarge) {
+        cudaGetLastError();
+        return TCA_OK;
+    }
+    TCA_CUDA_TRY(e);
+    count_launch();
+    *launched = true;
     return TCA_OK;
 }
 
@@ -711,10 +724,10 @@ bool grid_cg_eligible(const tca_operator *op)
     return grid_plan(op, op->num_sms, nullptr) <= kGridSmem;
 }
 
-tca_status launch_grid_cg(tca_operator *op, const void *b, void *x, int x0_zero, cudaStream_t s)
+tca_status launch_grid_cg(tca_operator *op, const void *b, void *x, int x0_zero, cudaStream_t s, bool *launched)
 {
-    if (op->dtype == TCA_F64) return launch_t<double>(op, b, x, x0_zero, s);
-    return launch_t<float>(op, b, x, x0_zero, s);
+    if (op->dtype == TCA_F64) return launch_t<double>(op, b, x, x0_zero, s, launched);
+    return launch_t<float>(op, b, x, x0_zero, s, launched);
 }
 
 }  // namespace tca

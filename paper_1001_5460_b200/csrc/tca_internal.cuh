@@ -343,7 +343,9 @@ bool tiny_cg_eligible(const tca_operator *op);
 tca_status launch_tiny_cg(const tca_operator *op, const void *b, void *x, int x0_zero, cudaStream_t s);
 // whole-solve cooperative-grid CG for mid-size problems (tca_grid.cu)
 bool grid_cg_eligible(const tca_operator *op);
-tca_status launch_grid_cg(tca_operator *op, const void *b, void *x, int x0_zero, cudaStream_t s);
+// *launched = false (TCA_OK): the blocks cannot all be co-resident on this device
+// right now; the caller runs the general engine
+tca_status launch_grid_cg(tca_operator *op, const void *b, void *x, int x0_zero, cudaStream_t s, bool *launched);
 
 // process-wide count of kernel launches issued by the library
 extern std::atomic<int64_t> g_launches;
