@@ -217,7 +217,9 @@ int tca_operator_cg_fused_step(const tca_operator *op);
  * block per SM, phases separated by grid-wide barriers, vectors L2-resident;
  * chosen when the single-block engine is not, for N <= 2^21 and n_d <= 1024
  * with the tap tables and fibre tiles in 200 KB of shared memory, single GPU,
- * not scattered, not Kronecker-sum-only; TCA_GRID=0 disables it), 0 = general
+ * not scattered, not Kronecker-sum-only; TCA_GRID=0 disables it; a solve
+ * still runs the general engine if the device cannot co-schedule every block
+ * at that moment, e.g. a shared GPU), 0 = general
  * multi-kernel engine, -1 = op NULL.  Same iterates, stop rules, guards and
  * report on every engine (readings Z1-Z3, Z10, Z12, Z28). */
 int tca_operator_cg_engine(const tca_operator *op);

@@ -122,10 +122,9 @@ __device__ __forceinline__ double block_sum(double v, double *red)
 
 // every block: the sum of the gridDim partials in a fixed order (same value
 // everywhere).  (A single-warp variant, 5 partials per lane, measured slower:
-// 21.4 vs 20.7 us per config-1 iteration.)  slot: unused (kept for the callers)
-__device__ __forceinline__ double grid_total(const double *part, double *red, int slot)
+// 21.4 vs 20.7 us per config-1 iteration.)
+__device__ __forceinline__ double grid_total(const double *part, double *red)
 {
-    (void)slot;
     double v = 0.0;
     for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) v += __ldcg(part + i);
     v = block_sum(v, red);
@@ -474,8 +473,8 @@ __global__ void __launch_bounds__(kGridThreads, 1) grid_cg_kernel(const __grid_c
     v = block_sum(bb, red);
     if (threadIdx.x == 0) part[gridDim.x + blockIdx.x] = v;
     grid_sync(a.bar);
-    double rho = grid_total(part, red, 0);
-    const double ref = a.x0_zero ? rho : grid_total(part + gridDim.x, red, 1);   // stop reference <b, b> (Z28)
+    double rho = grid_total(part, red);
+    const double ref = a.x0_zero ? rho : grid_total(part + gridDim.x, red);   // stop reference <b, b> (Z28)
     const double rho0 = rho;
     double rho_last = rho;
     int status = TCA_OK, converged = 0, iters = 0;
@@ -501,7 +500,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) grid_cg_kernel(const __grid_c
         pq = block_sum(pq, red);
         if (threadIdx.x == 0) part[blockIdx.x] = pq;
         grid_sync(a.bar);
-        pq = grid_total(part, red, 0);                        // P+*Q
+        pq = grid_total(part, red);                        // P+*Q
         if (!isfinite(pq)) { status = TCA_ERR_NONFINITE; break; }
         if (!(pq > 0.0)) { status = TCA_ERR_BREAKDOWN; break; }
         const T alpha = (T)(rho / pq);
@@ -516,7 +515,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) grid_cg_kernel(const __grid_c
         r1 = block_sum(r1, red);
         if (threadIdx.x == 0) part[gridDim.x + blockIdx.x] = r1;
         grid_sync(a.bar);
-        const double rho1 = grid_total(part + gridDim.x, red, 1);   // rho1 := R+*R
+        const double rho1 = grid_total(part + gridDim.x, red);   // rho1 := R+*R
         iters += 1;
         rho_last = rho1;
         if (lead && a.hist) a.hist[iters] = rho1;
