@@ -187,14 +187,36 @@ tca_status build_params(const tca_operator *op_c, std::vector<unsigned char> &bl
     }
     const long long whole_cost =
         tiles <= std::min<long long>(band::MAXG, (long long)op->num_sms * minb) ? p->n1 + 2 * band::KH1 : (1ll << 60);
-    // measurement switch: TCA_BAND_SCHED=whole|split forces a schedule
-    // B1' prefers whole tile columns: all CTAs advance through mode 1 together,
-    // so the halo re-reads of D and P_old hit L2 (config 3 plain apply: DRAM
-    // reads 890 -> 273 MB per launch for 10 % more time, profiles/r01_sched_probe.txt)
+    //   lock: tiles < G.  CTA t < tiles owns output slabs [0, L) of tile t; the
+    //         G - tiles tail CTAs own slabs [L, n1) of consecutive tiles.  The
+    //         main CTAs advance through mode 1 together, so the halo rows one
+    //         tile stages were staged by its neighbours moments earlier and hit
+    //         L2 (DRAM reads of the split schedule: 3.5x the algorithmic bytes,
+    //         profiles/r01_sched_probe.txt); L balances the two kinds of CTA.
+    long long lock_cost = 1ll << 60, lockL = 0, ktail = 0;
+    if (tiles < G && p->n1 >= 4 * 2 * band::KH1) {
+        const long long nt = G - tiles;
+        ktail = (tiles + nt - 1) / nt;
+        for (long long Lc = 2 * band::KH1; Lc < p->n1; ++Lc) {
+            const long long c = std::max(Lc + 2 * band::KH1, ktail * (p->n1 - Lc + 2 * band::KH1));
+            if (c < lock_cost) { lock_cost = c; lockL = Lc; }
+        }
+    }
+    // measurement switch: TCA_BAND_SCHED=whole|split|lock forces a schedule
+    // B1' prefers the mode-1-synchronous schedules (whole, lock): its halo
+    // re-reads of D and P_old then hit L2
     static const char *force = getenv("TCA_BAND_SCHED");
-    const bool want_whole = fu ? tiles <= band::MAXG
-                               : (force && tiles <= band::MAXG ? force[0] == 'w' : whole_cost < split_cost);
-    if (want_whole) {
+    char pick = whole_cost <= split_cost ? 'w' : 's';
+    // (the plain apply is bound inside the SM, not by DRAM: on config 3 lock
+    // cuts DRAM reads 893 -> 317 MB per launch but runs 286 vs 278 us, so it is
+    // picked only when strictly cheaper)
+    if (lock_cost < (pick == 'w' ? whole_cost : split_cost)) pick = 'l';
+    if (fu) pick = lock_cost <= whole_cost ? 'l' : 'w';
+    if (force && (force[0] == 'w' || force[0] == 's' || force[0] == 'l')) pick = force[0];
+    if (pick == 'w' && tiles > band::MAXG) pick = 's';
+    if (pick == 'l' && lockL == 0) pick = tiles <= band::MAXG ? 'w' : 's';
+    p->o_next = 0;
+    if (pick == 'w') {
         for (long long t = 0; t < tiles; ++t) {
             p->s_tile[t].x = (short)(t / p->tiles3);
             p->s_tile[t].y = (short)(t % p->tiles3);
@@ -202,6 +224,26 @@ tca_status build_params(const tca_operator *op_c, std::vector<unsigned char> &bl
             p->s_cnt[t] = p->n1;
         }
         grid = (int)tiles;
+    } else if (pick == 'l') {
+        const long long nt = G - tiles;
+        for (long long t = 0; t < tiles; ++t) {
+            p->s_tile[t].x = (short)(t / p->tiles3);
+            p->s_tile[t].y = (short)(t % p->tiles3);
+            p->s_o0[t] = 0;
+            p->s_cnt[t] = (int)lockL;
+        }
+        int g = (int)tiles;
+        for (long long i = 0; i < nt; ++i) {
+            const long long t0 = tiles * i / nt, t1 = tiles * (i + 1) / nt;
+            if (t1 <= t0) continue;
+            p->s_tile[g].x = (short)(t0 / p->tiles3);
+            p->s_tile[g].y = (short)(t0 % p->tiles3);
+            p->s_o0[g] = (int)lockL;
+            p->s_cnt[g] = (int)((t1 - t0) * (p->n1 - lockL));
+            ++g;
+        }
+        p->o_next = (int)lockL;
+        grid = g;
     } else {
         for (int b = 0; b < G; ++b) {
             const long long u0 = total * b / G, u1 = total * (b + 1) / G;
@@ -213,6 +255,7 @@ tca_status build_params(const tca_operator *op_c, std::vector<unsigned char> &bl
         }
         grid = G;
     }
+    op->band_sched = pick;
     p->xoff = op->ghost;
     p->nin = (int)op->nloc1 + 2 * op->ghost;
     p->off1 = L.off[0];

@@ -110,7 +110,7 @@ static __device__ unsigned long long g_b2prof[64];
 // s_cnt[b] (tile, slab) units, tile-major.  A segment takes o1 - o0 + 6 steps
 // (input slabs o0-3 .. o1+2: the mode-1 ring's ramps).
 struct Sched {
-    int t2i, t3i, o0, cnt, n1, tiles3;
+    int t2i, t3i, o0, cnt, n1, tiles3, o_next;
     __device__ bool next(int &a2, int &a3, int &s0, int &s1)
     {
         if (cnt <= 0) return false;
@@ -119,7 +119,7 @@ struct Sched {
         cnt -= s1 - s0;
         a2 = t2i * T2;
         a3 = t3i * T3;
-        o0 = 0;
+        o0 = o_next;
         t3i = (t3i + 1 == tiles3) ? 0 : t3i + 1;
         t2i += (t3i == 0) ? 1 : 0;
         return true;
@@ -316,7 +316,7 @@ band3_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict_
     const int dbg = TCA_BAND_DBG ? a.dbg : 0;   // phase switches (measurement only): 1 AB, 2 C compute off
 
     const Sched sc0{a.s_tile[blockIdx.x].x, a.s_tile[blockIdx.x].y, a.s_o0[blockIdx.x], a.s_cnt[blockIdx.x], a.n1,
-                    a.tiles3};
+                    a.tiles3, a.o_next};
     int gtot = 0;   // pipeline steps of this CTA
     {
         Sched t = sc0;

@@ -80,6 +80,7 @@ struct ParamsBase {
     int off3, off2, off1;     // record offsets (rows) of the mode-3/2/1 tables; mode 4 at 0
     int dbg;                  // phase switches for bisecting (TCA_BAND_DEBUG; 0 in production)
     int onebox;               // 1: a slab is ONE 4-D TMA box (Cfg::ONEBOX and n3 n4 % UNIT == 0)
+    int o_next;               // first output slab of a CTA's second and later tiles (0; lockstep tails: L)
     short2 s_tile[MAXG];   // CTA b starts at tile (x = mode-2 tile, y = mode-3 tile) ...
     int s_o0[MAXG];        // ... at output slab s_o0 ...
     int s_cnt[MAXG];       // ... and processes s_cnt (tile, slab) units
@@ -168,7 +169,12 @@ struct Cfg {
     // pass B: each warp covers whole mode-2 rows of the block (RPW rows of N4
     // lanes) so its 32 lanes never put three rows on one bank pair of the
     // 128-B-aligned (TMA) slab rows
-    static constexpr int RPW = (32 / N4 < T2) ? (32 / N4 > 0 ? 32 / N4 : 1) : T2;
+    // rows start at lane multiples of LW (N4 rounded up to a power of two): each
+    // half-warp phase of a 64-bit access then covers one row of N4 consecutive
+    // elements, bank-conflict-free at any row pitch (with rows packed at stride
+    // N4 the phase that straddles two rows conflicted: profiles/r03_smem_wavefronts.txt)
+    static constexpr int LW = N4 <= 1 ? 1 : N4 <= 2 ? 2 : N4 <= 4 ? 4 : N4 <= 8 ? 8 : N4 <= 16 ? 16 : 32;
+    static constexpr int RPW = (32 / LW < T2) ? 32 / LW : T2;
     static constexpr int WPB = (T2 + RPW - 1) / RPW;  // warps per block
     static_assert(N4 <= 32, "pass B lane map");
     static constexpr size_t al(size_t e) { return (e * sizeof(T) + 127) / 128 * 128 / sizeof(T); }
@@ -181,18 +187,26 @@ struct Cfg {
     // memory wavefronts for the two warp access patterns that read these
     // buffers -- pass B lanes (RPW mode-2 rows x N4) and pass C lanes
     // (32 / T3 mode-2 rows x T3 columns of stride N4) -- counted per 4-byte bank
+    // shared-memory wavefronts of one warp access: 64-bit accesses are served per
+    // half-warp phase (lanes 0-15, 16-31), each phase costing the largest number
+    // of words one 4-byte bank holds; 32-bit accesses as one phase
     static constexpr int wavefronts(int X, int pass)
     {
-        int cnt[32] = {};   // words per 4-byte bank (the lanes' addresses are all distinct)
-        int worst = 0;
-        for (int l = 0; l < 32; ++l) {
-            if (pass == 0 && l >= RPW * N4) continue;
-            const int idx = pass == 0 ? (l / N4) * X + l % N4        // pass B
-                                      : (l / T3) * X + (l % T3) * S3;  // pass C
-            for (int h = 0; h < (int)sizeof(T) / 4; ++h) ++cnt[(idx * ((int)sizeof(T) / 4) + h) % 32];
+        constexpr int PH = sizeof(T) == 8 ? 16 : 32;   // lanes per phase
+        int total = 0;
+        for (int p0 = 0; p0 < 32; p0 += PH) {
+            int cnt[32] = {};   // words per 4-byte bank (the lanes' addresses are all distinct)
+            int worst = 0;
+            for (int l = p0; l < p0 + PH; ++l) {
+                if (pass == 0 && (l >= RPW * LW || l % LW >= N4)) continue;
+                const int idx = pass == 0 ? (l / LW) * X + l % LW        // pass B
+                                          : (l / T3) * X + (l % T3) * S3;  // pass C
+                for (int h = 0; h < (int)sizeof(T) / 4; ++h) ++cnt[(idx * ((int)sizeof(T) / 4) + h) % 32];
+            }
+            for (int b = 0; b < 32; ++b) worst = cnt[b] > worst ? cnt[b] : worst;
+            total += worst;
         }
-        for (int b = 0; b < 32; ++b) worst = cnt[b] > worst ? cnt[b] : worst;
-        return worst;
+        return total;
     }
     static constexpr int pick_wip()
     {
@@ -578,8 +592,8 @@ __device__ __forceinline__ void pass_b(const PA &a, const T *U2, const T *RA, co
         }
         constexpr int h0b = B * C::BL;
         const int r3 = __shfl_sync(0xffffffffu, a.off3 + a3 + h0b, 0);   // uniform table row base (all lanes)
-        if (lane >= C::RPW * N4) return;
-        const int i2 = (warp % C::WPB) * C::RPW + lane / N4, i4 = lane % N4;
+        if (lane >= C::RPW * C::LW || lane % C::LW >= N4) return;
+        const int i2 = (warp % C::WPB) * C::RPW + lane / C::LW, i4 = lane % C::LW;
         if (i2 >= T2) return;
         constexpr int h0 = B * C::BL;
         const T *u2 = U2 + i2 * C::WP + h0 * C::S3 + i4;
@@ -703,7 +717,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
     unsigned gi = 0, gc = 0;   // slabs issued / consumed (stage = g % NSTAGE, parity (g / NSTAGE) & 1)
     T acc[6][E];
     double pq = 0.0;           // <x, y> partial of this thread's emitted outputs
-    for (; cnt > 0; o0 = 0, t3i = (t3i + 1 == a.tiles3) ? 0 : t3i + 1, t2i += (t3i == 0) ? 1 : 0) {
+    for (; cnt > 0; o0 = a.o_next, t3i = (t3i + 1 == a.tiles3) ? 0 : t3i + 1, t2i += (t3i == 0) ? 1 : 0) {
         const int o1 = (a.n1 - o0 < cnt) ? a.n1 : o0 + cnt;
         cnt -= o1 - o0;
         const int a2 = __shfl_sync(0xffffffffu, t2i * T2, 0);   // provably warp-uniform

@@ -148,6 +148,7 @@ struct tca_operator {
     std::vector<double> bandG[tca::kD];
     std::vector<double> bandR[tca::kD];
     std::vector<unsigned char> band_params;   // prebuilt kernel-parameter block (tap tables)
+    char band_sched = 0;                      // schedule of the last band-apply parameter build: w(hole) / s(plit) / l(ock)
     int band_gt = 0;                          // tap tables: 0 block; global (band_gtaps) with modes 4 (1) or 4+3 (2) in the block
     void *band_gtaps = nullptr;
     size_t band_gtaps_bytes = 0;
