@@ -206,6 +206,17 @@ tca_status tca_operator_create_scattered(tca_operator **op, int order,
  * (no CG solve so far) or op NULL.  Results are the same iterates either way. */
 int tca_operator_cg_fused_step(const tca_operator *op);
 
+/* Whether CG / PCG solves on this operator defer the x update of Fig. 2
+ * (C := C + alpha P) into the next iteration's operator
+ * apply, where one extra warp per CTA streams it beside the banded apply
+ * (DESIGN.md 6.5): the iteration's vector kernels then move 6 words per
+ * unknown (R := R - alpha Q; P_next := R|Z + beta P into a second P buffer)
+ * instead of 8.  Same arithmetic, same iterates.  Default on for fp32 fused
+ * operators on one GPU (the extra warp costs no occupancy there), off for fp64
+ * (its apply would lose registers); TCA_DX=1|0 in the environment at the first
+ * solve forces it.  1 = yes, 0 = no, -1 = not decided yet or op NULL. */
+int tca_operator_cg_deferred_x(const tca_operator *op);
+
 /* Which engine tca_cg_solve uses on this operator: 1 = single-block engine
  * (tca_tiny.cu: the whole Fig. 2 solve, in ONE kernel launch
  * by one 1024-thread block: p and two apply temporaries in shared memory, x,

@@ -689,6 +689,24 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
         }
         return TCA_OK;   // C and P are updated by the next step's B1' (or b1_finish)
     }
+    if (op->dx == 1) {   // deferred C update: Q := A*P, P+*Q, C += alpha_prev P_prev in the apply (MODE 2)
+        T *pc = (T *)(op->pcur ? op->p2 : op->p_own), *pp = (T *)(op->pcur ? op->p_own : op->p2);
+        TCA_TRY(timed_call(op, s, [&] { return launch_fused_dx(op, pc, q, x, pp, op->part, s); }));
+        TCA_TRY(cg_reduce(op, 1, op->part, op->band_grid_dx, s));   // alpha
+        launch_cg_update_r<T>(r, q, op->N, op->sc, op->part, s);     // R := R - alpha*Q, R+*R
+        TCA_TRY(cg_reduce(op, 2, op->part, kRedBlocks, s));          // rho1 (PCG: R+*R), stop, beta
+        const T *d = r;
+        if (op->solver == 1) {
+            T *z = (T *)op->z;
+            TCA_TRY(apply_precond<T>(op, r, z, done, s));            // Z := P^-1 R
+            launch_dot_partials<T>(r, z, op->N, op->part, done, s);  // R+*Z
+            TCA_TRY(cg_reduce(op, 3, op->part, kRedBlocks, s));      // rho1, beta
+            d = z;
+        }
+        launch_cg_update_p<T>(pp, pc, d, op->N, op->sc, s);          // P_next := R|Z + beta*P (other buffer)
+        op->pcur ^= 1;
+        return TCA_OK;   // C += alpha P: by the next apply (or after the loop)
+    }
     static const bool no_fused_dot = getenv("TCA_NO_FUSED_DOT") != nullptr;   // measurement switch
     if (fused_used(op, pe, q) && !no_fused_dot) {
         TCA_TRY(timed_apply(op, pe, q, done, s, op->part));           // Q := A*(P*D), P+*Q in the epilogue
@@ -930,6 +948,8 @@ static tca_status cg_run(tca_operator *op, const T *b, T *x, double rtol, int32_
     }
     if (op->b1 == 1)   // the last step's pending C := C + alpha P (x only: done is set)
         launch_cg_update_xp<T>(x, (T *)(op->pcur ? op->p2 : op->p_own), (const T *)op->r, op->N, op->sc, s);
+    if (op->dx == 1)   // the last iteration's pending C := C + alpha P (its P: the buffer before the flip)
+        launch_cg_update_xp<T>(x, (T *)(op->pcur ? op->p_own : op->p2), (const T *)op->r, op->N, op->sc, s);
     return TCA_OK;
 }
 
@@ -954,9 +974,24 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
             if (e != cudaSuccess) { op->b1 = 0; cudaGetLastError(); }
         }
     }
-    const int b1_saved = op->b1;
+    if (op->dx < 0) {   // deferred C update in the apply: default on for fp32 (TCA_DX=0|1 forces)
+        const char *e = getenv("TCA_DX");
+        const bool want = (e && (e[0] == '0' || e[0] == '1') ? e[0] == '1' : op->dtype == TCA_F32) && op->b1 != 1;
+        op->dx = (want && !op->transport && fused_used(op, op->p_own, op->q) && fused_dx_supported(op)) ? 1 : 0;
+        if (op->dx == 1 && !op->p2) {
+            cudaError_t e2 = cudaMallocAsync(&op->p2, (size_t)op->N * op->esize, s);
+            if (e2 != cudaSuccess) { op->dx = 0; cudaGetLastError(); }
+        }
+    }
+    const int b1_saved = op->b1, dx_saved = op->dx;
     if (pcg == 2 || pcg == 3 || tiny || gridc) op->b1 = 0;   // single-reduction CG, Jacobi, whole-solve engines: own steps
+    if (pcg == 2 || pcg == 3 || tiny || gridc || op->b1 == 1) op->dx = 0;
     op->pcur = 0;
+    if (op->dx == 1) {
+        const void *ptrs[3] = {op->p_own, op->p2, op->q};
+        const int kinds[3] = {0, 0, 1};
+        TCA_TRY(fused_dx_prepare(op, ptrs, kinds, 3, s));
+    }
     if (op->b1 == 1) {
         const void *ptrs[4] = {op->p_own, op->p2, pcg == 1 ? op->z : op->r, op->q};
         const int kinds[4] = {0, 0, 0, 1};
@@ -972,6 +1007,7 @@ static tca_status cg_t(tca_operator *op, const T *b, T *x, double rtol, int32_t 
         if (!launched) TCA_TRY(cg_run<T>(op, b, x, rtol, max_iters, h, s, pcg, x0_zero));
     }
     op->b1 = b1_saved;
+    op->dx = dx_saved;
     TCA_CUDA_TRY(cudaGetLastError());
     TCA_CUDA_TRY(cudaEventRecord(op->ev1, s));
     if (rep) {   // true residual |b - M x_k| / |b| (reading Z2): one more apply, after the timed solve
@@ -1438,6 +1474,8 @@ tca_status tca_operator_query(const tca_operator *op, int64_t *own_lo, int64_t *
 int tca_operator_apply_path(const tca_operator *op) { return op ? op->apply_path : -1; }
 
 int tca_operator_cg_fused_step(const tca_operator *op) { return op ? op->b1 : -1; }
+
+int tca_operator_cg_deferred_x(const tca_operator *op) { return op ? op->dx : -1; }
 
 int tca_operator_cg_engine(const tca_operator *op)
 {

@@ -50,6 +50,12 @@ extern template tca_status launch_dispatch_fu<Params<double>>(const tca_operator
 extern template tca_status launch_dispatch_fu<Params<float>>(const tca_operator *, const Params<float> &,
                                                              cudaStream_t, const CUtensorMap *, const CUtensorMap *,
                                                              const CUtensorMap *, const FuArgs<float> &);
+extern template tca_status launch_dispatch_dx<Params<double>>(const tca_operator *, const Params<double> &,
+                                                              cudaStream_t, const CUtensorMap *, const CUtensorMap *,
+                                                              const FuArgs<double> &);
+extern template tca_status launch_dispatch_dx<Params<float>>(const tca_operator *, const Params<float> &,
+                                                             cudaStream_t, const CUtensorMap *, const CUtensorMap *,
+                                                             const FuArgs<float> &);
 extern template int fu_ok_for<double>(int);
 extern template int fu_ok_for<float>(int);
 }  // namespace band
@@ -589,6 +595,77 @@ tca_status launch_fused_b1(const tca_operator *op, const void *pold, void *pnew,
 {
     if (op->dtype == TCA_F64) return launch_b1_t<double>(op, pold, pnew, d, q, x, pq_part, s);
     return launch_b1_t<float>(op, pold, pnew, d, q, x, pq_part, s);
+}
+
+// Apply with the deferred C update (MODE 2): q = A p and the
+// per-CTA <p, q> partials (op->band_grid_dx entries), and C += alpha P_prev by
+// a streaming warp when sc->xupd (sc->done: only that update).  One GPU,
+// parameter-block tables; the mode-1-synchronous schedule of B1' (lock/whole).
+bool fused_dx_supported(const tca_operator *op)
+{
+    if (op->band_v2) return false;
+    if (op->ghost != 0 || op->band_gt || op->band_params.empty()) return false;
+    return true;
+}
+
+tca_status fused_dx_prepare(const tca_operator *op_c, const void *const *ptrs, const int *kinds, int n, cudaStream_t s)
+{
+    tca_operator *op = const_cast<tca_operator *>(op_c);
+    if (op->band_params_dx.empty()) {
+        if (op->dtype == TCA_F64) TCA_TRY(build_params<double>(op, op->band_params_dx, op->band_grid_dx, true));
+        else TCA_TRY(build_params<float>(op, op->band_params_dx, op->band_grid_dx, true));
+        if (op->band_params_dx.empty()) return fail(TCA_ERR_INVALID_ARG, "deferred-x apply: tables not in block");
+    }
+    for (int i = 0; i < n; ++i) {
+        tca_status st = TCA_OK;
+        int slot = 0;
+        if (!cached_tmap(op, ptrs[i], kinds[i], s, &st, &slot)) return st;
+        TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[slot], s));
+    }
+    return TCA_OK;
+}
+
+namespace {
+template <typename T>
+tca_status launch_dx_t(const tca_operator *op_c, const void *p, void *q, void *x, const void *pprev,
+                       double *pq_part, cudaStream_t s)
+{
+    tca_operator *op = const_cast<tca_operator *>(op_c);
+    if (op->band_params_dx.empty()) return fail(TCA_ERR_INVALID_ARG, "deferred-x apply: not prepared");
+    tca_status st = TCA_OK;
+    int ps = 0, qs = 0;
+    const CUtensorMap *pm = cached_tmap(op, p, 0, s, &st, &ps);
+    if (!pm) return st;
+    const CUtensorMap *qm = cached_tmap(op, q, 1, s, &st, &qs);
+    if (!qm) return st;
+    auto *prm = reinterpret_cast<band::Params<T> *>(op->band_params_dx.data());
+    prm->x = (const T *)p;
+    prm->y = (T *)q;
+    prm->done = &op->sc->done;
+    prm->pq_part = pq_part;
+    {
+        static const char *e = getenv("TCA_BAND_DEBUG");   // measurement switches (results invalid)
+        prm->dbg = e ? atoi(e) : 0;
+    }
+    const band::FuArgs<T> fa{(T *)x, (T *)const_cast<void *>(pprev), op->sc};
+    TCA_TRY(band::launch_dispatch_dx(op, *prm, s, pm, qm, fa));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TCA_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) {
+        op->tmap_pinned |= (1u << ps) | (1u << qs);
+    } else {
+        TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[ps], s));
+        TCA_CUDA_TRY(cudaEventRecord(op->tmap_ev[qs], s));
+    }
+    return TCA_OK;
+}
+}  // namespace
+
+tca_status launch_fused_dx(const tca_operator *op, const void *p, void *q, void *x, const void *pprev,
+                           double *pq_part, cudaStream_t s)
+{
+    if (op->dtype == TCA_F64) return launch_dx_t<double>(op, p, q, x, pprev, pq_part, s);
+    return launch_dx_t<float>(op, p, q, x, pprev, pq_part, s);
 }
 
 bool fused_pointers_ok(const void *x, const void *y)

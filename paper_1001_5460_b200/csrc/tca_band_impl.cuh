@@ -646,15 +646,100 @@ __device__ __forceinline__ float4 v_axpy(float4 y, float a, float4 x)
     return make_float4(fmaf(a, x.x, y.x), fmaf(a, x.y, y.y), fmaf(a, x.z, y.z), fmaf(a, x.w, y.w));
 }
 
-template <typename T, int N4, typename PA, bool FU>
-__global__ void __launch_bounds__(Cfg<T, N4>::NTHR, Cfg<T, N4>::MINB)
+// Deferred C update (MODE 2): one extra warp per CTA streams
+// C := C + alpha P_prev over the CTA's share of the vector while the other
+// NTHR threads apply the operator.  P_prev is the previous iteration's search
+// direction (kept in the other buffer of a ping-pong pair) and alpha its step
+// (sc->alpha, valid when sc->xupd): the x update of Fig. 2
+// executed one iteration late, so the apply -- bound inside the SM, its DRAM
+// traffic a fraction of the peak -- carries the 3 words of the x update that
+// the vector kernels otherwise add to every iteration.  Loads: 16-B vectors,
+// XU of C and of P_prev in flight per lane (the DRAM latency is hidden by
+// the outstanding loads, not by other warps).
+__device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Deferred C update (MODE 2): one extra warp per CTA streams
+// C := C + alpha P_prev over the CTA's share of the vector while the other
+// NTHR threads apply the operator.  P_prev is the previous iteration's search
+// direction (the other buffer of a ping-pong pair) and alpha its step
+// (sc->alpha, valid when sc->xupd): the x update of Fig. 2
+// executed one iteration late, so the apply -- bound inside the SM, its DRAM
+// traffic a fraction of the peak -- carries the 3 words of the x update that
+// the vector kernels otherwise add to every iteration.  Chunks of the share are
+// bulk-prefetched into L2 two ahead of their 16-B loads (XU vectors of C and of
+// P_prev in flight per lane).  Used where the extra warp costs no occupancy
+// (fp32: 95 registers; fp64's 116-register body would be cut to 96 and spill).
+template <typename T>
+__device__ __forceinline__ void x_stream(const FuArgs<T> &f, size_t n, int lane)
+{
+    if (!f.sc->xupd) return;   // no valid alpha: first iteration, or the solve stopped earlier
+    const T alpha = (T)f.sc->alpha;
+    using V = typename V16<T>::V;
+    constexpr int VW = 16 / (int)sizeof(T);
+    constexpr int XU = 8;
+    constexpr int CH = 32 * XU * 4;   // vectors per chunk
+    const size_t nv = n / VW;
+    const size_t v0 = nv * blockIdx.x / gridDim.x, v1 = nv * (blockIdx.x + 1) / gridDim.x;
+    V *xv = reinterpret_cast<V *>(f.x);
+    const V *pv = reinterpret_cast<const V *>(f.pn);
+    auto pf = [&](size_t c0) {
+        if (lane == 0 && c0 < v1) {
+            const size_t c1 = c0 + CH < v1 ? c0 + CH : v1;
+            prefetch_l2(xv + c0, (unsigned)((c1 - c0) * 16));
+            prefetch_l2(pv + c0, (unsigned)((c1 - c0) * 16));
+        }
+    };
+    pf(v0);
+    pf(v0 + CH);
+    for (size_t c = v0; c < v1; c += CH) {
+        pf(c + 2 * CH);
+        const size_t ce = c + CH < v1 ? c + CH : v1;
+        size_t i = c + lane;
+        for (; i + (XU - 1) * 32 < ce; i += XU * 32) {
+            V xr[XU], pr[XU];
+#pragma unroll
+            for (int u = 0; u < XU; ++u) {
+                xr[u] = __ldcs(xv + i + u * 32);
+                pr[u] = __ldcs(pv + i + u * 32);
+            }
+#pragma unroll
+            for (int u = 0; u < XU; ++u) __stcs(xv + i + u * 32, v_axpy(xr[u], alpha, pr[u]));
+        }
+        for (; i < ce; i += 32) __stcs(xv + i, v_axpy(__ldcs(xv + i), alpha, __ldcs(pv + i)));
+    }
+    if (blockIdx.x == 0)   // scalar tail
+        for (size_t k = nv * VW + lane; k < n; k += 32) f.x[k] = fma(alpha, f.pn[k], f.x[k]);
+}
+
+// CTA barrier of the NTHR operator threads (MODE 2: the streaming warp does not take part)
+template <int MODE, int NTHR>
+__device__ __forceinline__ void cta_sync()
+{
+    if constexpr (MODE == 2) asm volatile("bar.sync 1, %0;\n" ::"n"(NTHR) : "memory");
+    else __syncthreads();
+}
+
+// MODE: 0 the apply; 1 the fused CG step B1' (FuArgs: C, P_new); 2 the apply
+// with the deferred C update (an extra streaming warp; FuArgs: C, P_prev as pn)
+template <typename T, int N4, typename PA, int MODE>
+__global__ void __launch_bounds__(Cfg<T, N4>::NTHR + (MODE == 2 ? 32 : 0), Cfg<T, N4>::MINB)
 band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict__ ymp,
                   const __grid_constant__ PA a, const CUtensorMap *__restrict__ rmp, const __grid_constant__ FuArgs<T> f)
 {
     using C = Cfg<T, N4>;
+    constexpr bool FU = MODE == 1;
     constexpr int W = C::W, WI = C::WI, PP = C::PP, T3 = C::T3, E = C::E, NTHR = C::NTHR;
     constexpr int NS = FU ? C::NSTAGE_FU : C::NSTAGE;   // input stages
     const int dbg = TCA_BAND_DBG ? a.dbg : 0;   // phase switches (measurement builds only)
+    if constexpr (MODE == 2) {
+        if (threadIdx.x >= NTHR) {   // the streaming warp
+            if (!(dbg & 4096)) x_stream<T>(f, (size_t)a.n1 * a.n2 * a.n3 * N4, threadIdx.x & 31);
+            return;
+        }
+    }
     if constexpr (FU) {
         if (*a.done) {   // stopped: only the pending C := C + alpha P_old of the last iteration
             if (f.sc->xupd) {
@@ -704,7 +789,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    __syncthreads();
+    cta_sync<MODE, NTHR>();
     if (dbg & 32) return;
 
     const int seg = tid / (NTHR / C::NSEG);   // warp-uniform
@@ -887,7 +972,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
                 }
                 if (j + 1 < o1) fetch_x(j + 1);
             }
-            __syncthreads();   // bar1: U2/RA complete; all threads finished slab j-1
+            cta_sync<MODE, NTHR>();   // bar1: U2/RA complete; all threads finished slab j-1
 
             if (pending >= 0) {   // uniform: every thread tracks the same pending slab
                 if (tid == 0 && !(dbg & (1 | 256))) {
@@ -915,7 +1000,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             }
             // ---- pass B: G3 on U2, lambda R3 on p (8 outputs along i3 per item; item = warp)
             if (live && !(dbg & 4)) pass_b<T, N4, 0, PA>(a, U2, RA, P, U3, RB, a3, warp, lane);
-            __syncthreads();   // bar2: U3/RB complete
+            cta_sync<MODE, NTHR>();   // bar2: U3/RB complete
 
             // ---- pass C + mode-1 ring + emission of output slab j-3
             const bool emit = (j - 3 >= o0) && (j - 3 < o1);
@@ -928,7 +1013,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             if (live) ++gc;
             rot = rot == 5 ? 0 : rot + 1;
         }
-        __syncthreads();
+        cta_sync<MODE, NTHR>();
         if (!FU && pending >= 0) {
             if (tid == 0 && !(dbg & (1 | 256))) {
                 if constexpr (C::PADDED) tma_store_4d(ymp, OUTB + ((pending + 3) & 1) * C::OUTE, 0, a3, a2, pending);
@@ -939,7 +1024,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
         }
         if (!FU) {
             if (tid == 0) bulk_wait<0>();   // the next segment rewrites the staging buffers
-            __syncthreads();
+            cta_sync<MODE, NTHR>();
         }
     }
     if (a.pq_part) {   // fixed-order CTA reduction of the <x, y> partials (deterministic)
@@ -947,7 +1032,7 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) pq += __shfl_xor_sync(0xffffffffu, pq, o);
         if (lane == 0) red[warp] = pq;
-        __syncthreads();
+        cta_sync<MODE, NTHR>();
         if (tid == 0) {
             double t = 0.0;
             for (int w = 0; w < NTHR / 32; ++w) t += red[w];
@@ -957,19 +1042,21 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
 }
 
 // ---------------------------------------------------------------- host side
-template <typename T, int N4, typename PA, bool FU>
+template <typename T, int N4, typename PA, int MODE>
 tca_status launch_n4(const tca_operator *op, const PA &prm, cudaStream_t s, const CUtensorMap *xm,
                      const CUtensorMap *ym, const CUtensorMap *rm, const FuArgs<T> &fa)
 {
     using C = Cfg<T, N4>;
+    constexpr bool FU = MODE == 1;
     if constexpr (FU && !C::FU_OK) {
         return fail(TCA_ERR_INVALID_ARG, "fused CG step: shape does not fit shared memory");
     } else {
         constexpr size_t smem = FU ? C::smem_fu : C::smem_bytes;
-        TCA_TRY(set_max_dynamic_smem((const void *)band_apply_kernel<T, N4, PA, FU>, smem));
+        TCA_TRY(set_max_dynamic_smem((const void *)band_apply_kernel<T, N4, PA, MODE>, smem));
         count_launch();
-        band_apply_kernel<T, N4, PA, FU>
-            <<<(unsigned)(FU ? op->band_grid_fu : op->band_grid), C::NTHR, smem, s>>>(xm, ym, prm, rm, fa);
+        const int grid = MODE == 1 ? op->band_grid_fu : MODE == 2 ? op->band_grid_dx : op->band_grid;
+        band_apply_kernel<T, N4, PA, MODE>
+            <<<(unsigned)grid, C::NTHR + (MODE == 2 ? 32 : 0), smem, s>>>(xm, ym, prm, rm, fa);
         TCA_CUDA_TRY(cudaGetLastError());
         return TCA_OK;
     }
@@ -1093,7 +1180,7 @@ tca_status launch_dispatch(const tca_operator *op, const PA &prm, cudaStream_t s
     const FuArgs<T> none{};
     switch ((int)op->n[3]) {
 #define TCA_CASE(n) \
-    case n: return launch_n4<T, n, PA, false>(op, prm, s, xm, ym, nullptr, none);
+    case n: return launch_n4<T, n, PA, 0>(op, prm, s, xm, ym, nullptr, none);
         TCA_BAND_N4_LIST(TCA_CASE)
 #undef TCA_CASE
     }
@@ -1108,7 +1195,22 @@ tca_status launch_dispatch_fu(const tca_operator *op, const PA &prm, cudaStream_
     using T = typename PA::value_type;
     switch ((int)op->n[3]) {
 #define TCA_CASE(n) \
-    case n: return launch_n4<T, n, PA, true>(op, prm, s, xm, ym, rm, fa);
+    case n: return launch_n4<T, n, PA, 1>(op, prm, s, xm, ym, rm, fa);
+        TCA_BAND_N4_LIST(TCA_CASE)
+#undef TCA_CASE
+    }
+    return fail(TCA_ERR_INVALID_ARG, "band apply: unsupported n4");
+}
+
+// apply with the deferred C update (MODE 2): fa = {C, P_prev, scalars}
+template <typename PA>
+tca_status launch_dispatch_dx(const tca_operator *op, const PA &prm, cudaStream_t s, const CUtensorMap *xm,
+                              const CUtensorMap *ym, const FuArgs<typename PA::value_type> &fa)
+{
+    using T = typename PA::value_type;
+    switch ((int)op->n[3]) {
+#define TCA_CASE(n) \
+    case n: return launch_n4<T, n, PA, 2>(op, prm, s, xm, ym, nullptr, fa);
         TCA_BAND_N4_LIST(TCA_CASE)
 #undef TCA_CASE
     }

@@ -17,4 +17,11 @@ bool fused_b1_supported(const tca_operator *op);
 tca_status fused_b1_prepare(const tca_operator *op, const void *const *ptrs, const int *kinds, int n, cudaStream_t s);
 tca_status launch_fused_b1(const tca_operator *op, const void *pold, void *pnew, const void *d, void *q, void *x,
                            double *pq_part, cudaStream_t s);
+// Apply with the deferred C update (one GPU): Q = A P, per-CTA <P, Q> partials
+// (op->band_grid_dx), C += alpha P_prev by a streaming warp when sc->xupd
+// (sc->done: only that update).
+bool fused_dx_supported(const tca_operator *op);
+tca_status fused_dx_prepare(const tca_operator *op, const void *const *ptrs, const int *kinds, int n, cudaStream_t s);
+tca_status launch_fused_dx(const tca_operator *op, const void *p, void *q, void *x, const void *pprev,
+                           double *pq_part, cudaStream_t s);
 }  // namespace tca

@@ -718,7 +718,7 @@ tca_status launch_t(tca_operator *op, const void *b, void *x, int x0_zero, cudaS
 
 bool grid_cg_eligible(const tca_operator *op)
 {
-    static const char *e = getenv("TCA_GRID");   // measurement switch: TCA_GRID=0 keeps the general path
+    const char *e = getenv("TCA_GRID");   // read per call: tests pin the general path per operator   // measurement switch: TCA_GRID=0 keeps the general path
     if (e && e[0] == '0') return false;
     if (op->transport || op->scat || op->apply_path == 2 || op->order < 1) return false;
     if (op->N > (int64_t)1 << 21) return false;   // vectors stay L2-resident (8 x 16 MB fp64)

@@ -214,6 +214,9 @@ struct tca_operator {
     // by neighbouring CTAs while P_new is written)
     std::vector<unsigned char> band_params_fu;
     int band_grid_fu = 0;
+    std::vector<unsigned char> band_params_dx;   // apply with the deferred C update (MODE 2)
+    int band_grid_dx = 0;
+    int dx = -1;                         // deferred C update in the apply: -1 not decided, 0 off, 1 on
     int b1 = -1;                         // -1: not decided, 0: off, 1: on
     void *p2 = nullptr;                  // second P buffer
     int pcur = 0;                        // 0: P in p_own, 1: P in p2
@@ -325,6 +328,8 @@ template <typename T>
 void launch_resid2(const T *b, const T *q, T *r, T *p, int64_t N, double *part_dd, double *part_bb, cudaStream_t s);
 template <typename T>
 void launch_cg_update_xp(T *x, T *p, const T *r, int64_t N, const CgScalars *sc, cudaStream_t s);
+template <typename T>
+void launch_cg_update_p(T *pn, const T *p, const T *d, int64_t N, const CgScalars *sc, cudaStream_t s);
 
 // finalisers (one block): 0 = init rho, 1 = pq -> alpha, 2 = rr -> beta/stop,
 // 8 = stop reference <b, b> of a warm start (stage 1 only: red[8], red[9] for the report)

@@ -989,6 +989,29 @@ cg_update_xp_kernel(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ 
     }
 }
 
+// P_next := D + beta*P (D = R, or Z in PCG) into the other buffer of the P
+// pair, unless the solve stopped at this iteration (3 words).  The x update of
+// this iteration is deferred to the next apply (MODE 2 of the band apply),
+// which still reads P from its own buffer.
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+cg_update_p_kernel(T *__restrict__ pn, const T *__restrict__ p, const T *__restrict__ d, int64_t N, const CgScalars *sc)
+{
+    if (sc->done) return;
+    using V = typename Vec<T>::V;
+    constexpr int VW = Vec<T>::W;
+    const T beta = (T)sc->beta;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    int64_t nv = 0;
+    if (aligned16(pn) && aligned16(p) && aligned16(d)) {
+        nv = N / VW;
+        V *pnv = reinterpret_cast<V *>(pn);
+        const V *pv = reinterpret_cast<const V *>(p), *dv = reinterpret_cast<const V *>(d);
+        for (int64_t i = tid; i < nv; i += nth) __stcs(pnv + i, vaxpy(__ldcs(dv + i), beta, __ldcs(pv + i)));
+    }
+    for (int64_t i = nv * VW + tid; i < N; i += nth) pn[i] = d[i] + beta * p[i];
+}
+
 // Single-reduction CG (Chronopoulos-Gear, reading Z24): one
 // streaming pass per iteration before the apply,
 //   P := R + beta*P;  S := W + beta*S;  C := C + alpha*P;  R := R - alpha*S
@@ -1065,6 +1088,13 @@ void launch_cg_update_r(T *r, const T *q, int64_t N, const CgScalars *sc, double
 {
     count_launch();
     cg_update_r_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, q, N, sc, part);
+}
+
+template <typename T>
+void launch_cg_update_p(T *pn, const T *p, const T *d, int64_t N, const CgScalars *sc, cudaStream_t s)
+{
+    count_launch();
+    cg_update_p_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(pn, p, d, N, sc);
 }
 
 template <typename T>
@@ -1407,6 +1437,8 @@ void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc
                                         double *, cudaStream_t);                          \
     template void launch_cg_update_xp<T>(T *, T *, const T *, int64_t, const CgScalars *, \
                                          cudaStream_t);                                   \
+    template void launch_cg_update_p<T>(T *, const T *, const T *, int64_t,               \
+                                        const CgScalars *, cudaStream_t);                 \
     template void launch_cgsr_update<T>(T *, T *, T *, T *, const T *, int64_t,            \
                                         const CgScalars *, double *, cudaStream_t);       \
     template void launch_ksum_apply<T>(const T *, T *, int64_t, const int64_t *, const T *, \

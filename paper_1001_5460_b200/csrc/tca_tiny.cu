@@ -385,7 +385,7 @@ tca_status launch_t(const tca_operator *op, const void *b, void *x, int x0_zero,
 
 bool tiny_cg_eligible(const tca_operator *op)
 {
-    static const char *e = getenv("TCA_TINY");   // measurement switch: TCA_TINY=0 keeps the general path
+    const char *e = getenv("TCA_TINY");   // read per call: tests pin the general path per operator   // measurement switch: TCA_TINY=0 keeps the general path
     if (e && e[0] == '0') return false;
     if (op->transport || op->scat || op->apply_path == 2 || op->order < 1) return false;
     const int E = tiny_e(op);

@@ -29,7 +29,7 @@ EXPORTED = ["tca_operator_create", "tca_operator_query", "tca_apply", "tca_rhs",
             "tca_cg_solve", "tca_solve_host", "tca_solve_host_batch", "tca_operator_destroy", "tca_generate_normal",
             "tca_forward_model", "tca_status_string", "tca_last_error", "tca_version",
             "tca_operator_set_timing", "tca_operator_get_timing", "tca_kernel_launches",
-            "tca_operator_apply_path", "tca_operator_cg_engine", "tca_operator_cg_fused_step", "tca_operator_create_scattered", "tca_shard_layout", "tca_nccl_get_unique_id",
+            "tca_operator_apply_path", "tca_operator_cg_engine", "tca_operator_cg_fused_step", "tca_operator_cg_deferred_x", "tca_operator_create_scattered", "tca_shard_layout", "tca_nccl_get_unique_id",
             "tca_nccl_comm_create", "tca_nccl_comm_destroy", "tca_local_group_create",
             "tca_local_group_destroy", "tca_pcg_solve", "tca_precond_apply", "tca_precond_info",
             "tca_cgsr_solve", "tca_operator_create_gram", "tca_jacobi_solve"]
@@ -103,6 +103,8 @@ _lib.tca_operator_apply_path.argtypes = [_vp]
 _lib.tca_operator_cg_engine.argtypes = [_vp]
 _lib.tca_operator_cg_fused_step.argtypes = [_vp]
 _lib.tca_operator_cg_fused_step.restype = ctypes.c_int
+_lib.tca_operator_cg_deferred_x.argtypes = [_vp]
+_lib.tca_operator_cg_deferred_x.restype = ctypes.c_int
 _lib.tca_pcg_solve.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int32, _vp, _vp]
 _lib.tca_precond_apply.argtypes = [_vp, _vp, _vp, _vp]
 _lib.tca_cgsr_solve.argtypes = [_vp, _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int32, _vp, _vp]
@@ -310,6 +312,14 @@ class Operator:
         """Which engine cg_solve runs: 'tiny' (one block, tca_tiny.cu), 'grid' (one
         cooperative grid, tca_grid.cu) or 'general' (graph-replayed kernels)."""
         return {1: "tiny", 2: "grid"}.get(_lib.tca_operator_cg_engine(self._h), "general")
+
+    @property
+    def cg_deferred_x(self):
+        """True when CG / PCG solves defer the x update into the next apply (a
+        streaming warp beside the operator), False otherwise, None
+        before the first solve."""
+        v = _lib.tca_operator_cg_deferred_x(self._h)
+        return None if v < 0 else bool(v)
 
     @property
     def cg_fused_step(self):

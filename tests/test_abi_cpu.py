@@ -82,6 +82,7 @@ def test_null_operator_calls_fail_cleanly():
     assert tca._lib.tca_operator_create_gram(None, 3, None, None, None, 1.0, 0, None, None) == tca.ERR_INVALID_ARG
     assert tca._lib.tca_solve_host_batch(None, 1, None, None, 0.0, 1, None, None) == tca.ERR_INVALID_ARG
     assert tca._lib.tca_operator_cg_fused_step(None) == -1
+    assert tca._lib.tca_operator_cg_deferred_x(None) == -1
     assert tca._lib.tca_operator_cg_engine(None) == -1
     tca._lib.tca_operator_destroy(None)
 

@@ -37,13 +37,18 @@ def make_op(tca, A, L, lam, dt, b1=True):
 
 
 def solve(op, b, dt, b1, how="cg", **kw):
+    # the general (graph-chunked) engine: the single-block and grid engines take
+    # small shapes otherwise, and B1' is a step of the general engine only
+    env = {"TCA_GRID": "0", "TCA_TINY": "0"}
     if b1:
-        os.environ["TCA_B1"] = "1"
+        env["TCA_B1"] = "1"
+    os.environ.update(env)
     try:
         fn = op.cg_solve if how == "cg" else op.pcg_solve
         return fn(dev(b, dt), **kw)
     finally:
-        os.environ.pop("TCA_B1", None)
+        for k in env:
+            os.environ.pop(k, None)
 
 
 def expect_b1(n, dt):
