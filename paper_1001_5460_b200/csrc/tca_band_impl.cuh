@@ -910,7 +910,12 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             // ---- pass A: G2 (all halo-extended columns), lambda R2 (interior columns)
             if (live && !(dbg & 4)) {
 #pragma unroll 1
-                for (int c = tid; c < W; c += NTHR) {
+                for (int t = tid; t < W; t += NTHR) {
+                    // interior columns (G2 and R2) on the first threads, the halo
+                    // columns (G2 only) after them: the heavy columns fill warps
+                    // 0-3, one per scheduler, instead of doubling up on one
+                    int c = t;
+                    if constexpr (W <= NTHR) c = t < WI ? 3 * C::S3 + t : (t < WI + 3 * C::S3 ? t - WI : t);
                     T v[PR];
                     if (FU && !(dbg & 2048)) {   // P_new := D + beta P_old on the staged slab (halo included)
 #pragma unroll
