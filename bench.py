@@ -353,7 +353,9 @@ def run_tca(args):
                 "frac": achieved / hbm, "traffic": traffic,
                 "kernel": "fused banded operator apply q = M p (band_apply_kernel) inside CG",
                 "bytes_per_launch": apply_bytes, "us_per_launch": apply_us,
-                "launches_timed": state["apply_cnt"], "peak_source": peak_src}
+                "launches_timed": state["apply_cnt"], "peak_source": peak_src,
+                "timing": "CUDA event pairs on the launching stream around the applies of every 16th CG "
+                          "iteration of each captured graph chunk and every eager one, over the timed region"}
 
     # phase breakdown of one extra step (outside the timed region)
     barrier()

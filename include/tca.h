@@ -408,9 +408,12 @@ tca_status tca_forward_model(const tca_operator *op, const void *x, void *ydata,
 /*
  * Timing instrumentation (measurement only; off by default).  When enabled,
  * tca_cg_solve and tca_apply record a CUDA event pair on `stream` around
- * every operator-apply launch (inside CG's graph chunks: external event
- * nodes of the captured graph, two alternating instances so that one is read
- * while the other runs); tca_operator_get_timing returns the summed device
+ * the operator-apply launches (eager launches: every one; inside CG's graph
+ * chunks of 32 iterations: the applies of iterations 0 and 16 of each chunk,
+ * as external event nodes of the captured graph -- a node pair costs ~20 us
+ * of replay time, so timing every apply would slow the solve it measures --
+ * two alternating instances so that one is read while the other runs);
+ * tca_operator_get_timing returns the summed device
  * time (ms) and the number of timed applies since the last reset.
  */
 tca_status tca_operator_set_timing(tca_operator *op, int enable);

@@ -488,6 +488,7 @@ template <typename Fn>
 static tca_status timed_call(tca_operator *op, cudaStream_t s, Fn &&fn)
 {
     if (!op->timing) return fn();
+    if (op->capturing && !op->cap_ev) return fn();   // not a sampled iteration of the chunk
     if (op->cap_ev) {
         cudaEvent_t a, b;
         TCA_CUDA_TRY(cudaEventCreate(&a));
@@ -758,6 +759,7 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
 // dominates the small configs.  Later kernels of a converged solve are no-ops
 // (device `done` flag), so the returned x is exactly x_k.
 constexpr int kGraphChunk = 32;
+constexpr int kTimingStride = 16;   // timed iterations per captured chunk: every 16th
 
 static void destroy_graphs(tca_operator *op)
 {
@@ -779,12 +781,19 @@ template <typename T>
 static tca_status capture_chunk(tca_operator *op, T *x, int g)
 {
     cudaGraph_t graph = nullptr;
-    op->cap_ev = op->timing ? &op->gev[g] : nullptr;
     TCA_CUDA_TRY(cudaStreamBeginCapture(op->gstream, cudaStreamCaptureModeThreadLocal));
     tca_status st = TCA_OK;
     const int64_t k0 = g_launches.load();
-    for (int i = 0; i < kGraphChunk && st == TCA_OK; ++i) st = cg_iteration<T>(op, x, op->gstream);
+    // timing samples the applies of every kTimingStride-th iteration of the
+    // chunk: an external event node pair costs ~20 us of replay time, which
+    // timing every apply would add to the solve it measures
+    op->capturing = true;
+    for (int i = 0; i < kGraphChunk && st == TCA_OK; ++i) {
+        op->cap_ev = op->timing && i % kTimingStride == 0 ? &op->gev[g] : nullptr;
+        st = cg_iteration<T>(op, x, op->gstream);
+    }
     cudaError_t e = cudaStreamEndCapture(op->gstream, &graph);
+    op->capturing = false;
     op->cap_ev = nullptr;
     // captured launches run at each replay, not now (single-threaded per operator)
     op->gkernels[g] = g_launches.load() - k0;

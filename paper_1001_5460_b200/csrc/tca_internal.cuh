@@ -235,7 +235,8 @@ struct tca_operator {
     int64_t gkernels[2] = {0, 0};        // kernel launches captured in instance g (added per replay)
     bool gpend[2] = {false, false};      // instance g has launched and its events are unharvested
     std::vector<cudaEvent_t> gev[2];     // captured (external) event pairs of instance g
-    std::vector<cudaEvent_t> *cap_ev = nullptr;   // event list being captured into
+    std::vector<cudaEvent_t> *cap_ev = nullptr;   // event list being captured into (sampled iteration)
+    bool capturing = false;              // a chunk is being captured (applies outside the sample run plain)
     cudaEvent_t gfork = nullptr, gjoin = nullptr;
     // sharded CG: the halo of p on a side stream under the interior p update
     cudaStream_t hstream = nullptr;
