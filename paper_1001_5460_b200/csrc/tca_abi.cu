@@ -595,6 +595,22 @@ static tca_status cg_reduce(tca_operator *op, int which, const double *part, int
     return TCA_OK;
 }
 
+// R := R - alpha Q and its <r, r> partials, then finaliser 2 (rho1, stop
+// test, beta): single GPU inside cg_update_r's last CTA (tca_finalize.cuh: one
+// launch and one graph-node gap less per iteration; TCA_NO_FUSED_FIN=1
+// measures the separate kernel), sharded through cg_reduce's all-reduce
+template <typename T>
+static tca_status update_r_reduce(tca_operator *op, T *r, const T *q, cudaStream_t s)
+{
+    static const bool no_fin = getenv("TCA_NO_FUSED_FIN") != nullptr;
+    if (!op->transport && !no_fin) {
+        launch_cg_update_r<T>(r, q, op->N, op->sc, op->part, s, true, op->hist);
+        return TCA_OK;
+    }
+    launch_cg_update_r<T>(r, q, op->N, op->sc, op->part, s);
+    return cg_reduce(op, 2, op->part, kRedBlocks, s);
+}
+
 static tca_status halo_p(tca_operator *op, cudaStream_t s)
 {
     if (!op->transport) return TCA_OK;
@@ -680,8 +696,7 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
         TCA_TRY(timed_call(op, s, [&] { return launch_fused_b1(op, pold, pnew, d, q, x, op->part, s); }));
         op->pcur ^= 1;
         TCA_TRY(cg_reduce(op, 1, op->part, op->band_grid_fu, s));     // alpha
-        launch_cg_update_r<T>(r, q, op->N, op->sc, op->part, s);       // R := R - alpha*Q, R+*R
-        TCA_TRY(cg_reduce(op, 2, op->part, kRedBlocks, s));            // rho1 (PCG: R+*R), stop, beta
+        TCA_TRY(update_r_reduce<T>(op, r, q, s));       // R := R - alpha*Q, R+*R; rho1 (PCG: R+*R), stop, beta
         if (op->solver == 1) {
             T *z = (T *)op->z;
             TCA_TRY(apply_precond<T>(op, r, z, done, s));              // Z := P^-1 R
@@ -694,8 +709,7 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
         T *pc = (T *)(op->pcur ? op->p2 : op->p_own), *pp = (T *)(op->pcur ? op->p_own : op->p2);
         TCA_TRY(timed_call(op, s, [&] { return launch_fused_dx(op, pc, q, x, pp, op->part, s); }));
         TCA_TRY(cg_reduce(op, 1, op->part, op->band_grid_dx, s));   // alpha
-        launch_cg_update_r<T>(r, q, op->N, op->sc, op->part, s);     // R := R - alpha*Q, R+*R
-        TCA_TRY(cg_reduce(op, 2, op->part, kRedBlocks, s));          // rho1 (PCG: R+*R), stop, beta
+        TCA_TRY(update_r_reduce<T>(op, r, q, s));     // R := R - alpha*Q, R+*R; rho1 (PCG: R+*R), stop, beta
         const T *d = r;
         if (op->solver == 1) {
             T *z = (T *)op->z;
@@ -709,16 +723,20 @@ static tca_status cg_iteration(tca_operator *op, T *x, cudaStream_t s)
         return TCA_OK;   // C += alpha P: by the next apply (or after the loop)
     }
     static const bool no_fused_dot = getenv("TCA_NO_FUSED_DOT") != nullptr;   // measurement switch
+    static const bool no_fin = getenv("TCA_NO_FUSED_FIN") != nullptr;   // measurement switch
     if (fused_used(op, pe, q) && !no_fused_dot) {
-        TCA_TRY(timed_apply(op, pe, q, done, s, op->part));           // Q := A*(P*D), P+*Q in the epilogue
-        TCA_TRY(cg_reduce(op, 1, op->part, op->band_grid, s));       // alpha
+        op->band_fin_req = !no_fin;                                   // alpha in the apply's last CTA
+        op->band_fin_done = false;
+        const tca_status st = timed_apply(op, pe, q, done, s, op->part);   // Q := A*(P*D), P+*Q in the epilogue
+        op->band_fin_req = false;
+        TCA_TRY(st);
+        if (!op->band_fin_done) TCA_TRY(cg_reduce(op, 1, op->part, op->band_grid, s));   // alpha
     } else {
         TCA_TRY(timed_apply(op, pe, q, done, s));                     // Q := A*(P*D)
         launch_dot_partials<T>(p, q, op->N, op->part, done, s);      // P+*Q
         TCA_TRY(cg_reduce(op, 1, op->part, kRedBlocks, s));          // alpha
     }
-    launch_cg_update_r<T>(r, q, op->N, op->sc, op->part, s);         // R := R - alpha*Q, R+*R
-    TCA_TRY(cg_reduce(op, 2, op->part, kRedBlocks, s));              // rho1 (PCG: R+*R), stop, beta
+    TCA_TRY(update_r_reduce<T>(op, r, q, s));         // R := R - alpha*Q, R+*R; rho1 (PCG: R+*R), stop, beta
     const T *d = r;
     if (op->solver == 1) {
         T *z = (T *)op->z;

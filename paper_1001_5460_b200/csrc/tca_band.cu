@@ -457,6 +457,11 @@ tca_status launch_t(const tca_operator *op, const void *x, void *y, const int32_
     p->y = (T *)y;
     p->done = done;
     p->pq_part = pq_part;
+    // CG's finaliser 1 in the last CTA: the one-pass kernel (MODE 0) with
+    // 256-thread CTAs (n4 <= 16, tca_finalize.cuh's block size), single GPU
+    op->band_fin_done = op->band_fin_req && pq_part && !op->band_v2 && !op->transport && op->n[3] <= 16;
+    p->fin_sc = op->band_fin_done ? op->sc : nullptr;
+    p->fin_hist = op->hist;
     {
         static const char *e = getenv("TCA_BAND_DEBUG");
         p->dbg = e ? atoi(e) : 0;

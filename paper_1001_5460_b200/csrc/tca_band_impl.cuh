@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 
 #include "tca_internal.cuh"
+#include "tca_finalize.cuh"
 
 #include <type_traits>
 
@@ -75,6 +76,8 @@ struct ParamsBase {
     T *y;
     const int32_t *done;
     double *pq_part;       // optional: per-CTA partial <x, y> of the emitted outputs (CG's <p, q>)
+    CgScalars *fin_sc;     // optional (with pq_part; MODE 0, 256-thread CTAs): the last CTA runs
+    double *fin_hist;      // CG's finaliser 1 (alpha := rho / <p, q>, tca_finalize.cuh)
     int n1, n2, n3, tiles3;   // n1: output slabs (local rows of a sharded operator)
     int xoff, nin;            // input slab j lives at slab j + xoff of an input of nin slabs (ghosts)
     int off3, off2, off1;     // record offsets (rows) of the mode-3/2/1 tables; mode 4 at 0
@@ -725,9 +728,8 @@ __device__ __forceinline__ void cta_sync()
 // MODE: 0 the apply; 1 the fused CG step B1' (FuArgs: C, P_new); 2 the apply
 // with the deferred C update (an extra streaming warp; FuArgs: C, P_prev as pn)
 template <typename T, int N4, typename PA, int MODE>
-__global__ void __launch_bounds__(Cfg<T, N4>::NTHR + (MODE == 2 ? 32 : 0), Cfg<T, N4>::MINB)
-band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict__ ymp,
-                  const __grid_constant__ PA a, const CUtensorMap *__restrict__ rmp, const __grid_constant__ FuArgs<T> f)
+__device__ __forceinline__ void band_apply_body(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict__ ymp,
+                                                const PA &a, const CUtensorMap *__restrict__ rmp, const FuArgs<T> &f)
 {
     using C = Cfg<T, N4>;
     constexpr bool FU = MODE == 1;
@@ -752,7 +754,11 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             return;
         }
     } else {
-        if (a.done && *a.done) return;
+        if (a.done && *a.done) {
+            if constexpr (MODE == 0 && NTHR == kRedThreads)   // finaliser 1 of a stopped solve: no x update
+                if (a.fin_sc && blockIdx.x == 0 && threadIdx.x == 0) a.fin_sc->xupd = 0;
+            return;
+        }
     }
     if (dbg & 16) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1043,8 +1049,19 @@ band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__rest
             for (int w = 0; w < NTHR / 32; ++w) t += red[w];
             a.pq_part[blockIdx.x] = t;
         }
+        if constexpr (MODE == 0 && NTHR == kRedThreads)
+            if (a.fin_sc) fin_last_cta(1, 0, a.pq_part, a.fin_sc, a.fin_hist, red);   // alpha in the last CTA
     }
 }
+
+template <typename T, int N4, typename PA, int MODE>
+__global__ void __launch_bounds__(Cfg<T, N4>::NTHR + (MODE == 2 ? 32 : 0), Cfg<T, N4>::MINB)
+band_apply_kernel(const CUtensorMap *__restrict__ xmp, const CUtensorMap *__restrict__ ymp,
+                  const __grid_constant__ PA a, const CUtensorMap *__restrict__ rmp, const __grid_constant__ FuArgs<T> f)
+{
+    band_apply_body<T, N4, PA, MODE>(xmp, ymp, a, rmp, f);
+}
+
 
 // ---------------------------------------------------------------- host side
 template <typename T, int N4, typename PA, int MODE>
@@ -1057,11 +1074,11 @@ tca_status launch_n4(const tca_operator *op, const PA &prm, cudaStream_t s, cons
         return fail(TCA_ERR_INVALID_ARG, "fused CG step: shape does not fit shared memory");
     } else {
         constexpr size_t smem = FU ? C::smem_fu : C::smem_bytes;
-        TCA_TRY(set_max_dynamic_smem((const void *)band_apply_kernel<T, N4, PA, MODE>, smem));
+        auto kern = band_apply_kernel<T, N4, PA, MODE>;
+        TCA_TRY(set_max_dynamic_smem((const void *)kern, smem));
         count_launch();
         const int grid = MODE == 1 ? op->band_grid_fu : MODE == 2 ? op->band_grid_dx : op->band_grid;
-        band_apply_kernel<T, N4, PA, MODE>
-            <<<(unsigned)grid, C::NTHR + (MODE == 2 ? 32 : 0), smem, s>>>(xm, ym, prm, rm, fa);
+        kern<<<(unsigned)grid, C::NTHR + (MODE == 2 ? 32 : 0), smem, s>>>(xm, ym, prm, rm, fa);
         TCA_CUDA_TRY(cudaGetLastError());
         return TCA_OK;
     }

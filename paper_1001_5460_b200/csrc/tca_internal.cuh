@@ -72,6 +72,8 @@ struct CgScalars {
     int32_t pad;
     double ref;      // stop reference: rtol is relative to <b, b> (= rho0 when x0 = 0; reading Z28)
     double red[10];  // reduced dot products (stage sum -> all-reduce -> stage apply); 8, 9: |b - Mx|^2, |b|^2
+    uint32_t fin_cnt[2];   // CTA arrival counters of the finalisers fused into their producer kernels
+                           // (0: the band apply's alpha, 1: cg_update_r's rho1); zero between launches
 };
 
 // Exchange steps of a mode-1 sharded operator (tca_dist.cu).
@@ -222,6 +224,8 @@ struct tca_operator {
     int pcur = 0;                        // 0: P in p_own, 1: P in p2
     int apply_path = 0;                  // 0 = generic multi-pass, 1 = fused banded, 2 = Kronecker-sum stencil
     int band_v2 = 0;                     // fused banded apply: 1 = warp-specialised kernel (tca_band2.cuh)
+    mutable bool band_fin_req = false;   // next fused apply with <p, q> partials: run CG's finaliser 1 in its last CTA
+    mutable bool band_fin_done = false;  // ... and the last launch did (else the caller runs cg_reduce)
     // CUDA-graph replay of CG chunks
     // (two instances when timing: each carries its own captured event pairs, so
     // one can be harvested while the other runs)
@@ -321,7 +325,10 @@ tca_status launch_precond_sweep(const tca_operator *op, int d, const T *src, T *
 // dense n x n matrix in the operator's dtype (tca_abi.cu)
 tca_status make_dense_mat(tca_dtype dt, const std::vector<double> &M, int n, BandMat *out, size_t *bytes);
 template <typename T>
-void launch_cg_update_r(T *r, const T *q, int64_t N, const CgScalars *sc, double *part, cudaStream_t s);
+// fin: run finaliser 2 (rho1, stop test, beta) in the kernel's last CTA
+// (single GPU; a sharded solve all-reduces the partials first)
+void launch_cg_update_r(T *r, const T *q, int64_t N, CgScalars *sc, double *part, cudaStream_t s,
+                        bool fin = false, double *hist = nullptr);
 // d = b - q: r and p (either may be NULL) receive d; part_dd / part_bb the
 // per-block partials of <d, d> and <b, b> (warm start R := B - A*C, and the
 // true residual of the report)

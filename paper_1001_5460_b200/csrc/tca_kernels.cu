@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "tca_internal.cuh"
+#include "tca_finalize.cuh"
 
 namespace tca {
 
@@ -926,7 +927,8 @@ dot_partials_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t N,
 // the apply read, so the iterates are exactly Fig. 2's.
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads)
-cg_update_r_kernel(T *__restrict__ r, const T *__restrict__ q, int64_t N, const CgScalars *sc, double *part)
+cg_update_r_kernel(T *__restrict__ r, const T *__restrict__ q, int64_t N, CgScalars *sc, double *part, int fin,
+                   double *hist)
 {
     if (sc->done) return;
     using V = typename Vec<T>::V;
@@ -952,6 +954,10 @@ cg_update_r_kernel(T *__restrict__ r, const T *__restrict__ q, int64_t N, const 
     }
     const double s = block_sum(acc);
     if (threadIdx.x == 0) part[blockIdx.x] = s;
+    if (fin) {   // rho1, stop test, beta in the last CTA (tca_finalize.cuh)
+        __shared__ double red[kRedThreads / 32 + 1];
+        fin_last_cta(2, 1, part, sc, hist, red);
+    }
 }
 
 // C := C + alpha*P*D when this iteration's alpha is valid (sc->xupd), then
@@ -1084,10 +1090,11 @@ void launch_dot_partials(const T *a, const T *b, int64_t N, double *part,
 }
 
 template <typename T>
-void launch_cg_update_r(T *r, const T *q, int64_t N, const CgScalars *sc, double *part, cudaStream_t s)
+void launch_cg_update_r(T *r, const T *q, int64_t N, CgScalars *sc, double *part, cudaStream_t s, bool fin,
+                        double *hist)
 {
     count_launch();
-    cg_update_r_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, q, N, sc, part);
+    cg_update_r_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, q, N, sc, part, fin ? 1 : 0, hist);
 }
 
 template <typename T>
@@ -1128,60 +1135,7 @@ cg_finalize_kernel(int which, const double *__restrict__ part, int nparts, CgSca
         if (threadIdx.x != 0) return;
         s = sc->red[which];
     }
-    if (which == 8) {                      // warm start: stop reference <b, b> (reading Z28)
-        sc->ref = s;
-        return;
-    }
-    if (which == 0) {                      // rho := R+*R
-        sc->rho = s;
-        sc->rho0 = s;
-        sc->ref = s;
-        sc->rr = s;
-        sc->iters = 0;
-        sc->converged = 0;
-        sc->status = TCA_OK;
-        sc->done = 0;
-        sc->xupd = 0;
-        if (hist) hist[0] = s;
-        if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; }
-        else if (s == 0.0) { sc->converged = 1; sc->done = 1; }
-        else if (sc->max_iters <= 0) { sc->done = 1; if (sc->rtol2 > 0.0) sc->status = TCA_NOT_CONVERGED; }
-    } else if (which == 1) {               // alpha := rho / (P+*Q)
-        sc->pq = s;
-        sc->xupd = 0;
-        if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; }
-        else if (!(s > 0.0)) { sc->status = TCA_ERR_BREAKDOWN; sc->done = 1; }
-        else { sc->alpha = sc->rho / s; sc->xupd = 1; }
-    } else if (which == 2) {               // rho1 := R+*R (PCG: rr); stop test; CG: beta
-        const int k = sc->iters + 1;
-        sc->iters = k;
-        sc->rr = s;
-        if (hist) hist[k] = s;
-        if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; if (!sc->pcg) sc->rho = s; return; }
-        if (s == 0.0) { sc->converged = 1; sc->done = 1; if (!sc->pcg) sc->rho = s; return; }   // Z12
-        if (sc->rtol2 > 0.0 && s <= sc->rtol2 * sc->ref) {                                    // Z1, Z2, Z28
-            sc->converged = 1; sc->done = 1; if (!sc->pcg) sc->rho = s; return;
-        }
-        if (k >= sc->max_iters) {
-            sc->done = 1;
-            if (!sc->pcg) sc->rho = s;
-            if (sc->rtol2 > 0.0) sc->status = TCA_NOT_CONVERGED;
-            return;
-        }
-        if (!sc->pcg) {
-            sc->beta = s / sc->rho;
-            sc->rho = s;
-        }
-    } else if (which == 3) {               // PCG: rho1 := R+*Z; beta
-        if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
-        if (!(s > 0.0)) { sc->status = TCA_ERR_BREAKDOWN; sc->done = 1; return; }
-        sc->beta = s / sc->rho;
-        sc->rho = s;
-    } else {                               // 4, PCG start: rho := R+*Z (R = B, Z = P^-1 B)
-        if (!isfinite(s)) { sc->status = TCA_ERR_NONFINITE; sc->done = 1; return; }
-        if (!(s > 0.0)) { sc->status = TCA_ERR_BREAKDOWN; sc->done = 1; return; }
-        sc->rho = s;
-    }
+    cg_finalize_scalars(which, s, sc, hist);   // tca_finalize.cuh
 }
 
 // Single-reduction CG finaliser: gamma = R+*R (update-kernel partials) and
@@ -1433,8 +1387,8 @@ void launch_cg_finalize(int which, const double *part, int nparts, CgScalars *sc
                                    double *, cudaStream_t);                               \
     template void launch_dot_partials<T>(const T *, const T *, int64_t, double *,         \
                                          const int32_t *, cudaStream_t);                  \
-    template void launch_cg_update_r<T>(T *, const T *, int64_t, const CgScalars *,       \
-                                        double *, cudaStream_t);                          \
+    template void launch_cg_update_r<T>(T *, const T *, int64_t, CgScalars *, double *,   \
+                                        cudaStream_t, bool, double *);                    \
     template void launch_cg_update_xp<T>(T *, T *, const T *, int64_t, const CgScalars *, \
                                          cudaStream_t);                                   \
     template void launch_cg_update_p<T>(T *, const T *, const T *, int64_t,               \
