@@ -97,6 +97,21 @@ def workload_name(cfg, dtype, iters, rtol=None, solver="cg"):
     return f"config {cfg.index}: {n} unknowns {dtype}, data {m}, lambda {cfg.lam:g}, {stop}"
 
 
+def fit_config(cfg, dtype, iters, rtol, solver, world):
+    """The `config` object of the fit workload's line -- identical in the GPU arm
+    and the reference (oracle) arm, which times a bounded sample of the same
+    workload (described in its cpu_baseline.sample)."""
+    esize = 8 if dtype == "f64" else 4
+    return {"workload": workload_name(cfg, dtype, iters, rtol, solver), "solver": solver, "config_index": cfg.index,
+            "unknowns": cfg.N, "data_points": cfg.Mdata, "cg_iters_per_step": iters,
+            "step": "tca_operator_create + tca_rhs + tca_cg_solve (or tca_pcg_solve) + tca_operator_destroy",
+            "l2": ("inputs larger than L2 (each vector %.1f MB, y %.1f MB)" if cfg.N * esize * 5 > 126e6 else
+                   "vectors L2-resident (each vector %.1f MB, y %.1f MB; 126 MB L2)") % (
+                cfg.N * esize / 2**20, cfg.Mdata * esize / 2**20),
+            "parallelism": "single GPU" if world == 1 else
+            f"mode-1 sharding over {world} GPUs (NCCL halo + all-reduce)"}
+
+
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -187,6 +202,8 @@ def run_reference(args):
         return 0
     cfg = synth.CONFIGS[args.config]
     iters = args.iters or cfg.max_iters
+    rtol = cfg.rtol if args.rtol is None else args.rtol
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     import oracle
     A, L = synth.mode_matrices(cfg)
     op = oracle.Operator(A, L, cfg.lam)
@@ -211,8 +228,9 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, args.dtype, iters)},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",   # the oracle computes in fp64
+            "data": "synthetic (seeded; cubic B-spline A_d)",
+            "config": fit_config(cfg, args.dtype, iters, rtol, args.solver, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(),
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -504,14 +522,7 @@ def run_tca(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": dtype, "data": "synthetic (seeded counter RNG on device; cubic B-spline A_d)",
-        "config": {"workload": workload_name(cfg, dtype, iters, rtol, args.solver), "solver": args.solver, "config_index": cfg.index,
-                   "unknowns": cfg.N, "data_points": cfg.Mdata, "cg_iters_per_step": iters,
-                   "step": "tca_operator_create + tca_rhs + tca_cg_solve (or tca_pcg_solve) + tca_operator_destroy",
-                   "l2": ("inputs larger than L2 (each vector %.1f MB, y %.1f MB)" if cfg.N * esize * 5 > 126e6 else
-                          "vectors L2-resident (each vector %.1f MB, y %.1f MB; 126 MB L2)") % (
-                       cfg.N * esize / 2**20, cfg.Mdata * esize / 2**20),
-                   "parallelism": "single GPU" if world == 1 else
-                   f"mode-1 sharding over {world} GPUs (NCCL halo + all-reduce)"},
+        "config": fit_config(cfg, dtype, iters, rtol, args.solver, world),
         "roofline": roofline,
         "apply": apply_info,
         "cpu_baseline": cpu,
