@@ -18,6 +18,23 @@ namespace tca {
 
 std::atomic<int64_t> g_launches{0};
 
+// L2 hand-off between the CG vector kernels (default; TCA_L2REV=0 measures the
+// plain streaming form): cg_update_r sweeps the vector from its end (the
+// apply's last output slabs, high i1, are the ones still in L2) and keeps R
+// L2-normal (Q evict-first), so the R it wrote last (low indices) is still in
+// L2 when cg_update_xp sweeps from the start and reads it L2-normal.
+// Config 3 CG: f64 597.9 -> 592.3 us, f32 369.4 -> 362.2 us per iteration
+// (profiles/r02_l2_handoff_probe.txt).  The <r, r> partials are summed in the
+// sweep's (fixed) order: deterministic.
+static int l2_handoff()
+{
+    static const int on = [] {
+        const char *e = getenv("TCA_L2REV");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    return on;
+}
+
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ double warp_sum(double v)
 {
@@ -928,7 +945,7 @@ dot_partials_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t N,
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads)
 cg_update_r_kernel(T *__restrict__ r, const T *__restrict__ q, int64_t N, CgScalars *sc, double *part, int fin,
-                   double *hist)
+                   double *hist, int rev)
 {
     if (sc->done) return;
     using V = typename Vec<T>::V;
@@ -941,10 +958,18 @@ cg_update_r_kernel(T *__restrict__ r, const T *__restrict__ q, int64_t N, CgScal
         nv = N / VW;
         V *rv = reinterpret_cast<V *>(r);
         const V *qv = reinterpret_cast<const V *>(q);
-        for (int64_t i = tid; i < nv; i += nth) {
-            const V rn = vaxpy(__ldcs(rv + i), -alpha, __ldcs(qv + i));   // R := R - alpha*Q
-            __stcs(rv + i, rn);
-            acc += vdot(rn, rn);                                           // rho1 := R+*R (partials)
+        if (rev) {   // L2 hand-off (see launch_cg_update_r): last slabs first, R kept in L2 for cg_update_xp
+            for (int64_t i = nv - 1 - tid; i >= 0; i -= nth) {
+                const V rn = vaxpy(__ldcg(rv + i), -alpha, __ldcs(qv + i));
+                __stcg(rv + i, rn);
+                acc += vdot(rn, rn);
+            }
+        } else {
+            for (int64_t i = tid; i < nv; i += nth) {
+                const V rn = vaxpy(__ldcs(rv + i), -alpha, __ldcs(qv + i));   // R := R - alpha*Q
+                __stcs(rv + i, rn);
+                acc += vdot(rn, rn);                                           // rho1 := R+*R (partials)
+            }
         }
     }
     for (int64_t i = nv * VW + tid; i < N; i += nth) {
@@ -964,7 +989,8 @@ cg_update_r_kernel(T *__restrict__ r, const T *__restrict__ q, int64_t N, CgScal
 // P := R + beta*P unless the solve stopped at this iteration.
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads)
-cg_update_xp_kernel(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ r, int64_t N, const CgScalars *sc)
+cg_update_xp_kernel(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ r, int64_t N, const CgScalars *sc,
+                    int keep_r)
 {
     if (!sc->xupd) return;
     using V = typename Vec<T>::V;
@@ -980,7 +1006,7 @@ cg_update_xp_kernel(T *__restrict__ x, T *__restrict__ p, const T *__restrict__ 
         const V *rv = reinterpret_cast<const V *>(r);
         if (upd_p) {
             for (int64_t i = tid; i < nv; i += nth) {
-                const V pi = __ldcs(pv + i), xi = __ldcs(xv + i), ri = __ldcs(rv + i);
+                const V pi = __ldcs(pv + i), xi = __ldcs(xv + i), ri = keep_r ? __ldcg(rv + i) : __ldcs(rv + i);
                 __stcs(xv + i, vaxpy(xi, alpha, pi));   // C := C + alpha*P*D
                 __stcs(pv + i, vaxpy(ri, beta, pi));    // P := R + beta*P
             }
@@ -1094,7 +1120,7 @@ void launch_cg_update_r(T *r, const T *q, int64_t N, CgScalars *sc, double *part
                         double *hist)
 {
     count_launch();
-    cg_update_r_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, q, N, sc, part, fin ? 1 : 0, hist);
+    cg_update_r_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(r, q, N, sc, part, fin ? 1 : 0, hist, l2_handoff());
 }
 
 template <typename T>
@@ -1108,7 +1134,7 @@ template <typename T>
 void launch_cg_update_xp(T *x, T *p, const T *r, int64_t N, const CgScalars *sc, cudaStream_t s)
 {
     count_launch();
-    cg_update_xp_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(x, p, r, N, sc);
+    cg_update_xp_kernel<T><<<kRedBlocks, kRedThreads, 0, s>>>(x, p, r, N, sc, l2_handoff());
 }
 
 // ---------------------------------------------------------------- finalisers
