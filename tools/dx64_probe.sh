@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment record: the variant this measured was reverted; see its log under profiles/ and DESIGN.md 6.3)
 # fp64 deferred-x apply (MODE 2 at 112 registers) vs the default iteration, config 3
 mkdir -p gpurun_out/dx64
 for i in 1 2; do

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment record: the variant this measured was reverted; see its log under profiles/ and DESIGN.md 6.3)
 # programmatic dependent launch of the CG kernel chain vs plain launches (TCA_PDL=0): config 3
 # CG per iteration; then the GPU parity suite and the f64 bench line
 mkdir -p gpurun_out/pdl

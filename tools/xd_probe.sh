@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment record: the variant this measured was reverted; see its log under profiles/ and DESIGN.md 6.3)
 # deferred x update over a ring of P buffers (TCA_XD=0|2|4) and programmatic
 # dependent launch (TCA_PDL=0|1): config 3 CG per iteration, the XD tests, then
 # the full GPU suite
