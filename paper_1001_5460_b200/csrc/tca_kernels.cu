@@ -24,7 +24,9 @@ std::atomic<int64_t> g_launches{0};
 // L2-normal (Q evict-first), so the R it wrote last (low indices) is still in
 // L2 when cg_update_xp sweeps from the start and reads it L2-normal.
 // Config 3 CG: f64 597.9 -> 592.3 us, f32 369.4 -> 362.2 us per iteration
-// (profiles/r02_l2_handoff_probe.txt).  The <r, r> partials are summed in the
+// (profiles/r02_l2_handoff_probe.txt); with 4 vectors in flight per thread in
+// the reverse sweep f64 577.4 -> 569.1 us, f32 361.4 -> 356.9 us
+// (profiles/r02_unroll_probe.txt).  The <r, r> partials are summed in the
 // sweep's (fixed) order: deterministic.
 static int l2_handoff()
 {
@@ -958,8 +960,21 @@ cg_update_r_kernel(T *__restrict__ r, const T *__restrict__ q, int64_t N, CgScal
         nv = N / VW;
         V *rv = reinterpret_cast<V *>(r);
         const V *qv = reinterpret_cast<const V *>(q);
-        if (rev) {   // L2 hand-off (see launch_cg_update_r): last slabs first, R kept in L2 for cg_update_xp
-            for (int64_t i = nv - 1 - tid; i >= 0; i -= nth) {
+        if (rev) {   // L2 hand-off (see l2_handoff): last slabs first, R kept in L2 for cg_update_xp;
+                     // 4 vectors of R and Q in flight per thread (f64 CG 577.4 -> 569.1 us per iteration)
+            int64_t i = nv - 1 - tid;
+            for (; i - 3 * nth >= 0; i -= 4 * nth) {
+                V ra[4], qa[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) { ra[u] = __ldcg(rv + i - u * nth); qa[u] = __ldcs(qv + i - u * nth); }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const V rn = vaxpy(ra[u], -alpha, qa[u]);
+                    __stcg(rv + i - u * nth, rn);
+                    acc += vdot(rn, rn);
+                }
+            }
+            for (; i >= 0; i -= nth) {
                 const V rn = vaxpy(__ldcg(rv + i), -alpha, __ldcs(qv + i));
                 __stcg(rv + i, rn);
                 acc += vdot(rn, rn);
