@@ -962,13 +962,17 @@ cg_update_r_kernel(T *__restrict__ r, const T *__restrict__ q, int64_t N, CgScal
         const V *qv = reinterpret_cast<const V *>(q);
         if (rev) {   // L2 hand-off (see l2_handoff): last slabs first, R kept in L2 for cg_update_xp;
                      // 4 vectors of R and Q in flight per thread (f64 CG 577.4 -> 569.1 us per iteration)
+#ifndef TCA_R_UNR
+#define TCA_R_UNR 4   // vectors in flight per thread (2: same within noise, 8: +8 us; profiles/r02_runroll_probe.txt)
+#endif
+            constexpr int U = TCA_R_UNR;
             int64_t i = nv - 1 - tid;
-            for (; i - 3 * nth >= 0; i -= 4 * nth) {
-                V ra[4], qa[4];
+            for (; i - (U - 1) * nth >= 0; i -= U * nth) {
+                V ra[U], qa[U];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) { ra[u] = __ldcg(rv + i - u * nth); qa[u] = __ldcs(qv + i - u * nth); }
+                for (int u = 0; u < U; ++u) { ra[u] = __ldcg(rv + i - u * nth); qa[u] = __ldcs(qv + i - u * nth); }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const V rn = vaxpy(ra[u], -alpha, qa[u]);
                     __stcg(rv + i - u * nth, rn);
                     acc += vdot(rn, rn);
