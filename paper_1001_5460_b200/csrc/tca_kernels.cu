@@ -1058,7 +1058,17 @@ cg_update_p_kernel(T *__restrict__ pn, const T *__restrict__ p, const T *__restr
         nv = N / VW;
         V *pnv = reinterpret_cast<V *>(pn);
         const V *pv = reinterpret_cast<const V *>(p), *dv = reinterpret_cast<const V *>(d);
-        for (int64_t i = tid; i < nv; i += nth) __stcs(pnv + i, vaxpy(__ldcs(dv + i), beta, __ldcs(pv + i)));
+        // D (= R, just written by cg_update_r's reverse sweep) read L2-normal from the
+        // start: the L2 hand-off; 4 vectors of D and P in flight per thread
+        int64_t i = tid;
+        for (; i + 3 * nth < nv; i += 4 * nth) {
+            V da[4], pa[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { da[u] = __ldcg(dv + i + u * nth); pa[u] = __ldcs(pv + i + u * nth); }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) __stcs(pnv + i + u * nth, vaxpy(da[u], beta, pa[u]));
+        }
+        for (; i < nv; i += nth) __stcs(pnv + i, vaxpy(__ldcg(dv + i), beta, __ldcs(pv + i)));
     }
     for (int64_t i = nv * VW + tid; i < N; i += nth) pn[i] = d[i] + beta * p[i];
 }
